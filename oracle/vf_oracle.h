@@ -1,0 +1,97 @@
+/* TEST INFRASTRUCTURE ONLY — the CPU parity oracle.
+ *
+ * A plain-C restatement of the reference's per-frame dense-fusion path
+ * (/root/reference/proj, "voxfuse", the CPU re-implementation of InfiniTAM,
+ * arXiv 1410.0925).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / reference legs may load it; the product library never does.
+ *
+ * Pinning: tests/test_oracle_vs_ref.py checks this restatement bit-for-bit
+ * against the reference's own sources compiled unmodified (oracle/_ref, via
+ * oracle/eigen_shim) and tests/golden/ holds fixtures generated from that
+ * build.  Arithmetic contract: IEEE binary32/binary64, strict left-to-right
+ * reductions, no FMA contraction (-ffp-contract=off).
+ */
+#ifndef VF_ORACLE_H
+#define VF_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same field layout as oracle/ref_driver.cpp's vfr_config (ctypes shares one
+ * mirror for both). */
+typedef struct vfo_config {
+  int voxel_type; /* 1 = VoxelS, 2 = VoxelSRgb */
+  float voxel_size, mu;
+  int max_weight, stop_integrating_at_max;
+  int bucket_count, bucket_size, excess_count, block_count;
+  float near_clip, far_clip;
+  int margin_px, swap_margin_px;
+  int levels, rotation_only_levels, max_iterations, min_valid_points;
+  float icp_dist_threshold, convergence_eps;
+  double max_condition;
+  double fx, fy, cx, cy;
+  int width, height;
+  double rgb_fx, rgb_fy, rgb_cx, rgb_cy;
+  int rgb_width, rgb_height;
+  double rgb_to_depth[12];
+} vfo_config;
+
+typedef struct vfo_stats {
+  int frame, tracking_ok, tracking_iterations, blocks_allocated, allocation_dropped, visible_blocks;
+  double tracking_cost;
+  double pose[12];
+  double ms_tracking, ms_allocation, ms_integration, ms_raycast, ms_total;
+} vfo_stats;
+
+typedef struct vfo_alloc_stats {
+  int requested, allocated, dropped_vba_full, dropped_excess_full;
+} vfo_alloc_stats;
+
+typedef struct vfo_ctx vfo_ctx;
+
+vfo_ctx* vfo_create(const vfo_config* cfg, int tracking);
+void vfo_destroy(vfo_ctx* c);
+/* One frame.  tracking != 0: IPipeline::process_frame semantics
+ * (pipeline_impl.hpp:65-123).  tracking == 0: `pose` (row-major R, t) is the
+ * known world->camera pose and the stages run in pipeline order. */
+int vfo_process(vfo_ctx* c, const float* depth, const uint8_t* rgb, const double* pose, vfo_stats* st);
+
+/* Stage entry points (stage-isolated parity). */
+int vfo_stage_allocate(vfo_ctx* c, const float* depth, const double* pose, vfo_alloc_stats* out);
+int vfo_stage_integrate(vfo_ctx* c, const float* depth, const uint8_t* rgb, const double* pose);
+int vfo_stage_raycast(vfo_ctx* c, const double* pose);
+int vfo_stage_icp(vfo_ctx* c, const float* depth, double* out_pose, int* out_iters, double* out_cost,
+                  int* out_valid);
+
+void vfo_get_pose(const vfo_ctx* c, double* out);
+void vfo_set_pose(vfo_ctx* c, const double* pose);
+int vfo_get_maps(const vfo_ctx* c, float* points, float* normals);
+int vfo_set_maps(vfo_ctx* c, const float* points, const float* normals, const double* render_pose);
+long vfo_export_entries(const vfo_ctx* c, void* out);
+long vfo_export_voxels(const vfo_ctx* c, void* out);
+long vfo_visible_list(const vfo_ctx* c, int* out);
+long vfo_export_ranges(const vfo_ctx* c, float* out);
+long vfo_allocated_blocks(const vfo_ctx* c);
+/* free-stack state: tops and slot arrays (hash_volume.hpp:62-110) */
+void vfo_free_stacks(const vfo_ctx* c, int* vba_top, int* vba_slots, int* excess_top, int* excess_slots);
+uint64_t vfo_digest(const vfo_ctx* c);
+/* last ICP solve trace: per accepted/evaluated iteration the 29 sums */
+long vfo_icp_trace(const vfo_ctx* c, double* out, long max_rows);
+
+/* Free functions. */
+uint32_t vfo_hash_block_pos(int x, int y, int z, uint32_t mask);
+void vfo_depth_pyramid(const float* depth, int w, int h, int levels, float* out);
+void vfo_render_depth(int n_spheres, const double* spheres, int n_planes, const double* planes,
+                      const double* world_to_cam, double fx, double fy, double cx, double cy, int w,
+                      int h, double near_clip, double far_clip, float* out);
+void vfo_render_rgb(int n_spheres, const double* spheres, int n_planes, const double* planes,
+                    const double* world_to_cam, double fx, double fy, double cx, double cy, int w,
+                    int h, double near_clip, double far_clip, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
