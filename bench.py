@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: frames/s of the dense-fusion hot path (ICP + allocation +
+integration + raycast) at 640x480 on B200, plus voxel updates/s.
+
+One step = one frame of the synthetic box-room sequence through the full
+per-frame path (pipeline_impl.hpp:65-123).  Frames are rendered on the GPU
+once, outside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+
+* value: device-resident inputs (vf_process_frame_device), CUDA events on the
+  pipeline's stream around each frame, L2 flushed between frames (outside the
+  per-frame intervals), summed over the K timed frames; max over ranks.
+* e2e: the reference-facing call vf_process_frame with pinned HOST buffers —
+  depth H2D and the stats / pose D2H inside every timed step.
+* roofline: per-stage CUDA events (profiling pass, same frames) for the
+  dominant kernel and for integration.
+* cpu_baseline: the reference's own code (oracle/_ref, shim-built) on the
+  host cores, bounded sample, rank 0 at N=1 only.
+* --impl reference: that CPU reference as the arm of record.
+Under torchrun (N>1) every rank runs an independent replica on its own GPU
+(scaling "weak"); the sharded large-scene configuration is not built yet.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec (alloc+integrate+raycast+ICP) at 640x480; voxel updates/sec"
+UNIT = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--l2-flush-mib", type=int, default=256)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (one process per GPU; torch.distributed for barrier/max)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self, n_expected: int):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo")
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference (CPU) arm
+# ---------------------------------------------------------------------------
+def cpu_reference_run(cfg, n_frames: int, budget_s: float, threads: int = 0):
+    """Time the reference's own pipeline (oracle/_ref) on the host cores.
+    Frames 1.. (tracked) are timed; frame 0 (no tracking) is untimed."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import vf_py
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, trajectory
+
+    if not vf_py.ref_available():
+        return None
+    lib = vf_py.ref_lib()
+    lib.lib.vfr_set_threads(threads if threads > 0 else (os.cpu_count() or 1))
+    cores = int(lib.lib.vfr_get_threads())
+    poses = trajectory(n_frames + 1)
+    vol = vf_py.Volume(lib, cfg, tracking=cfg.tracking)
+    rgb = cfg.voxel_type == 2
+    depth0 = vf_py.render_depth(lib, cfg, poses[0], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+    c0 = vf_py.render_rgb(lib, cfg, poses[0], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) if rgb else None
+    vol.process(depth0, c0, None if cfg.tracking else poses[0])
+    t_total, frames, voxels = 0.0, 0, 0
+    for i in range(1, n_frames + 1):
+        d = vf_py.render_depth(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        c = vf_py.render_rgb(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) if rgb else None
+        t0 = time.perf_counter()
+        st = vol.process(d, c, None if cfg.tracking else poses[i])
+        t_total += time.perf_counter() - t0
+        frames += 1
+        voxels += st.visible_blocks * 512
+        if t_total >= budget_s:
+            break
+    vol.close()
+    return {"fps": frames / t_total, "frames": frames, "seconds": t_total, "cores": cores,
+            "voxel_updates_per_s": voxels / t_total}
+
+
+def run_reference_arm(args, dist: Dist):
+    from paper_1410_0925_b200.scene import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if dist.rank != 0:
+        return
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import vf_py
+
+    if not vf_py.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libvoxfuse_ref.so not built"}))
+        return
+    budget = max(5.0, min(60.0, args.cpu_seconds))
+    frames_each = max(1, min(args.steps, 10))
+    times, vps = [], []
+    res = None
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_reference_run(cfg, 1, budget)  # warm-up: page in, pool spin-up
+    for _ in range(max(1, min(args.steps, 3))):
+        res = cpu_reference_run(cfg, frames_each, budget / 3)
+        times.append(res["fps"])
+        vps.append(res["voxel_updates_per_s"])
+    fps = float(np.mean(times))
+    fx, fy, cx, cy, w, h = cfg.intrinsics
+    sample = (f"{cfg.name}: frames 1..{res['frames']} of the tracked sequence per step (frame 0 untimed), "
+              f"{len(times)} steps, reference pipeline via make_pipeline/process_frame")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "warmup": 1, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} {w}x{h} {cfg.voxel_size * 1000:.0f}mm voxels, box room + spheres",
+                   "l2": "n/a (CPU)"},
+        "voxel_updates_per_s": float(np.mean(vps)),
+        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": res["cores"], "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, dist: Dist):
+    from paper_1410_0925_b200 import DeviceBuffer, Intrinsics, make_pipeline, render_synthetic, settings_from_config
+    from paper_1410_0925_b200 import _abi
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, trajectory
+
+    L = _abi.load()
+    cfg = CONFIGS[args.config]
+    device = dist.local_rank
+    fx, fy, cx, cy, w, h = cfg.intrinsics
+    intr = Intrinsics(fx, fy, cx, cy, w, h)
+    rgb = cfg.voxel_type == 2
+    n_frames = args.warmup + args.steps
+    poses = trajectory(n_frames)
+    # inputs rendered once on the GPU, resident in HBM
+    d_frames = [DeviceBuffer(w * h * 4) for _ in range(n_frames)]
+    c_frames = [DeviceBuffer(w * h * 3) for _ in range(n_frames)] if rgb else None
+    for i in range(n_frames):
+        render_synthetic(poses[i], intr, BOX_ROOM_SPHERES, BOX_ROOM_PLANES, d_frames[i].ptr,
+                         c_frames[i].ptr if rgb else None, device=device)
+    settings, calib = settings_from_config(cfg)
+    flush = args.l2_flush_mib << 20
+
+    def run_device(collect_stages=False):
+        p = make_pipeline(settings, calib, device=device)
+        hctx = p.handle
+        ms_frames, vis_blocks, modified = [], [], []
+        stage = np.zeros(8)
+        for i in range(n_frames):
+            timed = i >= args.warmup
+            if collect_stages and i == args.warmup:
+                p.set_profiling(True)  # resets the per-stage accumulators
+            if not cfg.tracking:
+                p.set_pose(poses[i])
+            if timed:
+                _abi.check("vf_flush_l2", L.vf_flush_l2(hctx, flush))
+                if i == args.warmup:
+                    p.synchronize()
+                    dist.barrier()
+                _abi.check("vf_event_record", L.vf_event_record(hctx, 8))
+            p.process_frame_device(d_frames[i].ptr, c_frames[i].ptr if rgb else None)
+            if timed:
+                _abi.check("vf_event_record", L.vf_event_record(hctx, 9))
+                ms = C.c_float()
+                _abi.check("vf_event_elapsed_ms", L.vf_event_elapsed_ms(hctx, 8, 9, C.byref(ms)))
+                ms_frames.append(ms.value)
+                st = _abi.VfFrameStats()
+                _abi.check("vf_read_stats", L.vf_read_stats(hctx, C.byref(st)))
+                vis_blocks.append(st.visible_blocks)
+                modified.append(L.vf_last_modified_voxels(hctx))
+        if collect_stages:
+            stage, nprof = p.stage_times()
+            stage = stage / max(nprof, 1)
+        launches = sum(p.kernel_launches_per_frame(cfg.tracking and i > 0) for i in range(args.warmup, n_frames))
+        p.close()
+        return np.array(ms_frames), np.array(vis_blocks), np.array(modified), stage, launches
+
+    # --- timed pass (graphs on) ---
+    clocks = ClockSampler(device)
+    clocks.start()
+    ms_frames, vis, modified, _, launches = run_device()
+    clk = clocks.stop()
+    t_local = float(ms_frames.sum()) / 1000.0
+    t_max = dist.max(t_local)
+    frames_total = dist.sum(float(args.steps))
+    value = frames_total / t_max
+    vox_updates = dist.sum(float(vis.sum() * 512)) / t_max
+
+    # --- e2e pass: host pinned buffers through vf_process_frame ---
+    p = make_pipeline(settings, calib, device=device)
+    hctx = p.handle
+    npix = w * h
+    host_depth = []
+    for i in range(n_frames):
+        ptr = L.vf_host_alloc_pinned(npix * 4)
+        arr = np.ctypeslib.as_array((C.c_float * npix).from_address(ptr))
+        arr[:] = d_frames[i].to_host(np.float32, (npix,))
+        host_depth.append((ptr, arr))
+    host_rgb = []
+    if rgb:
+        for i in range(n_frames):
+            ptr = L.vf_host_alloc_pinned(npix * 3)
+            arr = np.ctypeslib.as_array((C.c_uint8 * (npix * 3)).from_address(ptr))
+            arr[:] = c_frames[i].to_host(np.uint8, (npix * 3,))
+            host_rgb.append((ptr, arr))
+    st = _abi.VfFrameStats()
+    e2e_ms = 0.0
+    for i in range(n_frames):
+        timed = i >= args.warmup
+        if not cfg.tracking:
+            p.set_pose(poses[i])
+        if timed:
+            _abi.check("vf_flush_l2", L.vf_flush_l2(hctx, flush))
+            p.synchronize()
+            if i == args.warmup:
+                dist.barrier()
+            t0 = time.perf_counter()
+        _abi.check("vf_process_frame", L.vf_process_frame(hctx, C.c_void_p(host_depth[i][0]),
+                                                          C.c_void_p(host_rgb[i][0]) if rgb else None, C.byref(st)))
+        if timed:
+            e2e_ms += (time.perf_counter() - t0) * 1000.0
+    readback = int(L.vf_readback_bytes(hctx))
+    p.close()
+    for ptr, _ in host_depth + host_rgb:
+        L.vf_host_free_pinned(ptr)
+    e2e_t = dist.max(e2e_ms / 1000.0)
+    e2e_value = frames_total / e2e_t
+
+    # --- profiling pass: per-stage events (no graphs) ---
+    _, vis_p, mod_p, stage_ms, _ = run_device(collect_stages=True)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    vsize = 8 if rgb else 4
+    nvis = float(vis_p.mean())
+    nmod = float(mod_p.mean())
+    # B = N_vis (512 sizeof(V) + 4 + 16) + N_mod sizeof(V) + W H 4 (+ W H 3 rgb)
+    integ_bytes = nvis * (512 * vsize + 4 + 16) + nmod * vsize + npix * 4 + (npix * 3 if rgb else 0)
+    stages = {"tracking": stage_ms[0], "allocation": stage_ms[1], "integration": stage_ms[2],
+              "raycast": stage_ms[3]}
+    integ_ms = stage_ms[2]
+    integ_gbs = integ_bytes / (integ_ms * 1e-3) / 1e9 if integ_ms > 0 else 0.0
+    dominant = max(stages, key=stages.get)
+    roofline = {
+        "kernel": "k_integrate (TSDF integration)", "bound": "hbm", "achieved": integ_gbs, "peak": hbm_peak,
+        "unit": "GB/s", "frac": integ_gbs / hbm_peak, "traffic": None,
+        "algorithmic_bytes_per_launch": integ_bytes, "ms_per_launch": integ_ms, "peak_source": peak_src,
+        "note": f"dominant stage by time is {dominant}; integration is the HBM-graded kernel",
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TSDF/raycast) + f64 (allocation DDA, ICP)",
+        "data": "synthetic (GPU-rendered box room + spheres, 100-frame small-motion trajectory)",
+        "config": {
+            "workload": f"{cfg.name}: {w}x{h} depth, {cfg.voxel_size * 1000:.0f} mm voxels, mu {cfg.mu * 1000:.0f} mm, "
+                        f"{'VoxelSRgb' if rgb else 'VoxelS'}, hash {cfg.hash.bucket_count}x{cfg.hash.bucket_size}"
+                        f"+{cfg.hash.excess_count} / {cfg.hash.block_count} blocks, "
+                        f"{'ICP tracking on' if cfg.tracking else 'known poses'}",
+            "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single GPU",
+            "l2": f"flushed between frames ({args.l2_flush_mib} MiB write, outside the timed intervals)",
+            "graphs": True,
+        },
+        "voxel_updates_per_s": vox_updates,
+        "stage_ms": stages,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": npix * 4 + (npix * 3 if rgb else 0),
+                "d2h_bytes_per_step": readback},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "clocks": clk,
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        ref = cpu_reference_run(cfg, min(n_frames - 1, 30), args.cpu_seconds)
+        if ref:
+            line["cpu_baseline"] = {"value": ref["fps"], "unit": UNIT, "cores": ref["cores"], "kind": "reference",
+                                    "sample": f"{cfg.name} frames 1..{ref['frames']} ({ref['seconds']:.1f} s), "
+                                              "reference pipeline (oracle/_ref) via process_frame"}
+    if dist.rank == 0:
+        print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    dist = Dist(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+/*
+ * voxfuse_b200 — C ABI of the B200 (sm_100a) dense-fusion hot path.
+ *
+ * Drop-in replacement for the reference's per-frame path
+ * (/root/reference/proj, the CPU re-implementation of InfiniTAM, arXiv 1410.0925):
+ * voxel-block-hash allocation, TSDF / colour integration, hash-walking raycast
+ * and the point-to-plane ICP tracker.  The reference exposes that path as the
+ * C++ interface IPipeline + make_pipeline (proj/include/voxfuse/engine/pipeline.hpp:66-86)
+ * and as stage templates (allocation.hpp, integration.hpp, raycast.hpp,
+ * pyramid.hpp, depth_tracker.hpp); every entry point below names the
+ * reference interface it replaces.  Plain C types only: pointers, sizes, POD
+ * structs.  INTEGRATION.md shows the C++ IPipeline adapter and ctypes binding.
+ *
+ * Conventions (reference SPEC.md:708, pipeline.hpp): one context = one volume
+ * = one CUDA stream; a context is not thread-safe; the hot path never throws;
+ * every function returns VF_OK or a negative status.  There is no CPU
+ * fallback: without a usable sm_100 device vf_create fails with
+ * VF_ERR_NO_DEVICE.
+ *
+ * Poses are world-to-camera rigid transforms stored as 12 doubles: the
+ * row-major 3x3 rotation followed by the translation (reference Pose,
+ * proj/include/voxfuse/core/pose.hpp:8-46).  Images are row-major; depth is
+ * float metres with <= 0 marking missing samples; RGB is packed u8 x 3.
+ */
+#ifndef VOXFUSE_B200_H
+#define VOXFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define VF_ABI_VERSION 1
+
+enum vf_status {
+  VF_OK = 0,
+  VF_ERR_INVALID = -1,   /* bad argument / settings (reference: std::invalid_argument) */
+  VF_ERR_CUDA = -2,      /* CUDA runtime error; see vf_last_error */
+  VF_ERR_NO_DEVICE = -3, /* no sm_100 device: there is no CPU fallback */
+  VF_ERR_STATE = -4,     /* call not valid in the current state (e.g. maps not rendered yet) */
+  VF_ERR_OVERFLOW = -5   /* a device-side capacity was exceeded (see vf_frame_stats.error_flags) */
+};
+
+enum vf_voxel_type { VF_VOXEL_S = 1, VF_VOXEL_S_RGB = 2 }; /* voxel.hpp:90 (VoxelS, VoxelSRgb) */
+
+/* EngineSettings + SceneParams + HashConfig + TrackerSettings
+ * (pipeline.hpp:19-41, scene_params.hpp:6-13, hash_volume.hpp:49-58,
+ * tracking_state.hpp:12-23).  vf_default_settings() fills the reference
+ * defaults. */
+typedef struct vf_settings {
+  int voxel_type;
+  float voxel_size; /* metres */
+  float mu;         /* truncation band, metres */
+  int max_weight;
+  int stop_integrating_at_max;
+  int bucket_count; /* power of two */
+  int bucket_size;
+  int excess_count;
+  int block_count;
+  float near_clip;
+  float far_clip;
+  int visibility_margin_px;
+  int swap_margin_px;
+  int hierarchy_levels; /* <= 6 */
+  int rotation_only_levels;
+  int max_iterations;
+  int min_valid_points;
+  float icp_dist_threshold;
+  float convergence_eps;
+  double max_condition;
+  int tracking; /* 1: ICP tracker (reference behaviour); 0: known poses via vf_set_pose (config 2) */
+  int use_graphs; /* 1: replay each frame as one CUDA graph */
+} vf_settings;
+
+typedef struct vf_intrinsics { /* Intrinsics (core/intrinsics.hpp:10-32) */
+  double fx, fy, cx, cy;
+  int width, height;
+} vf_intrinsics;
+
+typedef struct vf_calib { /* Calibration (io/calibration.hpp:31-36) */
+  vf_intrinsics rgb;
+  vf_intrinsics depth;
+  double rgb_to_depth[12];
+  double disparity_a, disparity_b;
+} vf_calib;
+
+/* FrameStats (pipeline.hpp:45-58) plus device counters. */
+typedef struct vf_frame_stats {
+  int frame;
+  int tracking_ok;
+  int tracking_iterations;
+  int blocks_allocated;
+  int allocation_dropped;
+  int visible_blocks;
+  double tracking_cost;
+  int tracking_valid_points;
+  int allocation_requested;
+  int allocated_total; /* HashVolume::allocated_block_count */
+  int error_flags;
+  double pose[12];
+  double ms_tracking, ms_allocation, ms_integration, ms_swapping, ms_raycast, ms_total;
+} vf_frame_stats;
+
+typedef struct vf_alloc_stats { /* AllocationStats (allocation.hpp:42-47) */
+  int requested, allocated, dropped_vba_full, dropped_excess_full;
+} vf_alloc_stats;
+
+typedef struct vf_ctx vf_ctx;
+
+/* --- lifecycle (make_pipeline, pipeline.hpp:86; src/pipeline_factory.cpp:18-30) --- */
+int vf_abi_version(void);
+void vf_default_settings(vf_settings* s);
+int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out);
+int vf_destroy(vf_ctx* ctx);
+const char* vf_last_error(const vf_ctx* ctx);
+
+/* --- frame (IPipeline::process_frame, pipeline.hpp:70; pipeline_impl.hpp:65-123) ---
+ * Host buffers; the H2D copy of depth (and rgb) and the D2H of the stats are
+ * part of the call.  rgb may be NULL. */
+int vf_process_frame(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb, vf_frame_stats* stats);
+/* Same with inputs already resident in device memory (d_depth / d_rgb are
+ * device pointers).  stats may be NULL: then nothing is read back and the call
+ * does not synchronise. */
+int vf_process_frame_device(vf_ctx* ctx, const float* d_depth, const uint8_t* d_rgb, vf_frame_stats* stats);
+int vf_synchronize(vf_ctx* ctx);
+int vf_read_stats(vf_ctx* ctx, vf_frame_stats* stats);
+
+/* --- pose / state (IPipeline::pose, tracking_state; no reference setter: SURVEY §3(C)) --- */
+int vf_set_pose(vf_ctx* ctx, const double pose[12]);
+int vf_get_pose(vf_ctx* ctx, double pose[12]);
+int vf_frame_count(const vf_ctx* ctx);
+/* World-space point / normal maps (TrackingState::points/normals): width*height float4 each. */
+int vf_get_maps(vf_ctx* ctx, float* points, float* normals);
+int vf_set_maps(vf_ctx* ctx, const float* points, const float* normals, const double render_pose[12]);
+/* FNV-1a volume digest (IPipeline::volume_digest, pipeline_impl.hpp:144-164). */
+int vf_volume_digest(vf_ctx* ctx, uint64_t* out);
+
+/* --- state export / import (stage-isolated parity) --- */
+long vf_entry_count(const vf_ctx* ctx);
+long vf_voxel_bytes(const vf_ctx* ctx);
+int vf_export_entries(vf_ctx* ctx, void* out /* entry_count * 16 B HashEntry */);
+int vf_export_voxels(vf_ctx* ctx, void* out /* block_count * 512 * sizeof(voxel) */);
+int vf_export_free_stacks(vf_ctx* ctx, int* vba_top, int* vba_slots, int* excess_top, int* excess_slots);
+int vf_import_state(vf_ctx* ctx, const void* entries, const void* voxels, int vba_top, const int* vba_slots,
+                    int excess_top, const int* excess_slots);
+long vf_export_visible_list(vf_ctx* ctx, int* out, long cap);
+long vf_export_ranges(vf_ctx* ctx, float* out /* frag_w * frag_h * 2 */);
+
+/* --- stage entry points (the stage templates) --- */
+/* mark_blocks + perform_allocations + build_visible_list (allocation.hpp:137-248) */
+int vf_stage_allocate(vf_ctx* ctx, const float* depth_m, const double pose[12], vf_alloc_stats* out);
+/* integrate_frame, hash overload (integration.hpp:123-148), over the current visible list */
+int vf_stage_integrate(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb, const double pose[12]);
+/* create_expected_depths + render_maps (raycast.hpp:268-435) over the current visible list */
+int vf_stage_raycast(vf_ctx* ctx, const double pose[12]);
+/* build_depth_pyramid + icp_track (pyramid.hpp:101-111, depth_tracker.hpp:115-239)
+ * against the current maps; the current pose is the render pose. */
+int vf_stage_icp(vf_ctx* ctx, const float* depth_m, double out_pose[12], int* iterations, double* cost,
+                 int* valid_points, int* ok);
+/* Per-iteration ICP sums of the last track: rows of 32 doubles
+ * (level, iter, 21 H, 6 g, cost, count, 0). Returns the row count. */
+long vf_icp_trace(vf_ctx* ctx, double* out, long max_rows);
+/* Depth pyramid levels 0..levels-1 back to back (pyramid.hpp:101-111). */
+int vf_depth_pyramid(vf_ctx* ctx, const float* depth_m, float* out);
+
+/* --- synthetic input (io/synthetic.hpp:14-51; bench inputs rendered on the GPU) --- */
+/* spheres: n x {cx,cy,cz,r,ar,ag,ab}; planes: n x {nx,ny,nz,offset,ar,ag,ab,checker,checker_size}.
+ * Outputs are device pointers (d_depth: w*h floats, d_rgb: w*h*3 bytes or NULL). */
+int vf_render_synthetic(int device, int n_spheres, const double* spheres, int n_planes, const double* planes,
+                        const double world_to_cam[12], const vf_intrinsics* intr, double near_clip,
+                        double far_clip, float* d_depth, uint8_t* d_rgb);
+
+/* --- device memory helpers for callers without a CUDA runtime of their own --- */
+void* vf_device_alloc(size_t bytes);
+int vf_device_free(void* p);
+int vf_memcpy_h2d(void* dst, const void* src, size_t bytes);
+int vf_memcpy_d2h(void* dst, const void* src, size_t bytes);
+void* vf_host_alloc_pinned(size_t bytes);
+int vf_host_free_pinned(void* p);
+
+/* --- timing: CUDA events on the context's stream --- */
+int vf_event_record(vf_ctx* ctx, int slot);
+int vf_event_elapsed_ms(vf_ctx* ctx, int slot_a, int slot_b, float* ms);
+/* per-kernel profiling: when enabled, each stage is bracketed by events and
+ * vf_stage_times returns accumulated milliseconds per stage. */
+int vf_set_profiling(vf_ctx* ctx, int enabled);
+int vf_stage_times(vf_ctx* ctx, double* ms_out /* 8 */, long* frames);
+int vf_kernel_launches_per_frame(vf_ctx* ctx, int tracking_frame);
+/* Bytes of the per-frame stats readback (the D2H of vf_process_frame). */
+long vf_readback_bytes(const vf_ctx* ctx);
+/* Evict the L2 by writing `bytes` of scratch on the context's stream (bench hygiene). */
+int vf_flush_l2(vf_ctx* ctx, size_t bytes);
+/* Voxels whose state the last frame's integration changed (roofline accounting). */
+long vf_last_modified_voxels(vf_ctx* ctx);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXFUSE_B200_H */

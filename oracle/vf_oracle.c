@@ -810,8 +810,16 @@ static void create_expected_depths(vfo_ctx* c, const pose_t* w2c) {
   }
 }
 
+/* instrumentation (test infra): sample / probe counters of the last raycast */
+static long g_ray_samples, g_ray_reads, g_ray_trilinear, g_ray_rays, g_ray_coarse;
+long vfo_raycast_counters(long* out) {
+  out[0] = g_ray_rays; out[1] = g_ray_samples; out[2] = g_ray_reads; out[3] = g_ray_trilinear; out[4] = g_ray_coarse;
+  return 5;
+}
+
 /* HashSdfSampler::read (raycast.hpp:73-76) */
 static int sdf_read(vfo_ctx* c, i3 v, float* value) {
+  ++g_ray_reads;
   const uint8_t* vox = volume_read(c, v);
   int16_t sdf = 32767;
   int w = 0;
@@ -825,6 +833,7 @@ static int sdf_read(vfo_ctx* c, i3 v, float* value) {
 
 /* trilinear_sdf (raycast.hpp:102-117) */
 static int trilinear_sdf(vfo_ctx* c, f3 p, float* out) {
+  ++g_ray_trilinear;
   const f3 q = f3m(p.x - 0.5f, p.y - 0.5f, p.z - 0.5f);
   const i3 base = {(int)floorf(q.x), (int)floorf(q.y), (int)floorf(q.z)};
   const f3 f = f3m(q.x - (float)base.x, q.y - (float)base.y, q.z - (float)base.z);
@@ -883,6 +892,8 @@ static int cast_ray(vfo_ctx* c, int x, int y, const float* range, const pose_t* 
   enum { COARSE, FINE, SURFACE } state = COARSE;
   float t = 0.0f, t_front = -1.0f, sdf_front = 1.0f;
   while (t <= total) {
+    ++g_ray_samples;
+    if (state == COARSE) ++g_ray_coarse;
     const f3 p = f3m(start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t);
     float value;
     const int found = sdf_read(c, (i3){(int)floorf(p.x), (int)floorf(p.y), (int)floorf(p.z)}, &value);
@@ -946,6 +957,8 @@ static int cast_ray(vfo_ctx* c, int x, int y, const float* range, const pose_t* 
 /* render_maps (raycast.hpp:415-435) */
 static void render_maps(vfo_ctx* c, const pose_t* w2c) {
   const intr_t* in = &c->depth_intr;
+  g_ray_samples = g_ray_reads = g_ray_trilinear = g_ray_coarse = 0;
+  g_ray_rays = (long)in->width * in->height;
   const size_t n = (size_t)in->width * (size_t)in->height;
   memset(c->points, 0, sizeof(f4) * n);
   memset(c->normals, 0, sizeof(f4) * n);

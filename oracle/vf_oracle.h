@@ -78,6 +78,8 @@ long vfo_allocated_blocks(const vfo_ctx* c);
 /* free-stack state: tops and slot arrays (hash_volume.hpp:62-110) */
 void vfo_free_stacks(const vfo_ctx* c, int* vba_top, int* vba_slots, int* excess_top, int* excess_slots);
 uint64_t vfo_digest(const vfo_ctx* c);
+/* raycast counters of the last render: rays, samples, voxel reads, trilinear calls, coarse samples */
+long vfo_raycast_counters(long* out);
 /* last ICP solve trace: per accepted/evaluated iteration the 29 sums */
 long vfo_icp_trace(const vfo_ctx* c, double* out, long max_rows);
 

@@ -1,0 +1,435 @@
+// K1 — voxel-block allocation: mark (K1a), commit (K1b scan + apply) and the
+// visible list (K1c).
+//
+// Reference: proj/include/voxfuse/engine/allocation.hpp:56-248 and
+// proj/include/voxfuse/volume/hash_volume.hpp:161-258.
+//
+// Determinism.  The reference's mark_blocks writes one request per bucket with
+// plain stores from many threads (allocation.hpp:134-136,155-159); with one
+// worker the surviving request is the last visit in (raster index, DDA step)
+// order.  K1a reproduces exactly that winner with a 64-bit atomicMax of the key
+// ((pixel+1) << 12 | step) per bucket — the key is all that is stored; K1b
+// re-walks the winning pixel's DDA to recover the block position.  K1b then
+// commits the requests in ascending bucket order with prefix sums over the
+// free-stack tops, which reproduces the sequential perform_allocations slot
+// numbering (allocation.hpp:179-206) bit-for-bit; only when a free list would
+// run dry does it fall back to the reference's sequential loop on one thread.
+#include "vf_device.cuh"
+#include "vf_kernels.h"
+
+namespace vf {
+
+namespace {
+
+constexpr int kStepBits = 12;
+constexpr unsigned long long kStepMask = (1ull << kStepBits) - 1ull;
+
+// detail::dda_cells (allocation.hpp:60-96) in FP64.  Visit(cell, step) returns
+// false to stop the walk early.
+template <typename Visit>
+__device__ __forceinline__ void dda_cells(const D3 p0, const D3 p1, Visit&& visit) {
+  const double a0[3] = {p0.x, p0.y, p0.z};
+  const double a1[3] = {p1.x, p1.y, p1.z};
+  int cell[3], end[3], step[3];
+  double t_max[3], t_delta[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cell[a] = __double2int_rz(floor(a0[a]));
+    end[a] = __double2int_rz(floor(a1[a]));
+  }
+  if (!visit(cell[0], cell[1], cell[2], 0)) return;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double d = a1[a] - a0[a];
+    if (d > 0) {
+      step[a] = 1;
+      t_max[a] = (cell[a] + 1 - a0[a]) / d;
+      t_delta[a] = 1.0 / d;
+    } else if (d < 0) {
+      step[a] = -1;
+      t_max[a] = (cell[a] - a0[a]) / d;
+      t_delta[a] = -1.0 / d;
+    } else {
+      step[a] = 0;
+      t_max[a] = __longlong_as_double(0x7ff0000000000000ll);
+      t_delta[a] = __longlong_as_double(0x7ff0000000000000ll);
+    }
+  }
+  const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
+  for (int i = 0; i < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++i) {
+    int axis = 0;
+    if (t_max[1] < t_max[axis]) axis = 1;
+    if (t_max[2] < t_max[axis]) axis = 2;
+    if (t_max[axis] > 1.0) break;
+    cell[axis] += step[axis];
+    t_max[axis] += t_delta[axis];
+    if (!visit(cell[0], cell[1], cell[2], i + 1)) return;
+  }
+}
+
+// The per-pixel segment of mark_blocks (allocation.hpp:140-148).
+__device__ __forceinline__ void pixel_segment(int x, int y, float d, const IntrD& in, const PoseD& c2w, float voxel_size,
+                                              float mu, D3& p0, D3& p1) {
+  const double inv_block = 1.0 / (double)(voxel_size * (float)kBlockSide);
+  const D3 dir = mk((x - in.cx) / in.fx, (y - in.cy) / in.fy, 1.0);
+  const double v = (double)d - (double)mu;
+  const double near_d = (0.001 < v) ? v : 0.001;  // std::max(0.001, v)
+  const double far_d = (double)d + (double)mu;
+  const D3 q0 = apply(c2w, mk(dir.x * near_d, dir.y * near_d, dir.z * near_d));
+  const D3 q1 = apply(c2w, mk(dir.x * far_d, dir.y * far_d, dir.z * far_d));
+  p0 = mk(q0.x * inv_block, q0.y * inv_block, q0.z * inv_block);
+  p1 = mk(q1.x * inv_block, q1.y * inv_block, q1.z * inv_block);
+}
+
+}  // namespace
+
+// One thread computes the frame's derived camera parameters from the device
+// pose (CameraF, integration.hpp:18-33; rgb camera integration.hpp:128).
+__global__ void k_prep(const PoseD* __restrict__ pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb,
+                       FrameParams* __restrict__ fp) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const PoseD w2c = *pose;
+  fp->w2c = w2c;
+  fp->c2w = pose_inverse(w2c);
+  fp->depth_cam = make_camf(w2c, depth_in);
+  fp->rgb_cam = make_camf(pose_compose(depth_to_rgb, w2c), rgb_in);
+}
+
+// K1a: mark_blocks (allocation.hpp:137-168).  One thread per pixel.
+__global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, IntrD in, const FrameParams* __restrict__ fp,
+                                              HashView hv, float voxel_size, float mu,
+                                              unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
+                                              Counters* __restrict__ ctr) {
+  __shared__ PoseD s_c2w;
+  if (threadIdx.x < sizeof(PoseD) / sizeof(double))
+    reinterpret_cast<double*>(&s_c2w)[threadIdx.x] = reinterpret_cast<const double*>(&fp->c2w)[threadIdx.x];
+  __syncthreads();
+  const int npix = in.width * in.height;
+  const int pixel = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pixel >= npix) return;
+  const float d = __ldg(depth + pixel);
+  if (d <= 0.0f) return;
+  const int y = pixel / in.width, x = pixel - y * in.width;
+  D3 p0, p1;
+  pixel_segment(x, y, d, in, s_c2w, voxel_size, mu, p0, p1);
+  const unsigned long long key_base = (unsigned long long)(pixel + 1) << kStepBits;
+  dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
+    if (find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0) {
+      if ((unsigned long long)step > kStepMask) {
+        atomicOr(&ctr->error_flags, kErrDdaSteps);
+        return true;
+      }
+      const uint32_t bucket = hash_block(cx, cy, cz, hv.mask);
+      const unsigned long long old = atomicMax(req_key + bucket, key_base | (unsigned long long)step);
+      if (old == 0ull) atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
+    }
+    return true;
+  });
+}
+
+// Recover the block position a request key points at by re-walking that
+// pixel's DDA (bit-identical FP64 arithmetic).
+__device__ __forceinline__ void decode_request(unsigned long long key, const float* __restrict__ depth, const IntrD& in,
+                                               const PoseD& c2w, float voxel_size, float mu, int& bx, int& by, int& bz) {
+  const int pixel = (int)(key >> kStepBits) - 1;
+  const int target = (int)(key & kStepMask);
+  const int y = pixel / in.width, x = pixel - y * in.width;
+  D3 p0, p1;
+  pixel_segment(x, y, depth[pixel], in, c2w, voxel_size, mu, p0, p1);
+  bx = by = bz = 0;
+  dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
+    if (step == target) {
+      bx = cx;
+      by = cy;
+      bz = cz;
+      return false;
+    }
+    return true;
+  });
+}
+
+// K1b-scan (one CTA): ascending compaction of the request bitmap, the
+// bucket-full test that decides whether a request needs an excess entry, the
+// prefix sums that fix every request's free-stack pop, and the fast/slow
+// decision.  Also resets the per-frame counters consumed later in the frame.
+__global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_bits, int n_words, HashView hv,
+                                                     int* __restrict__ req_list, int* __restrict__ req_excess_rank,
+                                                     int max_requests, AllocMeta* __restrict__ meta,
+                                                     Counters* __restrict__ ctr, float2* __restrict__ ranges, int n_frag) {
+  __shared__ int s_scan[1024];
+  __shared__ int s_total;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int f = tid; f < n_frag; f += nt) ranges[f] = make_float2(3.402823466e+38f, 0.0f);
+  const int chunk = (n_words + nt - 1) / nt;
+  const int w0 = min(tid * chunk, n_words), w1 = min(w0 + chunk, n_words);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(__ldcg(req_bits + w));
+  // block exclusive scan (Hillis-Steele over 1024 entries)
+  s_scan[tid] = cnt;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    const int v = tid >= off ? s_scan[tid - off] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  int base = s_scan[tid] - cnt;
+  if (tid == nt - 1) s_total = s_scan[tid];
+  __syncthreads();
+  const int n = min(s_total, max_requests);
+  for (int w = w0; w < w1; ++w) {
+    uint32_t bits = __ldcg(req_bits + w);
+    if (!bits) continue;
+    req_bits[w] = 0u;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      if (base < max_requests) req_list[base] = w * 32 + b;
+      ++base;
+    }
+  }
+  __syncthreads();
+  // bucket-full test -> excess ranks, in list order
+  const int c2 = (n + nt - 1) / nt;
+  const int r0 = min(tid * c2, n), r1 = min(r0 + c2, n);
+  int ex = 0;
+  for (int k = r0; k < r1; ++k) {
+    const int h = req_list[k] * hv.bucket_size;
+    bool has_free = false;
+    for (int j = 0; j < hv.bucket_size; ++j)
+      if (load_entry_cg(hv.entries + h + j).block_state == kEntryUnallocated) {
+        has_free = true;
+        break;
+      }
+    req_excess_rank[k] = has_free ? -1 : 0;
+    ex += has_free ? 0 : 1;
+  }
+  s_scan[tid] = ex;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    const int v = tid >= off ? s_scan[tid - off] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  int ebase = s_scan[tid] - ex;
+  for (int k = r0; k < r1; ++k)
+    if (req_excess_rank[k] == 0) req_excess_rank[k] = ebase++;
+  if (tid == nt - 1) {
+    const int n_ex = s_scan[tid];
+    Counters c = *ctr;
+    AllocMeta m;
+    m.n = n;
+    m.n_excess = n_ex;
+    m.vba_base = c.vba_top;
+    m.excess_base = c.excess_top;
+    m.slow = (n > c.vba_top || n_ex > c.excess_top) ? 1 : 0;
+    if (s_total > max_requests) ctr->error_flags |= kErrRequestList;
+    if (!m.slow) {
+      ctr->vba_top = c.vba_top - n;
+      ctr->excess_top = c.excess_top - n_ex;
+      ctr->allocated = n;
+      ctr->dropped_vba_full = 0;
+      ctr->dropped_excess_full = 0;
+    }
+    ctr->requested = n;
+    ctr->n_requests = n;
+    ctr->visible_count = 0;
+    ctr->modified_voxels = 0;
+    *meta = m;
+  }
+}
+
+// K1b-apply: insert_block for every request (hash_volume.hpp:215-258).
+__global__ void __launch_bounds__(256) k_alloc_apply(const float* __restrict__ depth, IntrD in,
+                                                     const FrameParams* __restrict__ fp, float voxel_size, float mu,
+                                                     HashEntry* __restrict__ entries, uint32_t mask, int bucket_size,
+                                                     int ordered, unsigned long long* __restrict__ req_key,
+                                                     const int* __restrict__ req_list,
+                                                     const int* __restrict__ req_excess_rank,
+                                                     const AllocMeta* __restrict__ meta, int* __restrict__ vba_slots,
+                                                     int* __restrict__ excess_slots, int* __restrict__ alloc_list,
+                                                     int alloc_cap, Counters* __restrict__ ctr) {
+  const AllocMeta m = *meta;
+  const PoseD c2w = fp->c2w;
+  if (!m.slow) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m.n; k += gridDim.x * blockDim.x) {
+      const int bucket = req_list[k];
+      const unsigned long long key = req_key[bucket];
+      req_key[bucket] = 0ull;
+      int bx, by, bz;
+      decode_request(key, depth, in, c2w, voxel_size, mu, bx, by, bz);
+      const int slot = vba_slots[m.vba_base - 1 - k];
+      const int h = bucket * bucket_size;
+      int idx = -1;
+      const int er = req_excess_rank[k];
+      if (er < 0) {
+        for (int j = 0; j < bucket_size; ++j) {
+          HashEntry* e = entries + h + j;
+          if (e->block_state == kEntryUnallocated) {
+            e->x = (int16_t)bx;
+            e->y = (int16_t)by;
+            e->z = (int16_t)bz;
+            e->block_state = slot;
+            idx = h + j;
+            break;
+          }
+        }
+      } else {
+        const int ex = excess_slots[m.excess_base - 1 - er];
+        int last = h + bucket_size - 1;
+        while (entries[last].offset > 0) last = ordered + entries[last].offset - 1;
+        idx = ordered + ex;
+        HashEntry* e = entries + idx;
+        e->x = (int16_t)bx;
+        e->y = (int16_t)by;
+        e->z = (int16_t)bz;
+        e->offset = 0;
+        e->block_state = slot;
+        entries[last].offset = ex + 1;
+      }
+      if (idx >= 0) {
+        const int pos = atomicAdd(&ctr->alloc_count, 1);
+        if (pos < alloc_cap)
+          alloc_list[pos] = idx;
+        else
+          atomicOr(&ctr->error_flags, kErrAllocList);
+      }
+    }
+    return;
+  }
+  // Slow path: a free list runs dry this frame — the reference's sequential
+  // perform_allocations loop, verbatim, on one thread.
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  HashView hv{entries, mask, bucket_size, ordered};
+  int vtop = ctr->vba_top, etop = ctr->excess_top;
+  int allocated = 0, dvba = 0, dex = 0;
+  for (int k = 0; k < m.n; ++k) {
+    const int bucket = req_list[k];
+    const unsigned long long key = req_key[bucket];
+    req_key[bucket] = 0ull;
+    int bx, by, bz;
+    decode_request(key, depth, in, c2w, voxel_size, mu, bx, by, bz);
+    const int existing = find_entry<true>(hv, bx, by, bz, kEntrySwappedOut);
+    if (existing >= 0) {
+      HashEntry* e = entries + existing;
+      if (e->block_state >= 0) continue;
+      if (vtop <= 0) {
+        ++dvba;
+        continue;
+      }
+      e->block_state = vba_slots[--vtop];
+      continue;
+    }
+    const int h = (int)hash_block(bx, by, bz, mask) * bucket_size;
+    int idx = -1;
+    bool handled = false;
+    for (int j = 0; j < bucket_size; ++j) {
+      HashEntry* e = entries + h + j;
+      if (e->block_state == kEntryUnallocated) {
+        handled = true;
+        if (vtop <= 0) {
+          ++dvba;
+          break;
+        }
+        e->x = (int16_t)bx;
+        e->y = (int16_t)by;
+        e->z = (int16_t)bz;
+        e->block_state = vba_slots[--vtop];
+        idx = h + j;
+        break;
+      }
+    }
+    if (!handled) {
+      int last = h + bucket_size - 1;
+      while (entries[last].offset > 0) last = ordered + entries[last].offset - 1;
+      if (etop <= 0) {
+        ++dex;
+      } else {
+        const int ex = excess_slots[--etop];
+        if (vtop <= 0) {
+          excess_slots[etop++] = ex;  // FreeStack::push of the unused excess index
+          ++dvba;
+        } else {
+          idx = ordered + ex;
+          HashEntry* e = entries + idx;
+          e->x = (int16_t)bx;
+          e->y = (int16_t)by;
+          e->z = (int16_t)bz;
+          e->offset = 0;
+          e->block_state = vba_slots[--vtop];
+          entries[last].offset = ex + 1;
+        }
+      }
+    }
+    if (idx >= 0) {
+      ++allocated;
+      const int pos = ctr->alloc_count++;
+      if (pos < alloc_cap)
+        alloc_list[pos] = idx;
+      else
+        ctr->error_flags |= kErrAllocList;
+    }
+  }
+  ctr->vba_top = vtop;
+  ctr->excess_top = etop;
+  ctr->allocated = allocated;
+  ctr->dropped_vba_full = dvba;
+  ctr->dropped_excess_full = dex;
+}
+
+// detail::block_projects_into_view (allocation.hpp:101-130).  Corners are
+// int * 8 (+8) in int, times the FP32 voxel size, then widened (:110-112).
+__device__ __forceinline__ bool block_projects_into_view(int bx, int by, int bz, const PoseD& w2c, const IntrD& in,
+                                                         float vs, float near_clip, float far_clip, int margin) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double zmin = inf, zmax = -inf, xmin = inf, xmax = -inf, ymin = inf, ymax = -inf;
+  bool any_behind = false;
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    const D3 w = mk((double)((float)(bx * kBlockSide + ((corner & 1) ? kBlockSide : 0)) * vs),
+                    (double)((float)(by * kBlockSide + ((corner & 2) ? kBlockSide : 0)) * vs),
+                    (double)((float)(bz * kBlockSide + ((corner & 4) ? kBlockSide : 0)) * vs));
+    const D3 cam = apply(w2c, w);
+    zmin = cam.z < zmin ? cam.z : zmin;
+    zmax = zmax < cam.z ? cam.z : zmax;
+    if (cam.z <= 1e-6) {
+      any_behind = true;
+      continue;
+    }
+    const double u = in.fx * cam.x / cam.z + in.cx;
+    const double v = in.fy * cam.y / cam.z + in.cy;
+    xmin = u < xmin ? u : xmin;
+    xmax = xmax < u ? u : xmax;
+    ymin = v < ymin ? v : ymin;
+    ymax = ymax < v ? v : ymax;
+  }
+  if (zmax <= (double)near_clip || zmin >= (double)far_clip) return false;
+  if (any_behind) return true;
+  return xmax >= -margin && xmin <= in.width - 1 + margin && ymax >= -margin && ymin <= in.height - 1 + margin;
+}
+
+// K1c: build_visible_list (allocation.hpp:216-248) over the compact list of
+// allocated entries instead of all 2.2 M table slots.  The result is the same
+// set in a different order (order is irrelevant downstream).
+__global__ void __launch_bounds__(256) k_visible(const HashEntry* __restrict__ entries, const int* __restrict__ alloc_list,
+                                                 const FrameParams* __restrict__ fp, IntrD in, float vs, float near_clip,
+                                                 float far_clip, int margin, int* __restrict__ visible_list,
+                                                 Counters* __restrict__ ctr) {
+  __shared__ PoseD s_w2c;
+  if (threadIdx.x < sizeof(PoseD) / sizeof(double))
+    reinterpret_cast<double*>(&s_w2c)[threadIdx.x] = reinterpret_cast<const double*>(&fp->w2c)[threadIdx.x];
+  __syncthreads();
+  const int n = min(*(volatile int*)&ctr->alloc_count, 0x7fffffff);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int idx = alloc_list[i];
+    const HashEntry e = load_entry(entries + idx);
+    if (e.block_state < 0) continue;  // swapped out: never on the visible list
+    if (block_projects_into_view(e.x, e.y, e.z, s_w2c, in, vs, near_clip, far_clip, margin)) {
+      const int pos = warp_aggregated_add(&ctr->visible_count);
+      visible_list[pos] = idx;
+    }
+  }
+}
+
+}  // namespace vf

@@ -1,0 +1,930 @@
+// Host runtime behind the C ABI (include/voxfuse_b200.h): one context owns
+// the device-resident volume (hash table, VBA, free stacks), the per-frame
+// scratch, the tracking state (pose, point / normal maps) and one CUDA
+// stream; a frame is one CUDA-graph replay (pyramid -> ICP -> prep -> mark ->
+// commit -> visible -> integrate -> ranges -> raycast), and the only host
+// synchronisation per frame is the optional stats readback.
+//
+// Reference orchestration this replaces: Pipeline<TVoxel, hash>
+// (proj/include/voxfuse/engine/pipeline_impl.hpp:33-248).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/voxfuse_b200.h"
+#include "vf_device.cuh"
+#include "vf_kernels.h"
+
+using namespace vf;
+
+namespace {
+
+constexpr int kNumEvents = 16;
+constexpr int kTraceCap = 256;
+constexpr int kSmallPixels = 8192;
+
+// Everything the host reads back after a frame, contiguous for one D2H copy.
+struct DevState {
+  Counters ctr;
+  IcpResult icp;
+  PoseD pose;
+  FrameParams fp;
+  AllocMeta meta;
+};
+
+PoseD pose_from(const double* p) {
+  PoseD o;
+  std::memcpy(o.r, p, 9 * sizeof(double));
+  std::memcpy(o.t, p + 9, 3 * sizeof(double));
+  return o;
+}
+void pose_to(const PoseD& p, double* o) {
+  std::memcpy(o, p.r, 9 * sizeof(double));
+  std::memcpy(o + 9, p.t, 3 * sizeof(double));
+}
+IntrD intr_of(const vf_intrinsics& i) { return IntrD{i.fx, i.fy, i.cx, i.cy, i.width, i.height}; }
+// Intrinsics::half (core/intrinsics.hpp:22-31)
+IntrD intr_half(const IntrD& in) {
+  IntrD h;
+  h.fx = in.fx * 0.5;
+  h.fy = in.fy * 0.5;
+  h.cx = (in.cx - 0.5) * 0.5;
+  h.cy = (in.cy - 0.5) * 0.5;
+  h.width = (in.width + 1) / 2;
+  h.height = (in.height + 1) / 2;
+  return h;
+}
+
+}  // namespace
+
+struct vf_ctx {
+  vf_settings s;
+  vf_calib calib;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  int vsize = 4;
+  int ordered = 0, entry_count = 0;
+  uint32_t mask = 0;
+  IntrD din{}, rgbin{};
+  PoseD depth_to_rgb{};
+  int npix = 0, frag_w = 0, frag_h = 0;
+  std::vector<IntrD> levels;
+  size_t pyr_floats = 0;
+
+  // device buffers
+  HashEntry* entries = nullptr;
+  void* voxels = nullptr;
+  int* vba_slots = nullptr;
+  int* excess_slots = nullptr;
+  unsigned long long* req_key = nullptr;
+  uint32_t* req_bits = nullptr;
+  int* req_list = nullptr;
+  int* req_excess_rank = nullptr;
+  int* alloc_list = nullptr;
+  int alloc_cap = 0;
+  int* visible_list = nullptr;
+  DevState* dstate = nullptr;
+  float* depth = nullptr;
+  uint8_t* rgb = nullptr;
+  float* pyr = nullptr;
+  float2* ranges = nullptr;
+  float4* points = nullptr;
+  float4* normals = nullptr;
+  double* partials = nullptr;
+  void* ctl_scratch = nullptr;
+  double* trace = nullptr;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  int icp_grid = 0;
+
+  // host state
+  DevState* hstate = nullptr;  // pinned
+  PoseD* hpose = nullptr;      // pinned staging for vf_set_pose
+  int frame = 0;
+  bool maps_valid = false;
+  bool rgb_valid = false;
+
+  // graphs: [tracking][rgb]
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  bool graphs_ok = true;
+
+  cudaEvent_t ev[kNumEvents] = {};
+  cudaEvent_t ev_frame0 = nullptr, ev_frame1 = nullptr;
+  bool profiling = false;
+  double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long profiled_frames = 0;
+  int launches_last = 0;
+};
+
+#define VF_CUDA(ctx, call)                                                                  \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      if (ctx) (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e_);             \
+      std::fprintf(stderr, "[voxfuse_b200] %s failed: %s\n", #call, cudaGetErrorString(e_)); \
+      return VF_ERR_CUDA;                                                                   \
+    }                                                                                       \
+  } while (0)
+
+namespace {
+
+HashView hash_view(vf_ctx* c) { return HashView{c->entries, c->mask, c->s.bucket_size, c->ordered}; }
+
+int launch_icp(vf_ctx* c, cudaStream_t st) {
+  IcpArgs a{};
+  const int L = c->s.hierarchy_levels;
+  size_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    const IntrD& in = c->levels[l];
+    a.lv[l].depth = l == 0 ? c->depth : c->pyr + off;
+    if (l > 0) off += (size_t)in.width * in.height;
+    a.lv[l].w = in.width;
+    a.lv[l].h = in.height;
+    a.lv[l].fx = in.fx;
+    a.lv[l].fy = in.fy;
+    a.lv[l].cx = in.cx;
+    a.lv[l].cy = in.cy;
+  }
+  a.levels = L;
+  a.rotation_only_levels = c->s.rotation_only_levels;
+  a.max_iterations = c->s.max_iterations;
+  a.min_valid_points = c->s.min_valid_points;
+  a.dist_thr = c->s.icp_dist_threshold;
+  a.conv_eps = c->s.convergence_eps;
+  a.max_condition = c->s.max_condition;
+  a.points = c->points;
+  a.normals = c->normals;
+  a.map = c->din;
+  a.state_pose = &c->dstate->pose;
+  a.result = &c->dstate->icp;
+  a.partials = c->partials;
+  a.ctl_scratch = c->ctl_scratch;
+  a.trace = c->trace;
+  a.trace_cap = kTraceCap;
+  a.small_pixels = kSmallPixels;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c->icp_grid);
+  cfg.blockDim = dim3(kIcpThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VF_CUDA(c, cudaLaunchKernelEx(&cfg, k_icp, a));
+  return VF_OK;
+}
+
+void stage_mark(vf_ctx* c, int slot) {
+  if (c->profiling) cudaEventRecord(c->ev[slot], c->stream);
+}
+
+// VF_DEBUG_SYNC=1: synchronise and check after every launch (debugging only).
+bool debug_sync() {
+  static const bool on = std::getenv("VF_DEBUG_SYNC") != nullptr;
+  return on;
+}
+#define VF_LAUNCHED(ctx, name)                                                                      \
+  do {                                                                                              \
+    if (debug_sync()) {                                                                             \
+      cudaError_t e_ = cudaStreamSynchronize((ctx)->stream);                                        \
+      if (e_ == cudaSuccess) e_ = cudaGetLastError();                                               \
+      if (e_ != cudaSuccess) {                                                                      \
+        std::fprintf(stderr, "[voxfuse_b200] kernel %s failed: %s\n", name, cudaGetErrorString(e_)); \
+        (ctx)->err = std::string(name) + ": " + cudaGetErrorString(e_);                             \
+        return VF_ERR_CUDA;                                                                         \
+      }                                                                                             \
+    }                                                                                               \
+  } while (0)
+
+// The frame, as stream work.  With track=true the ICP runs first against the
+// maps of the previous frame; the updated pose stays on the device.
+int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
+  cudaStream_t st = c->stream;
+  const vf_settings& s = c->s;
+  int launches = 0;
+  stage_mark(c, 0);
+  if (track) {
+    if (s.hierarchy_levels > 1) {
+      k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, st>>>(
+          c->depth, c->din.width, c->din.height, s.hierarchy_levels, c->pyr);
+  VF_LAUNCHED(c, "k_pyramid");
+      ++launches;
+    }
+    if (int rc = launch_icp(c, st)) return rc;
+    VF_LAUNCHED(c, "k_icp");
+    ++launches;
+  }
+  stage_mark(c, 1);
+  k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
+  VF_LAUNCHED(c, "k_prep");
+  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, hash_view(c), s.voxel_size, s.mu,
+                                                c->req_key, c->req_bits, &c->dstate->ctr);
+  VF_LAUNCHED(c, "k_mark");
+  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_list, c->req_excess_rank,
+                                   s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
+                                   c->frag_w * c->frag_h);
+  VF_LAUNCHED(c, "k_alloc_scan");
+  k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
+                                                c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
+                                                c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots,
+                                                c->alloc_list, c->alloc_cap, &c->dstate->ctr);
+  VF_LAUNCHED(c, "k_alloc_apply");
+  k_visible<<<c->num_sms * 4, 256, 0, st>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
+                                            s.near_clip, s.far_clip, s.visibility_margin_px, c->visible_list,
+                                            &c->dstate->ctr);
+  VF_LAUNCHED(c, "k_visible");
+  launches += 5;
+  stage_mark(c, 2);
+  const bool color = c->vsize == 8;
+  if (color)
+    k_integrate_rgb<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
+                                                    c->depth, with_rgb ? c->rgb : nullptr, &c->dstate->fp,
+                                                    s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
+  else
+    k_integrate_s<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
+                                                  c->depth, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
+                                                  s.stop_integrating_at_max);
+  VF_LAUNCHED(c, "k_integrate");
+  ++launches;
+  stage_mark(c, 3);
+  k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
+                                           s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
+  VF_LAUNCHED(c, "k_ranges");
+  k_raycast<<<dim3(c->frag_w, c->frag_h), 256, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
+                                                         c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
+                                                         s.voxel_size, s.mu, c->points, c->normals);
+  VF_LAUNCHED(c, "k_raycast");
+  launches += 2;
+  stage_mark(c, 4);
+  c->launches_last = launches;
+  VF_CUDA(c, cudaGetLastError());
+  return VF_OK;
+}
+
+int run_frame(vf_ctx* c, bool track, bool with_rgb) {
+  if (c->s.use_graphs && c->graphs_ok && !c->profiling) {
+    cudaGraphExec_t& g = c->graph[track][with_rgb];
+    if (!g) {
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+      int rc = VF_OK;
+      if (e == cudaSuccess) {
+        rc = enqueue_frame(c, track, with_rgb);
+        e = cudaStreamEndCapture(c->stream, &graph);
+      }
+      if (e == cudaSuccess && rc == VF_OK) e = cudaGraphInstantiate(&g, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (e != cudaSuccess || rc != VF_OK) {
+        // Capture of the cooperative launch is unsupported on this driver:
+        // keep running the identical kernels without the graph.
+        cudaGetLastError();
+        g = nullptr;
+        c->graphs_ok = false;
+        std::fprintf(stderr, "[voxfuse_b200] CUDA graph capture unavailable (%s); launching kernels directly\n",
+                     cudaGetErrorString(e));
+        return enqueue_frame(c, track, with_rgb);
+      }
+    }
+    VF_CUDA(c, cudaGraphLaunch(g, c->stream));
+    return VF_OK;
+  }
+  return enqueue_frame(c, track, with_rgb);
+}
+
+int read_state(vf_ctx* c) {
+  VF_CUDA(c, cudaMemcpyAsync(c->hstate, c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return VF_OK;
+}
+
+void fill_stats(vf_ctx* c, bool tracked, int frame_index, vf_frame_stats* st) {
+  const DevState& h = *c->hstate;
+  std::memset(st, 0, sizeof(*st));
+  st->frame = frame_index;
+  st->tracking_ok = tracked ? h.icp.ok : 1;
+  st->tracking_iterations = tracked ? h.icp.iterations : 0;
+  st->tracking_cost = tracked ? h.icp.final_cost : 0.0;
+  st->tracking_valid_points = tracked ? h.icp.valid_points : 0;
+  st->allocation_requested = h.ctr.requested;
+  st->blocks_allocated = h.ctr.allocated;
+  st->allocation_dropped = h.ctr.dropped_vba_full + h.ctr.dropped_excess_full;
+  st->visible_blocks = h.ctr.visible_count;
+  st->allocated_total = c->s.block_count - h.ctr.vba_top;
+  st->error_flags = h.ctr.error_flags;
+  pose_to(h.pose, st->pose);
+}
+
+int upload(vf_ctx* c, void* dst, const void* src, size_t n, bool src_device) {
+  VF_CUDA(c, cudaMemcpyAsync(dst, src, n, src_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  return VF_OK;
+}
+
+int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_inputs, vf_frame_stats* stats) {
+  if (!c || !depth) return VF_ERR_INVALID;
+  if (int rc = upload(c, c->depth, depth, sizeof(float) * (size_t)c->npix, device_inputs)) return rc;
+  const bool with_rgb = rgb != nullptr && c->vsize == 8;
+  if (with_rgb) {
+    if (int rc = upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, device_inputs)) return rc;
+  }
+  const bool track = c->s.tracking && c->frame > 0 && c->maps_valid;
+  const int frame_index = c->frame;
+  if (stats) VF_CUDA(c, cudaEventRecord(c->ev_frame0, c->stream));
+  if (int rc = run_frame(c, track, with_rgb)) return rc;
+  c->maps_valid = true;
+  ++c->frame;
+  if (c->profiling) {
+    VF_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+      c->stage_ms[i] += ms;
+    }
+    ++c->profiled_frames;
+  }
+  if (stats) {
+    VF_CUDA(c, cudaEventRecord(c->ev_frame1, c->stream));
+    if (int rc = read_state(c)) return rc;
+    fill_stats(c, track, frame_index, stats);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev_frame0, c->ev_frame1);
+    stats->ms_total = ms;
+    if (c->hstate->ctr.error_flags) return VF_ERR_OVERFLOW;
+  }
+  return VF_OK;
+}
+
+template <typename T>
+int dalloc(vf_ctx* c, T** p, size_t bytes) {
+  VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(p), bytes));
+  return VF_OK;
+}
+
+void free_all(vf_ctx* c) {
+  for (auto& row : c->graph)
+    for (auto& g : row)
+      if (g) cudaGraphExecDestroy(g);
+  void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list,
+                  c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
+                  c->ranges, c->points, c->normals, c->partials, c->ctl_scratch, c->trace, c->flush_buf};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->hstate) cudaFreeHost(c->hstate);
+  if (c->hpose) cudaFreeHost(c->hpose);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_frame0) cudaEventDestroy(c->ev_frame0);
+  if (c->ev_frame1) cudaEventDestroy(c->ev_frame1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+int reset_volume(vf_ctx* c) {
+  // HashVolume(HashConfig) (hash_volume.hpp:133-140): all entries unallocated,
+  // default voxels, iota free stacks.
+  std::vector<HashEntry> he((size_t)c->entry_count);
+  for (auto& e : he) {
+    e.x = e.y = e.z = e.pad = 0;
+    e.offset = 0;
+    e.block_state = kEntryUnallocated;
+  }
+  VF_CUDA(c, cudaMemcpy(c->entries, he.data(), sizeof(HashEntry) * he.size(), cudaMemcpyHostToDevice));
+  const size_t nvox = (size_t)c->s.block_count * kBlockVolume;
+  k_fill_voxels<<<c->num_sms * 8, 256, 0, c->stream>>>(reinterpret_cast<uint32_t*>(c->voxels), nvox, c->vsize / 4);
+  std::vector<int> iota((size_t)std::max(c->s.block_count, c->s.excess_count));
+  for (size_t i = 0; i < iota.size(); ++i) iota[i] = (int)i;
+  VF_CUDA(c, cudaMemcpy(c->vba_slots, iota.data(), sizeof(int) * c->s.block_count, cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemcpy(c->excess_slots, iota.data(), sizeof(int) * c->s.excess_count, cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemset(c->req_key, 0, sizeof(unsigned long long) * c->s.bucket_count));
+  VF_CUDA(c, cudaMemset(c->req_bits, 0, sizeof(uint32_t) * (c->s.bucket_count / 32)));
+  DevState ds;
+  std::memset(&ds, 0, sizeof(ds));
+  ds.ctr.vba_top = c->s.block_count;
+  ds.ctr.excess_top = c->s.excess_count;
+  for (int i = 0; i < 9; ++i) ds.pose.r[i] = (i % 4 == 0) ? 1.0 : 0.0;  // tracking_state.hpp:27: identity
+  VF_CUDA(c, cudaMemcpy(c->dstate, &ds, sizeof(ds), cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemset(c->points, 0, sizeof(float4) * c->npix));
+  VF_CUDA(c, cudaMemset(c->normals, 0, sizeof(float4) * c->npix));
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaGetLastError());
+  c->frame = 0;
+  c->maps_valid = false;
+  return VF_OK;
+}
+
+int set_pose_dev(vf_ctx* c, const double* pose) {
+  *c->hpose = pose_from(pose);
+  VF_CUDA(c, cudaMemcpyAsync(&c->dstate->pose, c->hpose, sizeof(PoseD), cudaMemcpyHostToDevice, c->stream));
+  return VF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vf_abi_version(void) { return VF_ABI_VERSION; }
+
+void vf_default_settings(vf_settings* s) {
+  std::memset(s, 0, sizeof(*s));
+  s->voxel_type = VF_VOXEL_S;
+  s->voxel_size = 0.004f;  // scene_params.hpp:7
+  s->mu = 0.02f;
+  s->max_weight = 100;
+  s->stop_integrating_at_max = 0;
+  s->bucket_count = 1 << 20;  // hash_volume.hpp:50-53
+  s->bucket_size = 2;
+  s->excess_count = 1 << 17;
+  s->block_count = 1 << 18;
+  s->near_clip = 0.1f;  // pipeline.hpp:32-35
+  s->far_clip = 8.0f;
+  s->visibility_margin_px = 8;
+  s->swap_margin_px = 48;
+  s->hierarchy_levels = 5;  // tracking_state.hpp:14-22
+  s->rotation_only_levels = 2;
+  s->max_iterations = 20;
+  s->min_valid_points = 30;
+  s->icp_dist_threshold = 0.1f;
+  s->convergence_eps = 1e-5f;
+  s->max_condition = 1e8;
+  s->tracking = 1;
+  s->use_graphs = 1;
+}
+
+int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out) {
+  if (!s || !calib || !out) return VF_ERR_INVALID;
+  *out = nullptr;
+  if (s->bucket_count < 32 || (s->bucket_count & (s->bucket_count - 1)) != 0 || s->bucket_size < 1 ||
+      s->block_count < 1 || s->excess_count < 1 || (s->voxel_type != VF_VOXEL_S && s->voxel_type != VF_VOXEL_S_RGB) ||
+      s->hierarchy_levels < 1 || s->hierarchy_levels > kMaxLevels || calib->depth.width < 2 ||
+      calib->depth.height < 2 || !(s->voxel_size > 0) || !(s->mu > 0))
+    return VF_ERR_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
+    cudaGetLastError();
+    std::fprintf(stderr, "[voxfuse_b200] no CUDA device: the B200 path has no CPU fallback\n");
+    return VF_ERR_NO_DEVICE;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) {
+    std::fprintf(stderr, "[voxfuse_b200] device %d is not sm_100-class\n", device);
+    return VF_ERR_NO_DEVICE;
+  }
+  vf_ctx* c = new vf_ctx();
+  c->s = *s;
+  c->calib = *calib;
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return VF_ERR_CUDA;
+  }
+  c->vsize = s->voxel_type == VF_VOXEL_S_RGB ? 8 : 4;
+  c->ordered = s->bucket_count * s->bucket_size;
+  c->entry_count = c->ordered + s->excess_count;
+  c->mask = (uint32_t)(s->bucket_count - 1);
+  c->din = intr_of(calib->depth);
+  c->rgbin = intr_of(calib->rgb);
+  if (c->rgbin.width <= 0) c->rgbin = c->din;
+  {
+    PoseD r2d = pose_from(calib->rgb_to_depth);
+    c->depth_to_rgb = pose_inverse(r2d);  // Pose::inverse (pose.hpp:30-33)
+  }
+  c->npix = c->din.width * c->din.height;
+  c->frag_w = (c->din.width + kFragmentSize - 1) / kFragmentSize;
+  c->frag_h = (c->din.height + kFragmentSize - 1) / kFragmentSize;
+  c->levels.push_back(c->din);
+  c->pyr_floats = 0;
+  for (int l = 1; l < s->hierarchy_levels; ++l) {
+    c->levels.push_back(intr_half(c->levels.back()));
+    c->pyr_floats += (size_t)c->levels.back().width * c->levels.back().height;
+  }
+  c->alloc_cap = c->entry_count;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_icp, kIcpThreads, 0);
+  if (occ < 1) occ = 1;
+  c->icp_grid = c->num_sms * std::min(occ, 2);
+  int rc = VF_OK;
+  const size_t nvox = (size_t)s->block_count * kBlockVolume;
+  if ((rc = dalloc(c, &c->entries, sizeof(HashEntry) * (size_t)c->entry_count)) ||
+      (rc = dalloc(c, &c->voxels, nvox * (size_t)c->vsize)) ||
+      (rc = dalloc(c, &c->vba_slots, sizeof(int) * (size_t)s->block_count)) ||
+      (rc = dalloc(c, &c->excess_slots, sizeof(int) * (size_t)s->excess_count)) ||
+      (rc = dalloc(c, &c->req_key, sizeof(unsigned long long) * (size_t)s->bucket_count)) ||
+      (rc = dalloc(c, &c->req_bits, sizeof(uint32_t) * (size_t)(s->bucket_count / 32))) ||
+      (rc = dalloc(c, &c->req_list, sizeof(int) * (size_t)s->bucket_count)) ||
+      (rc = dalloc(c, &c->req_excess_rank, sizeof(int) * (size_t)s->bucket_count)) ||
+      (rc = dalloc(c, &c->alloc_list, sizeof(int) * (size_t)c->alloc_cap)) ||
+      (rc = dalloc(c, &c->visible_list, sizeof(int) * (size_t)c->alloc_cap)) ||
+      (rc = dalloc(c, &c->dstate, sizeof(DevState))) ||
+      (rc = dalloc(c, &c->depth, sizeof(float) * (size_t)c->npix)) ||
+      (rc = dalloc(c, &c->rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height)) ||
+      (rc = dalloc(c, &c->pyr, sizeof(float) * std::max<size_t>(c->pyr_floats, 1))) ||
+      (rc = dalloc(c, &c->ranges, sizeof(float2) * (size_t)c->frag_w * c->frag_h)) ||
+      (rc = dalloc(c, &c->points, sizeof(float4) * (size_t)c->npix)) ||
+      (rc = dalloc(c, &c->normals, sizeof(float4) * (size_t)c->npix)) ||
+      (rc = dalloc(c, &c->partials, sizeof(double) * 2 * 32 * (size_t)c->icp_grid)) ||
+      (rc = dalloc(c, &c->ctl_scratch, 1024)) || (rc = dalloc(c, &c->trace, sizeof(double) * 32 * kTraceCap))) {
+    free_all(c);
+    delete c;
+    return rc;
+  }
+  if (cudaMallocHost(reinterpret_cast<void**>(&c->hstate), sizeof(DevState)) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->hpose), sizeof(PoseD)) != cudaSuccess) {
+    free_all(c);
+    delete c;
+    return VF_ERR_CUDA;
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaEventCreate(&c->ev_frame0);
+  cudaEventCreate(&c->ev_frame1);
+  if ((rc = reset_volume(c))) {
+    free_all(c);
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return VF_OK;
+}
+
+int vf_destroy(vf_ctx* c) {
+  if (!c) return VF_ERR_INVALID;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  free_all(c);
+  delete c;
+  return VF_OK;
+}
+
+const char* vf_last_error(const vf_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int vf_process_frame(vf_ctx* c, const float* depth_m, const uint8_t* rgb, vf_frame_stats* stats) {
+  vf_frame_stats local;
+  return frame_common(c, depth_m, rgb, false, stats ? stats : &local);
+}
+
+int vf_process_frame_device(vf_ctx* c, const float* d_depth, const uint8_t* d_rgb, vf_frame_stats* stats) {
+  return frame_common(c, d_depth, d_rgb, true, stats);
+}
+
+int vf_synchronize(vf_ctx* c) {
+  if (!c) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return VF_OK;
+}
+
+int vf_read_stats(vf_ctx* c, vf_frame_stats* st) {
+  if (!c || !st) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  fill_stats(c, c->s.tracking && c->frame > 1, c->frame - 1, st);
+  return VF_OK;
+}
+
+int vf_set_pose(vf_ctx* c, const double pose[12]) {
+  if (!c || !pose) return VF_ERR_INVALID;
+  return set_pose_dev(c, pose);
+}
+
+int vf_get_pose(vf_ctx* c, double pose[12]) {
+  if (!c || !pose) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  pose_to(c->hstate->pose, pose);
+  return VF_OK;
+}
+
+int vf_frame_count(const vf_ctx* c) { return c ? c->frame : -1; }
+
+int vf_get_maps(vf_ctx* c, float* points, float* normals) {
+  if (!c) return VF_ERR_INVALID;
+  if (!c->maps_valid) return VF_ERR_STATE;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (points) VF_CUDA(c, cudaMemcpy(points, c->points, sizeof(float4) * c->npix, cudaMemcpyDeviceToHost));
+  if (normals) VF_CUDA(c, cudaMemcpy(normals, c->normals, sizeof(float4) * c->npix, cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+int vf_set_maps(vf_ctx* c, const float* points, const float* normals, const double render_pose[12]) {
+  if (!c || !points || !normals || !render_pose) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(c->points, points, sizeof(float4) * c->npix, cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemcpy(c->normals, normals, sizeof(float4) * c->npix, cudaMemcpyHostToDevice));
+  if (int rc = set_pose_dev(c, render_pose)) return rc;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->maps_valid = true;
+  return VF_OK;
+}
+
+long vf_entry_count(const vf_ctx* c) { return c ? c->entry_count : -1; }
+long vf_voxel_bytes(const vf_ctx* c) { return c ? (long)c->s.block_count * kBlockVolume * c->vsize : -1; }
+
+int vf_export_entries(vf_ctx* c, void* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(out, c->entries, sizeof(HashEntry) * c->entry_count, cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+int vf_export_voxels(vf_ctx* c, void* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(out, c->voxels, (size_t)vf_voxel_bytes(c), cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+int vf_export_free_stacks(vf_ctx* c, int* vba_top, int* vba_slots, int* excess_top, int* excess_slots) {
+  if (!c) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  if (vba_top) *vba_top = c->hstate->ctr.vba_top;
+  if (excess_top) *excess_top = c->hstate->ctr.excess_top;
+  if (vba_slots) VF_CUDA(c, cudaMemcpy(vba_slots, c->vba_slots, sizeof(int) * c->s.block_count, cudaMemcpyDeviceToHost));
+  if (excess_slots)
+    VF_CUDA(c, cudaMemcpy(excess_slots, c->excess_slots, sizeof(int) * c->s.excess_count, cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+int vf_import_state(vf_ctx* c, const void* entries, const void* voxels, int vba_top, const int* vba_slots,
+                    int excess_top, const int* excess_slots) {
+  if (!c || !entries || !voxels || !vba_slots || !excess_slots) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(c->entries, entries, sizeof(HashEntry) * c->entry_count, cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemcpy(c->voxels, voxels, (size_t)vf_voxel_bytes(c), cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemcpy(c->vba_slots, vba_slots, sizeof(int) * c->s.block_count, cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemcpy(c->excess_slots, excess_slots, sizeof(int) * c->s.excess_count, cudaMemcpyHostToDevice));
+  if (int rc = read_state(c)) return rc;
+  DevState ds = *c->hstate;
+  std::memset(&ds.ctr, 0, sizeof(ds.ctr));
+  ds.ctr.vba_top = vba_top;
+  ds.ctr.excess_top = excess_top;
+  VF_CUDA(c, cudaMemcpy(c->dstate, &ds, sizeof(ds), cudaMemcpyHostToDevice));
+  k_rebuild_alloc_list<<<c->num_sms * 4, 256, 0, c->stream>>>(c->entries, c->entry_count, c->alloc_list, c->alloc_cap,
+                                                              &c->dstate->ctr);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return VF_OK;
+}
+
+long vf_export_visible_list(vf_ctx* c, int* out, long cap) {
+  if (!c) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  const long n = c->hstate->ctr.visible_count;
+  if (out && cap > 0) {
+    const long k = n < cap ? n : cap;
+    if (k > 0 && cudaMemcpy(out, c->visible_list, sizeof(int) * k, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return VF_ERR_CUDA;
+  }
+  return n;
+}
+
+long vf_export_ranges(vf_ctx* c, float* out) {
+  if (!c) return VF_ERR_INVALID;
+  const long n = (long)c->frag_w * c->frag_h;
+  if (out) {
+    VF_CUDA(c, cudaStreamSynchronize(c->stream));
+    VF_CUDA(c, cudaMemcpy(out, c->ranges, sizeof(float2) * n, cudaMemcpyDeviceToHost));
+  }
+  return n;
+}
+
+int vf_stage_allocate(vf_ctx* c, const float* depth_m, const double pose[12], vf_alloc_stats* out) {
+  if (!c || !depth_m || !pose) return VF_ERR_INVALID;
+  const vf_settings& s = c->s;
+  cudaStream_t st = c->stream;
+  if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
+  if (int rc = set_pose_dev(c, pose)) return rc;
+  k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
+  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, hash_view(c), s.voxel_size, s.mu,
+                                                c->req_key, c->req_bits, &c->dstate->ctr);
+  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_list, c->req_excess_rank,
+                                   s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
+                                   c->frag_w * c->frag_h);
+  k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
+                                                c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
+                                                c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots,
+                                                c->alloc_list, c->alloc_cap, &c->dstate->ctr);
+  k_visible<<<c->num_sms * 4, 256, 0, st>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
+                                            s.near_clip, s.far_clip, s.visibility_margin_px, c->visible_list,
+                                            &c->dstate->ctr);
+  VF_CUDA(c, cudaGetLastError());
+  if (int rc = read_state(c)) return rc;
+  if (out) {
+    out->requested = c->hstate->ctr.requested;
+    out->allocated = c->hstate->ctr.allocated;
+    out->dropped_vba_full = c->hstate->ctr.dropped_vba_full;
+    out->dropped_excess_full = c->hstate->ctr.dropped_excess_full;
+  }
+  return c->hstate->ctr.error_flags ? VF_ERR_OVERFLOW : VF_OK;
+}
+
+int vf_stage_integrate(vf_ctx* c, const float* depth_m, const uint8_t* rgb, const double pose[12]) {
+  if (!c || !depth_m || !pose) return VF_ERR_INVALID;
+  const vf_settings& s = c->s;
+  cudaStream_t st = c->stream;
+  if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
+  const bool with_rgb = rgb && c->vsize == 8;
+  if (with_rgb && upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, false)) return VF_ERR_CUDA;
+  if (int rc = set_pose_dev(c, pose)) return rc;
+  k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
+  if (c->vsize == 8)
+    k_integrate_rgb<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
+                                                    c->depth, with_rgb ? c->rgb : nullptr, &c->dstate->fp,
+                                                    s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
+  else
+    k_integrate_s<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
+                                                  c->depth, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
+                                                  s.stop_integrating_at_max);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaStreamSynchronize(st));
+  return VF_OK;
+}
+
+int vf_stage_raycast(vf_ctx* c, const double pose[12]) {
+  if (!c || !pose) return VF_ERR_INVALID;
+  const vf_settings& s = c->s;
+  cudaStream_t st = c->stream;
+  if (int rc = set_pose_dev(c, pose)) return rc;
+  k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
+  k_init_ranges<<<(c->frag_w * c->frag_h + 255) / 256, 256, 0, st>>>(c->ranges, c->frag_w * c->frag_h);
+  k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
+                                           s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
+  k_raycast<<<dim3(c->frag_w, c->frag_h), 256, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
+                                                         c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
+                                                         s.voxel_size, s.mu, c->points, c->normals);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaStreamSynchronize(st));
+  c->maps_valid = true;
+  return VF_OK;
+}
+
+int vf_stage_icp(vf_ctx* c, const float* depth_m, double out_pose[12], int* iterations, double* cost,
+                 int* valid_points, int* ok) {
+  if (!c || !depth_m) return VF_ERR_INVALID;
+  if (!c->maps_valid) return VF_ERR_STATE;
+  cudaStream_t st = c->stream;
+  if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
+  if (c->s.hierarchy_levels > 1)
+    k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, st>>>(
+        c->depth, c->din.width, c->din.height, c->s.hierarchy_levels, c->pyr);
+  if (int rc = launch_icp(c, st)) return rc;
+  VF_CUDA(c, cudaGetLastError());
+  if (int rc = read_state(c)) return rc;
+  const IcpResult& r = c->hstate->icp;
+  if (out_pose) pose_to(r.pose, out_pose);
+  if (iterations) *iterations = r.iterations;
+  if (cost) *cost = r.final_cost;
+  if (valid_points) *valid_points = r.valid_points;
+  if (ok) *ok = r.ok;
+  return VF_OK;
+}
+
+long vf_icp_trace(vf_ctx* c, double* out, long max_rows) {
+  if (!c) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  const long n = std::min<long>(c->hstate->icp.trace_rows, kTraceCap);
+  if (out && max_rows > 0) {
+    const long k = std::min(n, max_rows);
+    if (cudaMemcpy(out, c->trace, sizeof(double) * 32 * k, cudaMemcpyDeviceToHost) != cudaSuccess) return VF_ERR_CUDA;
+  }
+  return n;
+}
+
+int vf_depth_pyramid(vf_ctx* c, const float* depth_m, float* out) {
+  if (!c || !depth_m || !out) return VF_ERR_INVALID;
+  if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
+  if (c->s.hierarchy_levels > 1)
+    k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, c->stream>>>(
+        c->depth, c->din.width, c->din.height, c->s.hierarchy_levels, c->pyr);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(out, c->depth, sizeof(float) * c->npix, cudaMemcpyDeviceToHost));
+  if (c->pyr_floats)
+    VF_CUDA(c, cudaMemcpy(out + c->npix, c->pyr, sizeof(float) * c->pyr_floats, cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+int vf_volume_digest(vf_ctx* c, uint64_t* out) {
+  // FNV-1a over allocated entries ascending: pos bytes, then the LE
+  // VoxelCodec bytes of each voxel (pipeline_impl.hpp:144-164, voxel.hpp:123-155).
+  if (!c || !out) return VF_ERR_INVALID;
+  std::vector<HashEntry> e((size_t)c->entry_count);
+  std::vector<uint8_t> v((size_t)vf_voxel_bytes(c));
+  if (int rc = vf_export_entries(c, e.data())) return rc;
+  if (int rc = vf_export_voxels(c, v.data())) return rc;
+  uint64_t h = 1469598103934665603ull;
+  auto fnv = [&](uint8_t b) {
+    h ^= b;
+    h *= 1099511628211ull;
+  };
+  const int codec = c->vsize == 8 ? 7 : 3;
+  for (const HashEntry& he : e) {
+    if (he.block_state < 0) continue;
+    const uint8_t* pb = reinterpret_cast<const uint8_t*>(&he);
+    for (int k = 0; k < 6; ++k) fnv(pb[k]);
+    for (int i = 0; i < kBlockVolume; ++i) {
+      const uint8_t* vx = v.data() + ((size_t)he.block_state * kBlockVolume + i) * c->vsize;
+      for (int k = 0; k < codec; ++k) fnv(vx[k]);
+    }
+  }
+  *out = h;
+  return VF_OK;
+}
+
+int vf_render_synthetic(int device, int n_spheres, const double* spheres, int n_planes, const double* planes,
+                        const double world_to_cam[12], const vf_intrinsics* intr, double near_clip, double far_clip,
+                        float* d_depth, uint8_t* d_rgb) {
+  if (!world_to_cam || !intr || (n_spheres > 0 && !spheres) || (n_planes > 0 && !planes)) return VF_ERR_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
+    cudaGetLastError();
+    return VF_ERR_NO_DEVICE;
+  }
+  cudaSetDevice(device);
+  double* dsp = nullptr;
+  double* dpl = nullptr;
+  const size_t bs = sizeof(double) * 7 * std::max(n_spheres, 1), bp = sizeof(double) * 9 * std::max(n_planes, 1);
+  if (cudaMalloc(&dsp, bs) != cudaSuccess || cudaMalloc(&dpl, bp) != cudaSuccess) return VF_ERR_CUDA;
+  if (n_spheres) cudaMemcpy(dsp, spheres, sizeof(double) * 7 * n_spheres, cudaMemcpyHostToDevice);
+  if (n_planes) cudaMemcpy(dpl, planes, sizeof(double) * 9 * n_planes, cudaMemcpyHostToDevice);
+  const PoseD c2w = pose_inverse(pose_from(world_to_cam));
+  const IntrD in = intr_of(*intr);
+  const int npix = in.width * in.height;
+  k_synth<<<(npix + 255) / 256, 256>>>(n_spheres, dsp, n_planes, dpl, c2w, in, near_clip, far_clip, d_depth, d_rgb);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(dsp);
+  cudaFree(dpl);
+  return e == cudaSuccess ? VF_OK : VF_ERR_CUDA;
+}
+
+void* vf_device_alloc(size_t bytes) {
+  void* p = nullptr;
+  return cudaMalloc(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+int vf_device_free(void* p) { return cudaFree(p) == cudaSuccess ? VF_OK : VF_ERR_CUDA; }
+int vf_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  return cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? VF_OK : VF_ERR_CUDA;
+}
+int vf_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  return cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? VF_OK : VF_ERR_CUDA;
+}
+void* vf_host_alloc_pinned(size_t bytes) {
+  void* p = nullptr;
+  return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+int vf_host_free_pinned(void* p) { return cudaFreeHost(p) == cudaSuccess ? VF_OK : VF_ERR_CUDA; }
+
+int vf_event_record(vf_ctx* c, int slot) {
+  if (!c || slot < 8 || slot >= kNumEvents) return VF_ERR_INVALID;  // 0..7 reserved for stage profiling
+  VF_CUDA(c, cudaEventRecord(c->ev[slot], c->stream));
+  return VF_OK;
+}
+int vf_event_elapsed_ms(vf_ctx* c, int a, int b, float* ms) {
+  if (!c || !ms || a < 0 || b < 0 || a >= kNumEvents || b >= kNumEvents) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaEventSynchronize(c->ev[b]));
+  VF_CUDA(c, cudaEventElapsedTime(ms, c->ev[a], c->ev[b]));
+  return VF_OK;
+}
+int vf_set_profiling(vf_ctx* c, int enabled) {
+  if (!c) return VF_ERR_INVALID;
+  c->profiling = enabled != 0;
+  for (double& m : c->stage_ms) m = 0;
+  c->profiled_frames = 0;
+  return VF_OK;
+}
+int vf_stage_times(vf_ctx* c, double* ms_out, long* frames) {
+  if (!c || !ms_out) return VF_ERR_INVALID;
+  for (int i = 0; i < 8; ++i) ms_out[i] = c->stage_ms[i];
+  if (frames) *frames = c->profiled_frames;
+  return VF_OK;
+}
+long vf_readback_bytes(const vf_ctx* c) { return c ? (long)sizeof(DevState) : -1; }
+
+int vf_flush_l2(vf_ctx* c, size_t bytes) {
+  if (!c) return VF_ERR_INVALID;
+  if (c->flush_bytes < bytes) {
+    if (c->flush_buf) cudaFree(c->flush_buf);
+    c->flush_buf = nullptr;
+    c->flush_bytes = 0;
+    VF_CUDA(c, cudaMalloc(&c->flush_buf, bytes));
+    c->flush_bytes = bytes;
+  }
+  VF_CUDA(c, cudaMemsetAsync(c->flush_buf, (int)(c->frame & 0xFF), bytes, c->stream));
+  return VF_OK;
+}
+
+long vf_last_modified_voxels(vf_ctx* c) {
+  if (!c) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  return c->hstate->ctr.modified_voxels;
+}
+
+int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
+  if (!c) return VF_ERR_INVALID;
+  return 8 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 2 : 1) : 0);
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// Kernel declarations shared between the kernel translation units and the
+// host runtime (vf_api.cu).
+#pragma once
+
+#include "vf_device.cuh"
+
+namespace vf {
+
+constexpr int kIcpThreads = 256;
+constexpr int kMaxLevels = 6;
+
+struct AllocMeta {
+  int n, n_excess, vba_base, excess_base, slow;
+  int pad[3];
+};
+
+struct IcpLevel {
+  const float* depth;
+  int w, h;
+  double fx, fy, cx, cy;
+};
+
+struct IcpResult {
+  PoseD pose;
+  double final_cost;
+  int ok, iterations, valid_points, trace_rows;
+};
+
+struct IcpArgs {
+  IcpLevel lv[kMaxLevels];
+  int levels, rotation_only_levels, max_iterations, min_valid_points;
+  float dist_thr, conv_eps;
+  double max_condition;
+  const float4* points;
+  const float4* normals;
+  IntrD map;
+  PoseD* state_pose;
+  IcpResult* result;
+  double* partials;
+  void* ctl_scratch;
+  double* trace;
+  int trace_cap;
+  int small_pixels;
+};
+
+__global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);
+__global__ void k_mark(const float* depth, IntrD in, const FrameParams* fp, HashView hv, float voxel_size, float mu,
+                       unsigned long long* req_key, uint32_t* req_bits, Counters* ctr);
+__global__ void k_alloc_scan(uint32_t* req_bits, int n_words, HashView hv, int* req_list, int* req_excess_rank,
+                             int max_requests, AllocMeta* meta, Counters* ctr, float2* ranges, int n_frag);
+__global__ void k_alloc_apply(const float* depth, IntrD in, const FrameParams* fp, float voxel_size, float mu,
+                              HashEntry* entries, uint32_t mask, int bucket_size, int ordered,
+                              unsigned long long* req_key, const int* req_list, const int* req_excess_rank,
+                              const AllocMeta* meta, int* vba_slots, int* excess_slots, int* alloc_list,
+                              int alloc_cap, Counters* ctr);
+__global__ void k_visible(const HashEntry* entries, const int* alloc_list, const FrameParams* fp, IntrD in, float vs,
+                          float near_clip, float far_clip, int margin, int* visible_list, Counters* ctr);
+__global__ void k_integrate_s(const HashEntry* entries, const int* visible_list, const Counters* ctr, void* voxels,
+                              const float* depth, const FrameParams* fp, float vs, float mu, int max_weight,
+                              int stop_at_max);
+__global__ void k_integrate_rgb(const HashEntry* entries, const int* visible_list, const Counters* ctr, void* voxels,
+                                const float* depth, const uint8_t* rgb, const FrameParams* fp, float vs, float mu,
+                                int max_weight, int stop_at_max);
+__global__ void k_ranges(const HashEntry* entries, const int* visible_list, const Counters* ctr,
+                         const FrameParams* fp, IntrD in, float vs, float near_clip, float far_clip, float2* ranges,
+                         int frag_w);
+__global__ void k_raycast(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
+                          IntrD in, float vs, float mu, float4* points, float4* normals);
+__global__ void k_pyramid(const float* depth0, int w0, int h0, int levels, float* out);
+__global__ void k_icp(IcpArgs a);
+__global__ void k_synth(int n_spheres, const double* spheres, int n_planes, const double* planes, PoseD c2w,
+                        IntrD in, double near_clip, double far_clip, float* depth, uint8_t* rgb);
+__global__ void k_fill_voxels(uint32_t* vox, size_t n_voxels, int words_per_voxel);
+__global__ void k_rebuild_alloc_list(const HashEntry* entries, int n, int* alloc_list, int cap, Counters* ctr);
+__global__ void k_init_ranges(float2* ranges, int n);
+__global__ void k_reset_visible(Counters* ctr);
+
+}  // namespace vf

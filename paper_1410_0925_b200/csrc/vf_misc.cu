@@ -1,0 +1,129 @@
+// Support kernels: synthetic depth/RGB rendering for benchmark inputs, VBA
+// initialisation, compact-list rebuild after a state import, range reset.
+#include "vf_device.cuh"
+#include "vf_kernels.h"
+
+namespace vf {
+
+// render_synthetic_depth / render_synthetic_rgb (reference proj/src/synthetic.cpp:19-108),
+// one thread per pixel, FP64 like the reference.  Used to generate the bench
+// inputs on the device (the CPU oracle restates the same renderer for tests).
+__global__ void __launch_bounds__(256) k_synth(int n_spheres, const double* __restrict__ spheres, int n_planes,
+                                               const double* __restrict__ planes, PoseD c2w, IntrD in,
+                                               double near_clip, double far_clip, float* __restrict__ depth,
+                                               uint8_t* __restrict__ rgb) {
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= in.width * in.height) return;
+  const int y = pix / in.width, x = pix - y * in.width;
+  const D3 origin = mk(c2w.t[0], c2w.t[1], c2w.t[2]);
+  const D3 dir = mat_vec(c2w.r, mk((x - in.cx) / in.fx, (y - in.cy) / in.fy, 1.0));
+  double best_t = __longlong_as_double(0x7ff0000000000000ll);
+  D3 best_p = mk(0, 0, 0), best_n = mk(0, 0, 0);
+  float alb[3] = {0.f, 0.f, 0.f};
+  for (int i = 0; i < n_spheres; ++i) {
+    const double* s = spheres + 7 * i;
+    const D3 oc = mk(origin.x - s[0], origin.y - s[1], origin.z - s[2]);
+    const double a = dir.x * dir.x + dir.y * dir.y + dir.z * dir.z;
+    const double b = 2.0 * (oc.x * dir.x + oc.y * dir.y + oc.z * dir.z);
+    const double c = (oc.x * oc.x + oc.y * oc.y + oc.z * oc.z) - s[3] * s[3];
+    const double disc = b * b - 4 * a * c;
+    if (disc < 0) continue;
+    const double sq = sqrt(disc);
+    const double ts[2] = {(-b - sq) / (2 * a), (-b + sq) / (2 * a)};
+    for (int k = 0; k < 2; ++k) {
+      const double t = ts[k];
+      if (t > near_clip && t < far_clip && t < best_t) {
+        best_t = t;
+        best_p = mk(origin.x + t * dir.x, origin.y + t * dir.y, origin.z + t * dir.z);
+        const D3 nn = mk(best_p.x - s[0], best_p.y - s[1], best_p.z - s[2]);
+        const double len = sqrt(nn.x * nn.x + nn.y * nn.y + nn.z * nn.z);
+        best_n = len > 0 ? mk(nn.x / len, nn.y / len, nn.z / len) : nn;
+        alb[0] = (float)s[4];
+        alb[1] = (float)s[5];
+        alb[2] = (float)s[6];
+      }
+    }
+  }
+  for (int i = 0; i < n_planes; ++i) {
+    const double* p = planes + 9 * i;
+    const double denom = p[0] * dir.x + p[1] * dir.y + p[2] * dir.z;
+    if (fabs(denom) < 1e-12) continue;
+    const double t = (p[3] - (p[0] * origin.x + p[1] * origin.y + p[2] * origin.z)) / denom;
+    if (t > near_clip && t < far_clip && t < best_t) {
+      best_t = t;
+      best_p = mk(origin.x + t * dir.x, origin.y + t * dir.y, origin.z + t * dir.z);
+      best_n = denom < 0 ? mk(p[0], p[1], p[2]) : mk(-p[0], -p[1], -p[2]);
+      float a3[3] = {(float)p[4], (float)p[5], (float)p[6]};
+      if (p[7] != 0.0) {
+        const double na[3] = {fabs(p[0]), fabs(p[1]), fabs(p[2])};
+        int drop = 0;
+        if (na[1] > na[drop]) drop = 1;
+        if (na[2] > na[drop]) drop = 2;
+        const double pt[3] = {best_p.x, best_p.y, best_p.z};
+        double uv[2] = {0, 0};
+        int k = 0;
+        for (int axis = 0; axis < 3; ++axis) {
+          if (axis == drop) continue;
+          uv[k++] = pt[axis];
+        }
+        const long long pu = (long long)floor(uv[0] / p[8]);
+        const long long pv = (long long)floor(uv[1] / p[8]);
+        if (((pu + pv) & 1) != 0)
+          for (int ch = 0; ch < 3; ++ch) a3[ch] *= 0.35f;
+      }
+      alb[0] = a3[0];
+      alb[1] = a3[1];
+      alb[2] = a3[2];
+    }
+  }
+  const bool valid = best_t < __longlong_as_double(0x7ff0000000000000ll);
+  if (depth) depth[pix] = valid ? (float)best_t : 0.0f;
+  if (rgb) {
+    uint8_t* o = rgb + 3 * (size_t)pix;
+    if (!valid) {
+      o[0] = o[1] = o[2] = 0;
+      return;
+    }
+    // light = (0.3, -0.7, -0.5).normalized()
+    const double l0 = 0.3, l1 = -0.7, l2 = -0.5;
+    const double ll = sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+    const D3 light = mk(l0 / ll, l1 / ll, l2 / ll);
+    const double dd = best_n.x * -light.x + best_n.y * -light.y + best_n.z * -light.z;
+    const float shade = 0.3f + 0.7f * (float)(0.0 < dd ? dd : 0.0);
+    for (int ch = 0; ch < 3; ++ch) {
+      const float cv = alb[ch] * shade * 255.0f;
+      o[ch] = (uint8_t)__float2int_rz(cv < 255.f ? cv : 255.f);
+    }
+  }
+}
+
+// VoxelS{} / VoxelSRgb{}: sdf 32767, weights 0 (voxel.hpp:29-46).
+__global__ void k_fill_voxels(uint32_t* __restrict__ vox, size_t n_voxels, int words_per_voxel) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_voxels; i += (size_t)gridDim.x * blockDim.x) {
+    vox[i * words_per_voxel] = 0x00007FFFu;
+    if (words_per_voxel == 2) vox[i * 2 + 1] = 0u;
+  }
+}
+
+// Compact list of allocated / swapped-out entries after vf_import_state.
+__global__ void k_rebuild_alloc_list(const HashEntry* __restrict__ entries, int n, int* __restrict__ alloc_list,
+                                     int cap, Counters* __restrict__ ctr) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const HashEntry e = load_entry(entries + i);
+    if (e.block_state >= kEntrySwappedOut) {
+      const int pos = warp_aggregated_add(&ctr->alloc_count);
+      if (pos < cap) alloc_list[pos] = i;
+    }
+  }
+}
+
+__global__ void k_init_ranges(float2* ranges, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    ranges[i] = make_float2(3.402823466e+38f, 0.0f);
+}
+
+__global__ void k_reset_visible(Counters* ctr) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) ctr->visible_count = 0;
+}
+
+}  // namespace vf

@@ -1,0 +1,292 @@
+// K3 — expected-depth range image (K3a) and the hash-walking raycast that
+// produces the point / normal maps (K3b).
+//
+// Reference: create_expected_depths (proj/include/voxfuse/engine/raycast.hpp:268-363),
+// cast_ray / trilinear_sdf / sdf_surface_normal / render_maps (raycast.hpp:102-162,
+// :171-263, :415-435).
+//
+// K3a folds each visible block's fragment box into the 16x16-fragment range
+// image with integer atomicMin / atomicMax on the float bit patterns (all
+// values are positive, so integer order is float order); min/max commute, so
+// the result equals the reference's serial fold.
+//
+// K3b: one CTA per 16x16 fragment (one range per CTA), one thread per pixel.
+// The reference probes the hash table for every voxel sample (1 per march
+// step, 8 per trilinear, 48 per normal).  Each thread keeps a 4-entry cache
+// of block -> VBA slot (misses included) in registers; the table does not
+// change during the raycast, so the values read — and therefore every
+// floating-point decision — are identical to the uncached reference.
+#include "vf_device.cuh"
+#include "vf_kernels.h"
+
+namespace vf {
+
+// K3a
+__global__ void __launch_bounds__(256) k_ranges(const HashEntry* __restrict__ entries,
+                                                const int* __restrict__ visible_list, const Counters* __restrict__ ctr,
+                                                const FrameParams* __restrict__ fp, IntrD in, float vs, float near_clip,
+                                                float far_clip, float2* __restrict__ ranges, int frag_w) {
+  __shared__ PoseD s_w2c;
+  if (threadIdx.x < sizeof(PoseD) / sizeof(double))
+    reinterpret_cast<double*>(&s_w2c)[threadIdx.x] = reinterpret_cast<const double*>(&fp->w2c)[threadIdx.x];
+  __syncthreads();
+  const int n = ctr->visible_count;
+  const double nearc = near_clip, farc = far_clip;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const HashEntry e = load_entry(entries + __ldg(visible_list + i));
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    double zmin = inf, zmax = -inf, xmin = inf, xmax = -inf, ymin = inf, ymax = -inf;
+    bool behind = false;
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner) {
+      const D3 w = mk((double)((float)(e.x * kBlockSide + ((corner & 1) ? kBlockSide : 0)) * vs),
+                      (double)((float)(e.y * kBlockSide + ((corner & 2) ? kBlockSide : 0)) * vs),
+                      (double)((float)(e.z * kBlockSide + ((corner & 4) ? kBlockSide : 0)) * vs));
+      const D3 cam = apply(s_w2c, w);
+      zmin = cam.z < zmin ? cam.z : zmin;
+      zmax = zmax < cam.z ? cam.z : zmax;
+      if (cam.z <= 1e-6) {
+        behind = true;
+        continue;
+      }
+      const double u = in.fx * cam.x / cam.z + in.cx;
+      const double v = in.fy * cam.y / cam.z + in.cy;
+      xmin = u < xmin ? u : xmin;
+      xmax = xmax < u ? u : xmax;
+      ymin = v < ymin ? v : ymin;
+      ymax = ymax < v ? v : ymax;
+    }
+    if (behind || !(zmax > nearc && zmin < farc)) continue;
+    int px0 = __double2int_rz(floor(xmin));
+    px0 = px0 < 0 ? 0 : px0;
+    int px1 = __double2int_rz(ceil(xmax));
+    px1 = in.width - 1 < px1 ? in.width - 1 : px1;
+    int py0 = __double2int_rz(floor(ymin));
+    py0 = py0 < 0 ? 0 : py0;
+    int py1 = __double2int_rz(ceil(ymax));
+    py1 = in.height - 1 < py1 ? in.height - 1 : py1;
+    if (!(px0 <= px1 && py0 <= py1)) continue;
+    const float fzmin = (float)(zmin < nearc ? nearc : zmin);
+    const float fzmax = (float)(farc < zmax ? farc : zmax);
+    const int imin = __float_as_int(fzmin), imax = __float_as_int(fzmax);
+    for (int fy = py0 / kFragmentSize; fy <= py1 / kFragmentSize; ++fy)
+      for (int fx = px0 / kFragmentSize; fx <= px1 / kFragmentSize; ++fx) {
+        int* r = reinterpret_cast<int*>(ranges + fy * frag_w + fx);
+        atomicMin(r, imin);
+        atomicMax(r + 1, imax);
+      }
+  }
+}
+
+namespace {
+
+// Register-resident 4-entry cache of block position -> VBA slot (or -1).
+struct BlockCache {
+  int bx[4], by[4], bz[4], slot[4];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      bx[i] = 0x7fffffff;
+      by[i] = bz[i] = 0;
+      slot[i] = -1;
+    }
+  }
+  __device__ __forceinline__ int lookup(const HashView& hv, int x, int y, int z) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (bx[i] == x && by[i] == y && bz[i] == z) return slot[i];
+    const int s = find_slot(hv, x, y, z);
+#pragma unroll
+    for (int i = 3; i > 0; --i) {
+      bx[i] = bx[i - 1];
+      by[i] = by[i - 1];
+      bz[i] = bz[i - 1];
+      slot[i] = slot[i - 1];
+    }
+    bx[0] = x;
+    by[0] = y;
+    bz[0] = z;
+    slot[0] = s;
+    return s;
+  }
+};
+
+struct Sampler {
+  HashView hv;
+  const uint32_t* vox;  // first 4 bytes of each voxel: sdf (lo 16), w_depth (byte 2)
+  int stride;           // 32-bit words per voxel: 1 (VoxelS) or 2 (VoxelSRgb)
+  BlockCache cache;
+
+  // HashSdfSampler::read (raycast.hpp:73-76)
+  __device__ __forceinline__ bool read(int vx, int vy, int vz, float& value) {
+    const int s = cache.lookup(hv, vx >> 3, vy >> 3, vz >> 3);
+    if (s < 0) {
+      value = 1.0f;  // sdf_to_float(32767)
+      return false;
+    }
+    const int lin = (vx & 7) + (vy & 7) * kBlockSide + (vz & 7) * kBlockSide * kBlockSide;
+    const uint32_t raw = __ldg(vox + ((size_t)s * kBlockVolume + lin) * stride);
+    value = sdf_to_float((int16_t)(raw & 0xFFFFu));
+    return ((raw >> 16) & 0xFFu) > 0;
+  }
+
+  // trilinear_sdf (raycast.hpp:102-117)
+  __device__ __forceinline__ bool trilinear(F3 p, float& out) {
+    const float qx = p.x - 0.5f, qy = p.y - 0.5f, qz = p.z - 0.5f;
+    const int bx = __float2int_rz(floorf(qx)), by = __float2int_rz(floorf(qy)), bz = __float2int_rz(floorf(qz));
+    const float fx = qx - (float)bx, fy = qy - (float)by, fz = qz - (float)bz;
+    float value = 0.0f;
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner) {
+      const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+      float v;
+      if (!read(bx + dx, by + dy, bz + dz, v)) {
+        out = 1.0f;
+        return false;
+      }
+      const float w = (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz);
+      value += w * v;
+    }
+    out = value;
+    return true;
+  }
+
+  // sdf_surface_normal (raycast.hpp:147-162)
+  __device__ __forceinline__ bool normal(F3 p, F3& n) {
+    float g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      F3 lo = p, hi = p;
+      if (a == 0) {
+        lo.x -= 1.0f;
+        hi.x += 1.0f;
+      } else if (a == 1) {
+        lo.y -= 1.0f;
+        hi.y += 1.0f;
+      } else {
+        lo.z -= 1.0f;
+        hi.z += 1.0f;
+      }
+      float vlo, vhi;
+      const bool ok_lo = trilinear(lo, vlo);
+      const bool ok_hi = ok_lo && trilinear(hi, vhi);
+      if (!ok_lo || !ok_hi) return false;
+      g[a] = vhi - vlo;
+    }
+    const float len = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (len < 1e-12f) return false;
+    n = F3{g[0] / len, g[1] / len, g[2] / len};
+    return true;
+  }
+};
+
+}  // namespace
+
+// K3b: render_maps (raycast.hpp:415-435) with cast_ray (:171-263) per pixel.
+__global__ void __launch_bounds__(256) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
+                                                 const float2* __restrict__ ranges, const FrameParams* __restrict__ fp,
+                                                 IntrD in, float vs, float mu, float4* __restrict__ points,
+                                                 float4* __restrict__ normals) {
+  __shared__ PoseD s_c2w;
+  if (threadIdx.x < sizeof(PoseD) / sizeof(double))
+    reinterpret_cast<double*>(&s_c2w)[threadIdx.x] = reinterpret_cast<const double*>(&fp->c2w)[threadIdx.x];
+  __syncthreads();
+  const int x = blockIdx.x * kFragmentSize + (threadIdx.x & 15);
+  const int y = blockIdx.y * kFragmentSize + (threadIdx.x >> 4);
+  if (x >= in.width || y >= in.height) return;
+  const size_t pix = (size_t)y * in.width + x;
+  float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float2 range = ranges[blockIdx.y * gridDim.x + blockIdx.x];
+  Sampler smp{hv, vox, vstride, {}};
+  smp.cache.init();
+  bool hit = false;
+  F3 hw{0.f, 0.f, 0.f};
+  if (range.x <= range.y) {  // RangeImage::valid
+    const double inv_vox = 1.0 / (double)vs;
+    const D3 dir_cam = mk((x - in.cx) / in.fx, (y - in.cy) / in.fy, 1.0);
+    const double r0 = range.x, r1 = range.y;
+    const D3 s0 = apply(s_c2w, mk(dir_cam.x * r0, dir_cam.y * r0, dir_cam.z * r0));
+    const D3 e0 = apply(s_c2w, mk(dir_cam.x * r1, dir_cam.y * r1, dir_cam.z * r1));
+    const F3 start{(float)(s0.x * inv_vox), (float)(s0.y * inv_vox), (float)(s0.z * inv_vox)};
+    const F3 end{(float)(e0.x * inv_vox), (float)(e0.y * inv_vox), (float)(e0.z * inv_vox)};
+    F3 dir{end.x - start.x, end.y - start.y, end.z - start.z};
+    const float total = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
+    if (total > 0) {
+      dir = F3{dir.x / total, dir.y / total, dir.z / total};
+      const float mu_vox = mu / vs;
+      const float fine_step = (8.0f < mu_vox) ? 8.0f : mu_vox;
+      int state = 0;  // 0 coarse, 1 fine, 2 surface
+      float t = 0.0f, t_front = -1.0f, sdf_front = 1.0f;
+      while (t <= total) {
+        const F3 p{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
+        float value;
+        const bool found = smp.read(__float2int_rz(floorf(p.x)), __float2int_rz(floorf(p.y)),
+                                    __float2int_rz(floorf(p.z)), value);
+        if (state == 0) {
+          if (!found) {
+            t += 8.0f;
+            continue;
+          }
+          state = 1;
+          const float tb = t - 8.0f;
+          t = (0.0f < tb) ? tb : 0.0f;
+          continue;
+        }
+        if (!found) {
+          if (state == 2) state = 1;
+          t_front = -1.0f;
+          t += fine_step;
+          continue;
+        }
+        float sdf = value;
+        if (state == 1 && sdf <= 0.0f) break;  // WRONG_SIDE
+        state = 2;
+        if (sdf <= 0.1f && sdf >= -0.5f) {
+          float tri;
+          if (smp.trilinear(p, tri)) sdf = tri;
+        }
+        if (sdf <= 0.0f) {
+          if (t_front >= 0.0f && sdf_front > sdf && t - t_front <= 2.0f * mu_vox) {
+            t = t + (t_front - t) * sdf / (sdf - sdf_front);
+          } else {
+            t += sdf * mu_vox;
+          }
+          float t_back = t, sdf_back = sdf;
+          for (int i = 0; i < 2; ++i) {
+            float tri;
+            if (!smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t}, tri)) break;
+            const float denom = sdf_back - tri;
+            if (fabsf(denom) > 1e-12f && fabsf(t_back - t) > 1e-6f) {
+              const float slope = denom / (t_back - t);
+              t_back = t;
+              sdf_back = tri;
+              t -= tri / (fabsf(slope) > 1e-6f ? slope : 1.0f / mu_vox);
+            } else {
+              t += tri * mu_vox;
+            }
+          }
+          const F3 h{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
+          hw = F3{h.x * vs, h.y * vs, h.z * vs};
+          hit = true;
+          break;
+        }
+        t_front = t;
+        sdf_front = sdf;
+        const float a = sdf * mu_vox;
+        const float b = (a < 1.0f) ? 1.0f : a;
+        t += (mu_vox < b) ? mu_vox : b;
+      }
+    }
+  }
+  if (hit) {
+    F3 n;
+    if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
+      out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
+      out_n = make_float4(n.x, n.y, n.z, 1.0f);
+    }
+  }
+  points[pix] = out_p;
+  normals[pix] = out_n;
+}
+
+}  // namespace vf

@@ -1,0 +1,424 @@
+"""Host-side mirror of the reference's engine interface over the C ABI.
+
+Names, argument order and meaning follow the reference:
+
+* ``make_pipeline(settings, calib)`` -> ``Pipeline`` (IPipeline,
+  proj/include/voxfuse/engine/pipeline.hpp:66-86);
+* ``Pipeline.process_frame(rgb, depth_m)`` -> ``FrameStats`` (pipeline.hpp:70);
+* ``pose()``, ``frame_count()``, ``settings()``, ``tracking_state()``,
+  ``volume_digest()``;
+* stage functions mirroring the stage templates (allocation.hpp,
+  integration.hpp, raycast.hpp, pyramid.hpp, depth_tracker.hpp) for
+  stage-isolated use.
+
+All compute runs in the sm_100a library; this module only marshals buffers.
+Construction fails with ``VoxfuseError(VF_ERR_NO_DEVICE)`` without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import VfAllocStats, VfCalib, VfFrameStats, VfIntrinsics, VfSettings, check
+
+ENTRY_DTYPE = np.dtype(
+    [("x", "<i2"), ("y", "<i2"), ("z", "<i2"), ("pad", "<i2"), ("offset", "<i4"), ("block_state", "<i4")]
+)
+VOXEL_TYPE_S = 1
+VOXEL_TYPE_S_RGB = 2
+
+
+@dataclass
+class Intrinsics:
+    """Intrinsics (proj/include/voxfuse/core/intrinsics.hpp:10-32)."""
+
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+    def to_c(self) -> VfIntrinsics:
+        return VfIntrinsics(self.fx, self.fy, self.cx, self.cy, self.width, self.height)
+
+
+@dataclass
+class Calibration:
+    """Calibration (proj/include/voxfuse/io/calibration.hpp:31-36)."""
+
+    depth: Intrinsics
+    rgb: Intrinsics | None = None
+    rgb_to_depth: np.ndarray = field(default_factory=lambda: np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0], float))
+    disparity_a: float = 0.0
+    disparity_b: float = 0.0
+
+    def to_c(self) -> VfCalib:
+        c = VfCalib()
+        c.depth = self.depth.to_c()
+        c.rgb = (self.rgb or self.depth).to_c()
+        for i, v in enumerate(np.asarray(self.rgb_to_depth, float).reshape(-1)):
+            c.rgb_to_depth[i] = float(v)
+        c.disparity_a = self.disparity_a
+        c.disparity_b = self.disparity_b
+        return c
+
+
+@dataclass
+class EngineSettings:
+    """EngineSettings + SceneParams + HashConfig + TrackerSettings with the
+    reference defaults (pipeline.hpp:19-41, scene_params.hpp:6-13,
+    hash_volume.hpp:49-58, tracking_state.hpp:12-23)."""
+
+    voxel_type: int = VOXEL_TYPE_S
+    voxel_size: float = 0.004
+    mu: float = 0.02
+    max_weight: int = 100
+    stop_integrating_at_max: bool = False
+    bucket_count: int = 1 << 20
+    bucket_size: int = 2
+    excess_count: int = 1 << 17
+    block_count: int = 1 << 18
+    near_clip: float = 0.1
+    far_clip: float = 8.0
+    visibility_margin_px: int = 8
+    swap_margin_px: int = 48
+    hierarchy_levels: int = 5
+    rotation_only_levels: int = 2
+    max_iterations: int = 20
+    min_valid_points: int = 30
+    icp_dist_threshold: float = 0.1
+    convergence_eps: float = 1e-5
+    max_condition: float = 1e8
+    tracking: bool = True
+    use_graphs: bool = True
+
+    def to_c(self) -> VfSettings:
+        s = VfSettings()
+        for name, _ in VfSettings._fields_:
+            v = getattr(self, name)
+            setattr(s, name, int(v) if isinstance(v, bool) else v)
+        return s
+
+    @property
+    def entry_count(self) -> int:
+        return self.bucket_count * self.bucket_size + self.excess_count
+
+
+def settings_from_config(cfg) -> tuple[EngineSettings, Calibration]:
+    """EngineSettings + Calibration for a paper_1410_0925_b200.scene.BenchConfig."""
+    fx, fy, cx, cy, w, h = cfg.intrinsics
+    s = EngineSettings(
+        voxel_type=cfg.voxel_type, voxel_size=cfg.voxel_size, mu=cfg.mu, max_weight=cfg.max_weight,
+        bucket_count=cfg.hash.bucket_count, bucket_size=cfg.hash.bucket_size, excess_count=cfg.hash.excess_count,
+        block_count=cfg.hash.block_count, near_clip=cfg.near_clip, far_clip=cfg.far_clip,
+        visibility_margin_px=cfg.margin_px, swap_margin_px=cfg.swap_margin_px, hierarchy_levels=cfg.levels,
+        rotation_only_levels=cfg.rotation_only_levels, max_iterations=cfg.max_iterations,
+        min_valid_points=cfg.min_valid_points, icp_dist_threshold=cfg.icp_dist_threshold,
+        convergence_eps=cfg.convergence_eps, max_condition=cfg.max_condition, tracking=cfg.tracking,
+    )
+    intr = Intrinsics(fx, fy, cx, cy, w, h)
+    return s, Calibration(depth=intr, rgb=intr)
+
+
+@dataclass
+class FrameStats:
+    """FrameStats (pipeline.hpp:45-58)."""
+
+    frame: int
+    tracking_ok: bool
+    tracking_iterations: int
+    tracking_cost: float
+    blocks_allocated: int
+    allocation_dropped: int
+    visible_blocks: int
+    pose: np.ndarray
+    ms_total: float
+    allocation_requested: int = 0
+    allocated_total: int = 0
+    tracking_valid_points: int = 0
+    error_flags: int = 0
+
+    @classmethod
+    def from_c(cls, s: VfFrameStats) -> "FrameStats":
+        return cls(s.frame, bool(s.tracking_ok), s.tracking_iterations, s.tracking_cost, s.blocks_allocated,
+                   s.allocation_dropped, s.visible_blocks, np.array(s.pose[:]), s.ms_total, s.allocation_requested,
+                   s.allocated_total, s.tracking_valid_points, s.error_flags)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f32(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if shape is not None and a.size != int(np.prod(shape)):
+        raise ValueError(f"expected {shape}, got {a.shape}")
+    return a
+
+
+def _pose(p):
+    p = np.ascontiguousarray(p, dtype=np.float64).reshape(-1)
+    if p.size != 12:
+        raise ValueError("pose must be 12 doubles: row-major R then t")
+    return p
+
+
+class Pipeline:
+    """IPipeline over one device-resident voxel-block hash volume."""
+
+    def __init__(self, settings: EngineSettings, calib: Calibration, device: int = 0):
+        self._L = _abi.load()
+        self._settings = settings
+        self._calib = calib
+        self._c_settings = settings.to_c()
+        self._c_calib = calib.to_c()
+        h = C.c_void_p()
+        check("vf_create", self._L.vf_create(C.byref(self._c_settings), C.byref(self._c_calib), device, C.byref(h)))
+        self._h = h
+        self.width, self.height = calib.depth.width, calib.depth.height
+        rgb = calib.rgb or calib.depth
+        self.rgb_width, self.rgb_height = rgb.width, rgb.height
+
+    # -- lifecycle --
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.vf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _chk(self, fn, rc):
+        return check(fn, rc, self._h)
+
+    # -- IPipeline --
+    def process_frame(self, rgb, depth_m) -> FrameStats:
+        """IPipeline::process_frame(rgb*, depth_m) with host arrays."""
+        d = _f32(depth_m, (self.height, self.width))
+        c = None if rgb is None else np.ascontiguousarray(rgb, dtype=np.uint8)
+        st = VfFrameStats()
+        self._chk("vf_process_frame", self._L.vf_process_frame(self._h, _ptr(d), _ptr(c), C.byref(st)))
+        return FrameStats.from_c(st)
+
+    def process_frame_device(self, d_depth: int, d_rgb: int | None = None, read_stats: bool = False):
+        """Inputs already in device memory (raw device pointers)."""
+        st = VfFrameStats() if read_stats else None
+        self._chk("vf_process_frame_device",
+                  self._L.vf_process_frame_device(self._h, C.c_void_p(d_depth),
+                                                  C.c_void_p(d_rgb) if d_rgb else None,
+                                                  C.byref(st) if st is not None else None))
+        return FrameStats.from_c(st) if st is not None else None
+
+    def synchronize(self):
+        self._chk("vf_synchronize", self._L.vf_synchronize(self._h))
+
+    def pose(self) -> np.ndarray:
+        out = np.zeros(12)
+        self._chk("vf_get_pose", self._L.vf_get_pose(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_pose(self, pose) -> None:
+        p = _pose(pose)
+        self._chk("vf_set_pose", self._L.vf_set_pose(self._h, p.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def frame_count(self) -> int:
+        return int(self._L.vf_frame_count(self._h))
+
+    def settings(self) -> EngineSettings:
+        return self._settings
+
+    def tracking_state(self):
+        """(points, normals) world-space maps, each H x W x 4 float32 (w = validity)."""
+        pts = np.zeros((self.height, self.width, 4), np.float32)
+        nrm = np.zeros((self.height, self.width, 4), np.float32)
+        self._chk("vf_get_maps", self._L.vf_get_maps(self._h, _ptr(pts), _ptr(nrm)))
+        return pts, nrm
+
+    def set_maps(self, points, normals, render_pose) -> None:
+        p = _f32(points, (self.height, self.width, 4))
+        n = _f32(normals, (self.height, self.width, 4))
+        rp = _pose(render_pose)
+        self._chk("vf_set_maps", self._L.vf_set_maps(self._h, _ptr(p), _ptr(n),
+                                                     rp.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def volume_digest(self) -> int:
+        out = C.c_uint64()
+        self._chk("vf_volume_digest", self._L.vf_volume_digest(self._h, C.byref(out)))
+        return int(out.value)
+
+    # -- state export / import --
+    def entries(self) -> np.ndarray:
+        out = np.zeros(self._L.vf_entry_count(self._h), ENTRY_DTYPE)
+        self._chk("vf_export_entries", self._L.vf_export_entries(self._h, _ptr(out)))
+        return out
+
+    def voxels(self) -> np.ndarray:
+        out = np.zeros(self._L.vf_voxel_bytes(self._h), np.uint8)
+        self._chk("vf_export_voxels", self._L.vf_export_voxels(self._h, _ptr(out)))
+        return out
+
+    def free_stacks(self):
+        s = self._settings
+        vs = np.zeros(s.block_count, np.int32)
+        es = np.zeros(s.excess_count, np.int32)
+        vt, et = C.c_int(), C.c_int()
+        self._chk("vf_export_free_stacks",
+                  self._L.vf_export_free_stacks(self._h, C.byref(vt), _ptr(vs), C.byref(et), _ptr(es)))
+        return vt.value, vs, et.value, es
+
+    def import_state(self, entries, voxels, vba_top, vba_slots, excess_top, excess_slots) -> None:
+        e = np.ascontiguousarray(entries)
+        v = np.ascontiguousarray(voxels)
+        vs = np.ascontiguousarray(vba_slots, np.int32)
+        es = np.ascontiguousarray(excess_slots, np.int32)
+        self._chk("vf_import_state", self._L.vf_import_state(self._h, _ptr(e), _ptr(v), int(vba_top), _ptr(vs),
+                                                             int(excess_top), _ptr(es)))
+
+    def visible_list(self) -> np.ndarray:
+        n = self._L.vf_export_visible_list(self._h, None, 0)
+        self._chk("vf_export_visible_list", n)
+        out = np.zeros(n, np.int32)
+        if n:
+            self._L.vf_export_visible_list(self._h, _ptr(out), n)
+        return out
+
+    def ranges(self) -> np.ndarray:
+        n = self._L.vf_export_ranges(self._h, None)
+        out = np.zeros((n, 2), np.float32)
+        self._chk("vf_export_ranges", self._L.vf_export_ranges(self._h, _ptr(out)))
+        return out
+
+    # -- stage templates --
+    def allocate(self, depth_m, pose) -> VfAllocStats:
+        """mark_blocks + perform_allocations + build_visible_list."""
+        d = _f32(depth_m, (self.height, self.width))
+        p = _pose(pose)
+        st = VfAllocStats()
+        self._chk("vf_stage_allocate", self._L.vf_stage_allocate(self._h, _ptr(d), p.ctypes.data_as(
+            C.POINTER(C.c_double)), C.byref(st)))
+        return st
+
+    def integrate(self, depth_m, rgb, pose) -> None:
+        """integrate_frame over the current visible list."""
+        d = _f32(depth_m, (self.height, self.width))
+        c = None if rgb is None else np.ascontiguousarray(rgb, dtype=np.uint8)
+        p = _pose(pose)
+        self._chk("vf_stage_integrate", self._L.vf_stage_integrate(self._h, _ptr(d), _ptr(c),
+                                                                   p.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def raycast(self, pose) -> None:
+        """create_expected_depths + render_maps."""
+        p = _pose(pose)
+        self._chk("vf_stage_raycast", self._L.vf_stage_raycast(self._h, p.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def icp_track(self, depth_m):
+        """build_depth_pyramid + icp_track against the current maps and pose."""
+        d = _f32(depth_m, (self.height, self.width))
+        pose = np.zeros(12)
+        it, valid, ok = C.c_int(), C.c_int(), C.c_int()
+        cost = C.c_double()
+        self._chk("vf_stage_icp", self._L.vf_stage_icp(self._h, _ptr(d), pose.ctypes.data_as(C.POINTER(C.c_double)),
+                                                       C.byref(it), C.byref(cost), C.byref(valid), C.byref(ok)))
+        return dict(pose=pose, ok=bool(ok.value), iterations=it.value, cost=cost.value, valid_points=valid.value)
+
+    def icp_trace(self) -> np.ndarray:
+        n = self._L.vf_icp_trace(self._h, None, 0)
+        out = np.zeros((max(n, 0), 32))
+        if n > 0:
+            self._L.vf_icp_trace(self._h, _ptr(out), n)
+        return out
+
+    def depth_pyramid(self, depth_m) -> list:
+        d = _f32(depth_m, (self.height, self.width))
+        sizes, w, h = [], self.width, self.height
+        for _ in range(self._settings.hierarchy_levels):
+            sizes.append((h, w))
+            w, h = (w + 1) // 2, (h + 1) // 2
+        out = np.zeros(sum(a * b for a, b in sizes), np.float32)
+        self._chk("vf_depth_pyramid", self._L.vf_depth_pyramid(self._h, _ptr(d), _ptr(out)))
+        res, off = [], 0
+        for hh, ww in sizes:
+            res.append(out[off:off + hh * ww].reshape(hh, ww))
+            off += hh * ww
+        return res
+
+    # -- profiling --
+    def set_profiling(self, enabled: bool) -> None:
+        self._chk("vf_set_profiling", self._L.vf_set_profiling(self._h, int(enabled)))
+
+    def stage_times(self):
+        ms = np.zeros(8)
+        n = C.c_long()
+        self._chk("vf_stage_times", self._L.vf_stage_times(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                                           C.byref(n)))
+        return ms, n.value
+
+    def kernel_launches_per_frame(self, tracking_frame: bool) -> int:
+        return self._chk("vf_kernel_launches_per_frame",
+                         self._L.vf_kernel_launches_per_frame(self._h, int(tracking_frame)))
+
+
+def make_pipeline(settings: EngineSettings, calib: Calibration, device: int = 0) -> Pipeline:
+    """make_pipeline (pipeline.hpp:86; src/pipeline_factory.cpp:18-30), hash backend."""
+    return Pipeline(settings, calib, device)
+
+
+# ---------------------------------------------------------------------------
+# device buffers + synthetic input rendering (bench inputs, no torch needed)
+# ---------------------------------------------------------------------------
+class DeviceBuffer:
+    def __init__(self, nbytes: int):
+        L = _abi.load()
+        self.nbytes = int(nbytes)
+        self.ptr = L.vf_device_alloc(self.nbytes)
+        if not self.ptr:
+            raise _abi.VoxfuseError("vf_device_alloc", _abi.VF_ERR_CUDA)
+
+    def free(self):
+        if self.ptr:
+            _abi.load().vf_device_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def to_host(self, dtype, shape) -> np.ndarray:
+        out = np.zeros(shape, dtype)
+        check("vf_memcpy_d2h", _abi.load().vf_memcpy_d2h(_ptr(out), C.c_void_p(self.ptr), out.nbytes))
+        return out
+
+    def from_host(self, arr: np.ndarray) -> None:
+        a = np.ascontiguousarray(arr)
+        check("vf_memcpy_h2d", _abi.load().vf_memcpy_h2d(C.c_void_p(self.ptr), _ptr(a), a.nbytes))
+
+
+def render_synthetic(pose, intr: Intrinsics, spheres, planes, d_depth: int, d_rgb: int | None = None,
+                     near: float = 0.05, far: float = 100.0, device: int = 0) -> None:
+    """render_synthetic_depth / _rgb (proj/src/synthetic.cpp) on the GPU into device buffers."""
+    sp = np.ascontiguousarray(spheres, np.float64)
+    pl = np.ascontiguousarray(planes, np.float64)
+    p = _pose(pose)
+    ci = intr.to_c()
+    check("vf_render_synthetic", _abi.load().vf_render_synthetic(
+        device, len(sp), _ptr(sp), len(pl), _ptr(pl), p.ctypes.data_as(C.POINTER(C.c_double)), C.byref(ci),
+        near, far, C.c_void_p(d_depth), C.c_void_p(d_rgb) if d_rgb else None))

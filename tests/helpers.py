@@ -1,0 +1,50 @@
+"""Shared helpers for the parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+
+import vf_py
+from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, trajectory
+
+ENTRY_FIELDS = ("x", "y", "z", "offset", "block_state")
+
+
+def frames(olib, cfg, n, rgb=False, amplitude=1.0):
+    poses = trajectory(n, amplitude)
+    out = []
+    for i in range(n):
+        d = vf_py.render_depth(olib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        c = vf_py.render_rgb(olib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) if rgb else None
+        out.append((poses[i], d, c))
+    return out
+
+
+def entries_equal(a, b):
+    return all(np.array_equal(a[f], b[f]) for f in ENTRY_FIELDS)
+
+
+def voxel_payload(v: np.ndarray, vsize: int) -> np.ndarray:
+    """Voxel bytes without the padding byte (sizeof VoxelS = 4, VoxelSRgb = 8)."""
+    v = v.reshape(-1, vsize)
+    return v[:, : vsize - 1]
+
+
+def allocated_blocks(entries, voxels, vsize):
+    """{(x,y,z): voxel payload bytes} for all allocated entries — layout-independent."""
+    pay = voxel_payload(voxels, vsize).reshape(-1, 512, vsize - 1)
+    out = {}
+    for e in entries[entries["block_state"] >= 0]:
+        out[(int(e["x"]), int(e["y"]), int(e["z"]))] = pay[int(e["block_state"])]
+    return out
+
+
+def rot_angle(p, q):
+    """Angle (rad) between the rotations of two 12-double poses."""
+    ra, rb = np.asarray(p[:9]).reshape(3, 3), np.asarray(q[:9]).reshape(3, 3)
+    return float(2.0 * np.arcsin(min(1.0, np.linalg.norm(ra - rb) / np.sqrt(8.0))))
+
+
+def centre_dist(p, q):
+    ra, rb = np.asarray(p[:9]).reshape(3, 3), np.asarray(q[:9]).reshape(3, 3)
+    ca, cb = -ra.T @ np.asarray(p[9:]), -rb.T @ np.asarray(q[9:])
+    return float(np.linalg.norm(ca - cb))
