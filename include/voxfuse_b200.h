@@ -159,11 +159,14 @@ int vf_stage_integrate(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb, co
 /* create_expected_depths + render_maps (raycast.hpp:268-435) over the current visible list */
 int vf_stage_raycast(vf_ctx* ctx, const double pose[12]);
 /* build_depth_pyramid + icp_track (pyramid.hpp:101-111, depth_tracker.hpp:115-239)
- * against the current maps; the current pose is the render pose. */
-int vf_stage_icp(vf_ctx* ctx, const float* depth_m, double out_pose[12], int* iterations, double* cost,
-                 int* valid_points, int* ok);
-/* Per-iteration ICP sums of the last track: rows of 32 doubles
- * (level, iter, 21 H, 6 g, cost, count, 0). Returns the row count. */
+ * against the current maps; the current pose is the render pose;
+ * initial_pose (nullable) is icp_track's `initial` argument.  Like the
+ * reference's icp_track it does not change the context's pose. */
+int vf_stage_icp(vf_ctx* ctx, const float* depth_m, const double initial_pose[12], double out_pose[12],
+                 int* iterations, double* cost, int* valid_points, int* ok);
+/* Per-iteration ICP sums of the last track: rows of 48 doubles
+ * (level, iter, 21 H, 6 g, cost, count, rotation_only, evaluation camera-to-world
+ * pose (12), 4 phase timers in SM cycles). Returns the row count. */
 long vf_icp_trace(vf_ctx* ctx, double* out, long max_rows);
 /* Depth pyramid levels 0..levels-1 back to back (pyramid.hpp:101-111). */
 int vf_depth_pyramid(vf_ctx* ctx, const float* depth_m, float* out);

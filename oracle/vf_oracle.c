@@ -1083,19 +1083,25 @@ static int well_conditioned(const double* h, int n, double max_condition) {
   return smin > 0 && smax / smin < max_condition;
 }
 
-static void trace_row(vfo_ctx* c, int level, int iter, const icp_acc_t* t) {
+#define TRACE_ROW 48
+/* trace row: level, iter, 21 H, 6 g, cost, count, rotation_only, evaluation
+ * camera-to-world pose (12), 4 unused */
+static void trace_row(vfo_ctx* c, int level, int iter, const icp_acc_t* t, int rot_only, const pose_t* c2w) {
   if (c->trace_rows >= c->trace_cap) {
     c->trace_cap = c->trace_cap ? c->trace_cap * 2 : 128;
-    c->trace = (double*)realloc(c->trace, sizeof(double) * 32 * (size_t)c->trace_cap);
+    c->trace = (double*)realloc(c->trace, sizeof(double) * TRACE_ROW * (size_t)c->trace_cap);
   }
-  double* r = c->trace + 32 * c->trace_rows++;
+  double* r = c->trace + TRACE_ROW * c->trace_rows++;
+  memset(r, 0, sizeof(double) * TRACE_ROW);
   r[0] = level;
   r[1] = iter;
   memcpy(r + 2, t->h, sizeof(t->h));
   memcpy(r + 23, t->g, sizeof(t->g));
   r[29] = t->cost;
   r[30] = (double)t->count;
-  r[31] = 0;
+  r[31] = rot_only;
+  memcpy(r + 32, c2w->r, sizeof(c2w->r));
+  memcpy(r + 41, c2w->t, sizeof(c2w->t));
 }
 
 typedef struct {
@@ -1105,9 +1111,10 @@ typedef struct {
 } track_result_t;
 
 /* icp_track (depth_tracker.hpp:115-239); pyramid levels back to back */
-static track_result_t icp_track(vfo_ctx* c, const float* pyr, const intr_t* intrs, int levels) {
+static track_result_t icp_track(vfo_ctx* c, const float* pyr, const intr_t* intrs, int levels,
+                                const pose_t* initial) {
   track_result_t res;
-  res.pose = c->pose;
+  res.pose = initial ? *initial : c->pose; /* result.pose = initial ? *initial : state.pose */
   res.ok = 0;
   res.iterations = 0;
   res.valid_points = 0;
@@ -1164,7 +1171,7 @@ static track_result_t icp_track(vfo_ctx* c, const float* pyr, const intr_t* intr
           }
         acc_merge(&total, &acc);
       }
-      trace_row(c, level, iter, &total);
+      trace_row(c, level, iter, &total, rotation_only, &cam_to_world);
       if (total.count < c->cfg.min_valid_points) {
         res.valid_points = (int)total.count;
         break;
@@ -1321,7 +1328,7 @@ int vfo_stage_raycast(vfo_ctx* c, const double* pose) {
   return 0;
 }
 
-static track_result_t run_tracker(vfo_ctx* c, const float* depth) {
+static track_result_t run_tracker(vfo_ctx* c, const float* depth, const pose_t* initial) {
   const int levels = c->cfg.levels;
   intr_t intrs[8];
   intrs[0] = c->depth_intr;
@@ -1332,13 +1339,25 @@ static track_result_t run_tracker(vfo_ctx* c, const float* depth) {
   }
   float* pyr = (float*)malloc(sizeof(float) * total);
   vfo_depth_pyramid(depth, c->depth_intr.width, c->depth_intr.height, levels, pyr);
-  const track_result_t r = icp_track(c, pyr, intrs, levels);
+  const track_result_t r = icp_track(c, pyr, intrs, levels, initial);
   free(pyr);
   return r;
 }
 
+int vfo_stage_icp_init(vfo_ctx* c, const float* depth, const double* initial, double* out_pose, int* out_iters,
+                       double* out_cost, int* out_valid) {
+  pose_t init;
+  if (initial) init = pose_from(initial);
+  const track_result_t r = run_tracker(c, depth, initial ? &init : NULL);
+  pose_to(&r.pose, out_pose);
+  *out_iters = r.iterations;
+  *out_cost = r.final_cost;
+  *out_valid = r.valid_points;
+  return r.ok;
+}
+
 int vfo_stage_icp(vfo_ctx* c, const float* depth, double* out_pose, int* out_iters, double* out_cost, int* out_valid) {
-  const track_result_t r = run_tracker(c, depth);
+  const track_result_t r = run_tracker(c, depth, NULL);
   pose_to(&r.pose, out_pose);
   *out_iters = r.iterations;
   *out_cost = r.final_cost;
@@ -1355,7 +1374,7 @@ int vfo_process(vfo_ctx* c, const float* depth, const uint8_t* rgb, const double
   double t0 = now_ms();
   if (c->tracking) {
     if (c->frame > 0) { /* pipeline_impl.hpp:78-86 */
-      const track_result_t r = run_tracker(c, depth);
+      const track_result_t r = run_tracker(c, depth, NULL);
       s.tracking_ok = r.ok;
       s.tracking_iterations = r.iterations;
       s.tracking_cost = r.final_cost;
@@ -1435,7 +1454,7 @@ void vfo_free_stacks(const vfo_ctx* c, int* vba_top, int* vba_slots, int* excess
 }
 long vfo_icp_trace(const vfo_ctx* c, double* out, long max_rows) {
   const long n = c->trace_rows < max_rows ? c->trace_rows : max_rows;
-  if (out && n > 0) memcpy(out, c->trace, sizeof(double) * 32 * (size_t)n);
+  if (out && n > 0) memcpy(out, c->trace, sizeof(double) * TRACE_ROW * (size_t)n);
   return c->trace_rows;
 }
 

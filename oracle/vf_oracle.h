@@ -65,6 +65,9 @@ int vfo_stage_integrate(vfo_ctx* c, const float* depth, const uint8_t* rgb, cons
 int vfo_stage_raycast(vfo_ctx* c, const double* pose);
 int vfo_stage_icp(vfo_ctx* c, const float* depth, double* out_pose, int* out_iters, double* out_cost,
                   int* out_valid);
+/* icp_track(pyramid, state, settings, initial) with an explicit initial pose (depth_tracker.hpp:115-118) */
+int vfo_stage_icp_init(vfo_ctx* c, const float* depth, const double* initial, double* out_pose, int* out_iters,
+                       double* out_cost, int* out_valid);
 
 void vfo_get_pose(const vfo_ctx* c, double* out);
 void vfo_set_pose(vfo_ctx* c, const double* pose);
@@ -80,7 +83,8 @@ void vfo_free_stacks(const vfo_ctx* c, int* vba_top, int* vba_slots, int* excess
 uint64_t vfo_digest(const vfo_ctx* c);
 /* raycast counters of the last render: rays, samples, voxel reads, trilinear calls, coarse samples */
 long vfo_raycast_counters(long* out);
-/* last ICP solve trace: per accepted/evaluated iteration the 29 sums */
+/* last ICP solve trace: rows of 48 doubles (level, iter, 21 H, 6 g, cost, count,
+ * rotation_only, evaluation camera-to-world pose (12), 4 unused) */
 long vfo_icp_trace(const vfo_ctx* c, double* out, long max_rows);
 
 /* Free functions. */

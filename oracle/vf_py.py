@@ -166,6 +166,9 @@ class OracleLib(_Lib):
         L.vfo_stage_icp.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                     C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.vfo_stage_icp.restype = C.c_int
+        L.vfo_stage_icp_init.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        L.vfo_stage_icp_init.restype = C.c_int
         L.vfo_set_pose.argtypes = [C.c_void_p, C.c_void_p]
         L.vfo_set_maps.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.vfo_free_stacks.argtypes = [C.c_void_p] * 5

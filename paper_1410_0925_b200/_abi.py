@@ -154,7 +154,7 @@ def load() -> C.CDLL:
         "vf_stage_allocate": (C.c_int, [vp, vp, dp, C.POINTER(VfAllocStats)]),
         "vf_stage_integrate": (C.c_int, [vp, vp, vp, dp]),
         "vf_stage_raycast": (C.c_int, [vp, dp]),
-        "vf_stage_icp": (C.c_int, [vp, vp, dp, ip, dp, ip, ip]),
+        "vf_stage_icp": (C.c_int, [vp, vp, dp, dp, ip, dp, ip, ip]),
         "vf_icp_trace": (C.c_long, [vp, vp, C.c_long]),
         "vf_depth_pyramid": (C.c_int, [vp, vp, vp]),
         "vf_render_synthetic": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, vp, dp, C.POINTER(VfIntrinsics),

@@ -25,13 +25,13 @@ namespace {
 
 constexpr int kNumEvents = 16;
 constexpr int kTraceCap = 256;
-constexpr int kSmallPixels = 8192;
 
 // Everything the host reads back after a frame, contiguous for one D2H copy.
 struct DevState {
   Counters ctr;
   IcpResult icp;
   PoseD pose;
+  PoseD init_pose;  // optional ICP initial pose (vf_stage_icp)
   FrameParams fp;
   AllocMeta meta;
 };
@@ -98,7 +98,8 @@ struct vf_ctx {
   float4* points = nullptr;
   float4* normals = nullptr;
   double* partials = nullptr;
-  void* ctl_scratch = nullptr;
+  double* utab = nullptr;  // per level: (x - cx) / fx then (y - cy) / fy
+  std::vector<size_t> utab_off;
   double* trace = nullptr;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
@@ -137,7 +138,7 @@ namespace {
 
 HashView hash_view(vf_ctx* c) { return HashView{c->entries, c->mask, c->s.bucket_size, c->ordered}; }
 
-int launch_icp(vf_ctx* c, cudaStream_t st) {
+int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool update_state = true) {
   IcpArgs a{};
   const int L = c->s.hierarchy_levels;
   size_t off = 0;
@@ -145,6 +146,8 @@ int launch_icp(vf_ctx* c, cudaStream_t st) {
     const IntrD& in = c->levels[l];
     a.lv[l].depth = l == 0 ? c->depth : c->pyr + off;
     if (l > 0) off += (size_t)in.width * in.height;
+    a.lv[l].ux = c->utab + c->utab_off[l];
+    a.lv[l].uy = c->utab + c->utab_off[l] + in.width;
     a.lv[l].w = in.width;
     a.lv[l].h = in.height;
     a.lv[l].fx = in.fx;
@@ -163,12 +166,12 @@ int launch_icp(vf_ctx* c, cudaStream_t st) {
   a.normals = c->normals;
   a.map = c->din;
   a.state_pose = &c->dstate->pose;
+  a.initial = with_initial ? &c->dstate->init_pose : nullptr;
+  a.update_state = update_state ? 1 : 0;
   a.result = &c->dstate->icp;
   a.partials = c->partials;
-  a.ctl_scratch = c->ctl_scratch;
   a.trace = c->trace;
   a.trace_cap = kTraceCap;
-  a.small_pixels = kSmallPixels;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c->icp_grid);
   cfg.blockDim = dim3(kIcpThreads);
@@ -259,7 +262,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
                                            s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
   VF_LAUNCHED(c, "k_ranges");
-  k_raycast<<<dim3(c->frag_w, c->frag_h), 256, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
+  k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
                                                          c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
                                                          s.voxel_size, s.mu, c->points, c->normals);
   VF_LAUNCHED(c, "k_raycast");
@@ -374,7 +377,7 @@ void free_all(vf_ctx* c) {
       if (g) cudaGraphExecDestroy(g);
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
-                  c->ranges, c->points, c->normals, c->partials, c->ctl_scratch, c->trace, c->flush_buf};
+                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -505,11 +508,18 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     c->levels.push_back(intr_half(c->levels.back()));
     c->pyr_floats += (size_t)c->levels.back().width * c->levels.back().height;
   }
+  std::vector<double> utab_h;
+  for (const IntrD& in : c->levels) {
+    // unproject's (px - cx) / fx and (py - cy) / fy (intrinsics.hpp:39-43), IEEE double
+    c->utab_off.push_back(utab_h.size());
+    for (int x = 0; x < in.width; ++x) utab_h.push_back((x - in.cx) / in.fx);
+    for (int y = 0; y < in.height; ++y) utab_h.push_back((y - in.cy) / in.fy);
+  }
   c->alloc_cap = c->entry_count;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_icp, kIcpThreads, 0);
   if (occ < 1) occ = 1;
-  c->icp_grid = c->num_sms * std::min(occ, 2);
+  c->icp_grid = std::min(c->num_sms * std::min(occ, 2), kMaxIcpGrid);
   int rc = VF_OK;
   const size_t nvox = (size_t)s->block_count * kBlockVolume;
   if ((rc = dalloc(c, &c->entries, sizeof(HashEntry) * (size_t)c->entry_count)) ||
@@ -530,10 +540,16 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->points, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->normals, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->partials, sizeof(double) * 2 * 32 * (size_t)c->icp_grid)) ||
-      (rc = dalloc(c, &c->ctl_scratch, 1024)) || (rc = dalloc(c, &c->trace, sizeof(double) * 32 * kTraceCap))) {
+      (rc = dalloc(c, &c->trace, sizeof(double) * kTraceRow * kTraceCap))) {
     free_all(c);
     delete c;
     return rc;
+  }
+  if (dalloc(c, &c->utab, sizeof(double) * utab_h.size()) ||
+      cudaMemcpy(c->utab, utab_h.data(), sizeof(double) * utab_h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    free_all(c);
+    delete c;
+    return VF_ERR_CUDA;
   }
   if (cudaMallocHost(reinterpret_cast<void**>(&c->hstate), sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->hpose), sizeof(PoseD)) != cudaSuccess) {
@@ -752,7 +768,7 @@ int vf_stage_raycast(vf_ctx* c, const double pose[12]) {
   k_init_ranges<<<(c->frag_w * c->frag_h + 255) / 256, 256, 0, st>>>(c->ranges, c->frag_w * c->frag_h);
   k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
                                            s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
-  k_raycast<<<dim3(c->frag_w, c->frag_h), 256, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
+  k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
                                                          c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
                                                          s.voxel_size, s.mu, c->points, c->normals);
   VF_CUDA(c, cudaGetLastError());
@@ -761,16 +777,20 @@ int vf_stage_raycast(vf_ctx* c, const double pose[12]) {
   return VF_OK;
 }
 
-int vf_stage_icp(vf_ctx* c, const float* depth_m, double out_pose[12], int* iterations, double* cost,
-                 int* valid_points, int* ok) {
+int vf_stage_icp(vf_ctx* c, const float* depth_m, const double initial_pose[12], double out_pose[12],
+                 int* iterations, double* cost, int* valid_points, int* ok) {
   if (!c || !depth_m) return VF_ERR_INVALID;
   if (!c->maps_valid) return VF_ERR_STATE;
   cudaStream_t st = c->stream;
   if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
+  if (initial_pose) {
+    *c->hpose = pose_from(initial_pose);
+    VF_CUDA(c, cudaMemcpyAsync(&c->dstate->init_pose, c->hpose, sizeof(PoseD), cudaMemcpyHostToDevice, st));
+  }
   if (c->s.hierarchy_levels > 1)
     k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, st>>>(
         c->depth, c->din.width, c->din.height, c->s.hierarchy_levels, c->pyr);
-  if (int rc = launch_icp(c, st)) return rc;
+  if (int rc = launch_icp(c, st, initial_pose != nullptr, /*update_state=*/false)) return rc;
   VF_CUDA(c, cudaGetLastError());
   if (int rc = read_state(c)) return rc;
   const IcpResult& r = c->hstate->icp;
@@ -788,7 +808,8 @@ long vf_icp_trace(vf_ctx* c, double* out, long max_rows) {
   const long n = std::min<long>(c->hstate->icp.trace_rows, kTraceCap);
   if (out && max_rows > 0) {
     const long k = std::min(n, max_rows);
-    if (cudaMemcpy(out, c->trace, sizeof(double) * 32 * k, cudaMemcpyDeviceToHost) != cudaSuccess) return VF_ERR_CUDA;
+    if (cudaMemcpy(out, c->trace, sizeof(double) * kTraceRow * k, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return VF_ERR_CUDA;
   }
   return n;
 }

@@ -335,6 +335,107 @@ __device__ __forceinline__ bool sample_map(const float4* __restrict__ map, int w
   return true;
 }
 
+// Fast controller path, fully unrolled so everything stays in registers:
+// unpivoted LDL^T of the SPD system (backward stable for SPD; differs from
+// Eigen's pivoted LDLT only by rounding), the solve, and the condition bound
+//   cond_2(H) <= |H|_F * trace(H^-1),   trace(H^-1) = |D^-1/2 L^-1|_F^2,
+// which decides the reference's SVD test exactly whenever it is below the
+// threshold.  Returns false (-> exact fallback path) if H is not numerically
+// SPD or the bound is inconclusive.
+template <int N>
+__device__ __forceinline__ bool spd_solve_fast(const double* __restrict__ tot, double max_condition, double* twist) {
+  double H[N][N];
+#pragma unroll
+  for (int s = 0, k = 0; s < 6; ++s)
+#pragma unroll
+    for (int t = s; t < 6; ++t, ++k)
+      if (s < N && t < N) {
+        H[s][t] = tot[k];
+        H[t][s] = tot[k];
+      }
+  double L[N][N], D[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double d = H[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= (L[j][k] * L[j][k]) * D[k];
+    if (!(d > 0)) return false;
+    D[j] = d;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      double sum = H[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) sum -= (L[i][k] * L[j][k]) * D[k];
+      L[i][j] = sum / d;
+    }
+  }
+  // Linv = L^-1 (unit lower triangular)
+  double Li[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      double sum = L[i][j];
+#pragma unroll
+      for (int k = j + 1; k < i; ++k) sum += L[i][k] * Li[k][j];
+      Li[i][j] = -sum;
+    }
+  }
+  double hf = 0, tr = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) hf += H[i][j] * H[i][j];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double row = 1.0;  // Li[k][k] = 1
+#pragma unroll
+    for (int i = 0; i < k; ++i) row += Li[k][i] * Li[k][i];
+    tr += row / D[k];
+  }
+  const double bound = sqrt(hf) * tr;
+  if (!(bound * (1.0 + 1e-6) < max_condition)) return false;
+  // solve H x = -g
+  double y[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = -tot[21 + i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v -= L[i][k] * y[k];
+    y[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i] /= D[i];
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    double v = y[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) v -= L[k][i] * twist[k];
+    twist[i] = v;
+  }
+  return true;
+}
+
+// Reduce 32 per-lane values across the warp with a transpose butterfly:
+// 31 shuffles instead of 5 per value.  On return lane l holds the warp sum
+// of value index l.
+__device__ __forceinline__ double warp_reduce32(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int step = 0; step < 5; ++step) {
+    const int half = 16 >> step;  // values kept per lane after this step
+    const bool upper = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      // keep v[i] (lower lanes) or v[i + half] (upper lanes); send the other
+      const double send = upper ? v[i] : v[i + half];
+      const double keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return v[0];
+}
+
 struct Ctl {
   PoseD c2w, accepted, render;
   double pending[6];
@@ -357,9 +458,11 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
   __shared__ double s_red[kIcpThreads / 32][kAccStride];
   __shared__ double s_tot[kAccStride];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const bool timer = blockIdx.x == 0 && tid == 0 && a.trace;
   if (tid == 0) {
     ctl.render = *a.state_pose;
-    ctl.c2w = pose_inverse(ctl.render);
+    // icp_track(..., initial) (depth_tracker.hpp:117): start from `initial` if given
+    ctl.c2w = pose_inverse(a.initial ? *a.initial : ctl.render);
     ctl.iterations = 0;
     ctl.any_solved = 0;
     ctl.valid_points = 0;
@@ -367,23 +470,11 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
     ctl.fail = 0;
   }
   __syncthreads();
-  bool synced = false;
   int buf = 0;
   int trace_rows = 0;
-  for (int level = a.levels - 1; level >= 0; --level) {
+  for (int level = a.levels - 1; level >= 0 && !ctl.fail; --level) {
     const IcpLevel lv = a.lv[level];
     const int npix = lv.w * lv.h;
-    const bool small = npix <= a.small_pixels;
-    if (!small && !synced) {
-      // hand CTA 0's coarse-level state to every CTA
-      if (blockIdx.x == 0 && tid == 0) *reinterpret_cast<Ctl*>(a.ctl_scratch) = ctl;
-      grid.sync();
-      if (tid == 0) ctl = *reinterpret_cast<const Ctl*>(a.ctl_scratch);
-      __syncthreads();
-      synced = true;
-    }
-    if (ctl.fail) continue;
-    if (small && blockIdx.x != 0) continue;
     const bool rotation_only = level >= a.levels - a.rotation_only_levels;
     if (tid == 0) {
       ctl.accepted_cost = __longlong_as_double(0x7ff0000000000000ll);
@@ -393,20 +484,19 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
     }
     __syncthreads();
     for (int iter = 0; iter < a.max_iterations; ++iter) {
+      long long t0 = timer ? clock64() : 0;
       const PoseD c2w = ctl.c2w;
       const PoseD render = ctl.render;
       const D3 rc = rotation_only ? mk(c2w.t[0], c2w.t[1], c2w.t[2]) : mk(0, 0, 0);
       double acc[kAcc];
 #pragma unroll
       for (int i = 0; i < kAcc; ++i) acc[i] = 0;
-      const int stride = small ? blockDim.x : gridDim.x * blockDim.x;
-      const int first = small ? tid : blockIdx.x * blockDim.x + tid;
-      for (int p = first; p < npix; p += stride) {
+      for (int p = blockIdx.x * blockDim.x + tid; p < npix; p += gridDim.x * blockDim.x) {
         const float d = __ldg(lv.depth + p);
         if (d <= 0.0f) continue;
         const int y = p / lv.w, x = p - y * lv.w;
-        // unproject (intrinsics.hpp:39-43)
-        const D3 pc = mk((x - lv.cx) / lv.fx * d, (y - lv.cy) / lv.fy * d, (double)d);
+        // unproject (intrinsics.hpp:39-43); (x - cx) / fx is tabulated per level
+        const D3 pc = mk(__ldg(lv.ux + x) * d, __ldg(lv.uy + y) * d, (double)d);
         const D3 pw = apply(c2w, pc);
         const D3 q = apply(render, pw);
         if (q.z <= 0.0) continue;
@@ -434,50 +524,67 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
         acc[27] += r * r;
         acc[28] += 1.0;
       }
-      // CTA reduction: warp shuffles, then warp 0 combines the warp sums.
+      // CTA reduction: transpose butterfly inside each warp, then one warp
+      // combines the warp sums.
+      {
+        double v32[32];
 #pragma unroll
-      for (int i = 0; i < kAcc; ++i) {
-        const double v = warp_sum(acc[i]);
-        if (lane == 0) s_red[warp][i] = v;
+        for (int i = 0; i < 32; ++i) v32[i] = i < kAcc ? acc[i] : 0.0;
+        const double mine = warp_reduce32(v32);
+        s_red[warp][lane] = mine;  // lane l holds value index l
       }
       __syncthreads();
-      if (small) {
-        if (tid < kAcc) {
-          double s = 0;
-          for (int w = 0; w < nwarps; ++w) s += s_red[w][tid];
-          s_tot[tid] = s;
-        }
-      } else {
-        double* part = a.partials + ((size_t)buf * gridDim.x + blockIdx.x) * kAccStride;
-        if (tid < kAcc) {
-          double s = 0;
-          for (int w = 0; w < nwarps; ++w) s += s_red[w][tid];
-          part[tid] = s;
-        }
-        __threadfence();
-        grid.sync();
-        // every CTA sums all partials in the same fixed order
-        for (int i = warp; i < kAcc; i += nwarps) {
-          double s = 0;
-          for (int b = lane; b < (int)gridDim.x; b += 32)
-            s += __ldcg(a.partials + ((size_t)buf * gridDim.x + b) * kAccStride + i);
-          s = warp_sum(s);
-          if (lane == 0) s_tot[i] = s;
-        }
-        buf ^= 1;
+      double* part = a.partials + ((size_t)buf * gridDim.x + blockIdx.x) * kAccStride;
+      if (tid < kAcc) {
+        double sum = 0;
+        for (int w = 0; w < nwarps; ++w) sum += s_red[w][tid];
+        part[tid] = sum;
       }
+      long long t1 = timer ? clock64() : 0;
+      grid.sync();
+      long long t2 = timer ? clock64() : 0;
+      // every CTA sums all partials in the same fixed order
+      {
+        // thread t < 32 * ... : value index i = t & 31 over CTA subset t >> 5;
+        // all loads independent, then a fixed-order combine
+        const double* base = a.partials + (size_t)buf * gridDim.x * kAccStride;
+        const int i = tid & 31, part = tid >> 5;  // 8 groups of CTAs
+        double sum = 0;
+        if (i < kAcc) {
+          double vals[kMaxIcpGrid / 8];
+#pragma unroll
+          for (int k = 0; k < kMaxIcpGrid / 8; ++k) {
+            const int b = part + 8 * k;
+            vals[k] = b < (int)gridDim.x ? __ldcg(base + (size_t)b * kAccStride + i) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < kMaxIcpGrid / 8; ++k) sum += vals[k];
+        }
+        s_red[part][i] = sum;
+        __syncthreads();
+        if (tid < kAcc) {
+          double t = 0;
+          for (int w = 0; w < nwarps; ++w) t += s_red[w][tid];
+          s_tot[tid] = t;
+        }
+      }
+      buf ^= 1;
       __syncthreads();
+      long long t3 = timer ? clock64() : 0;
       if (tid == 0) {
         const double* tot = s_tot;
         const long long count = (long long)tot[28];
+        double* row = nullptr;
         if (blockIdx.x == 0 && a.trace && trace_rows < a.trace_cap) {
-          double* row = a.trace + (size_t)trace_rows * 32;
+          row = a.trace + (size_t)trace_rows * kTraceRow;
           row[0] = level;
           row[1] = iter;
           for (int i = 0; i < 27; ++i) row[2 + i] = tot[i];
           row[29] = tot[27];
           row[30] = tot[28];
-          row[31] = 0;
+          row[31] = rotation_only ? 1 : 0;
+          for (int i = 0; i < 9; ++i) row[32 + i] = ctl.c2w.r[i];
+          for (int i = 0; i < 3; ++i) row[41 + i] = ctl.c2w.t[i];
         }
         ++trace_rows;
         ctl.decision = 0;
@@ -502,27 +609,31 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
             ctl.accepted = ctl.c2w;
             ctl.halvings = 0;
             double H[36];
-            int k = 0;
-            for (int s = 0; s < 6; ++s)
-              for (int t = s; t < 6; ++t) {
+            for (int s = 0, k = 0; s < 6; ++s)
+              for (int t = s; t < 6; ++t, ++k) {
                 H[s * 6 + t] = tot[k];
                 H[t * 6 + s] = tot[k];
-                ++k;
               }
             double twist[6] = {0, 0, 0, 0, 0, 0};
             const int n = rotation_only ? 3 : 6;
-            double hn[36], g[6];
-            for (int s = 0; s < n; ++s) {
-              for (int t = 0; t < n; ++t) hn[s * n + t] = H[s * 6 + t];
-              g[s] = -tot[21 + s];
+            bool good = rotation_only ? spd_solve_fast<3>(tot, a.max_condition, twist)
+                                      : spd_solve_fast<6>(tot, a.max_condition, twist);
+            if (!good) {
+              // exact path: the reference's pivoted LDLT and SVD condition test
+              double hn[36], g[6];
+              for (int s = 0; s < n; ++s) {
+                for (int t = 0; t < n; ++t) hn[s * n + t] = H[s * 6 + t];
+                g[s] = -tot[21 + s];
+              }
+              Ldlt f;
+              f.compute(hn, n);
+              good = well_conditioned(hn, n, f, a.max_condition);
+              if (good) f.solve(g, twist);
             }
-            Ldlt f;
-            f.compute(hn, n);
-            if (!well_conditioned(hn, n, f, a.max_condition)) {
+            if (!good) {
               ctl.fail = 1;
               ctl.decision = 2;
             } else {
-              f.solve(g, twist);
               ctl.c2w = pose_increment(ctl.c2w, twist, rotation_only);
               for (int i = 0; i < 6; ++i) ctl.pending[i] = twist[i];
               ++ctl.iterations;
@@ -538,6 +649,13 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
             }
           }
         }
+        if (row) {
+          const long long t4 = clock64();
+          row[44] = (double)(t1 - t0);  // pixel terms + CTA reduction
+          row[45] = (double)(t2 - t1);  // grid barrier
+          row[46] = (double)(t3 - t2);  // partial sums
+          row[47] = (double)(t4 - t3);  // controller
+        }
       }
       __syncthreads();
       if (ctl.decision != 0) break;
@@ -550,8 +668,8 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
     res.valid_points = ctl.valid_points;
     res.final_cost = ctl.final_cost;
     res.trace_rows = trace_rows;
-    res.pose = res.ok ? pose_inverse(ctl.c2w) : ctl.render;
-    if (res.ok) *a.state_pose = res.pose;  // pipeline_impl.hpp:83 — hold the pose on failure
+    res.pose = res.ok ? pose_inverse(ctl.c2w) : (a.initial ? *a.initial : ctl.render);
+    if (res.ok && a.update_state) *a.state_pose = res.pose;  // pipeline_impl.hpp:83 — hold the pose on failure
     *a.result = res;
   }
 }

@@ -7,6 +7,7 @@
 namespace vf {
 
 constexpr int kIcpThreads = 256;
+constexpr int kMaxIcpGrid = 512;  // partial-sum loop bound (grid <= 512 CTAs)
 constexpr int kMaxLevels = 6;
 
 struct AllocMeta {
@@ -16,9 +17,13 @@ struct AllocMeta {
 
 struct IcpLevel {
   const float* depth;
+  const double* ux;  // (x - cx) / fx per column
+  const double* uy;  // (y - cy) / fy per row
   int w, h;
   double fx, fy, cx, cy;
 };
+
+constexpr int kTraceRow = 48;  // level, iter, 21 H, 6 g, cost, count, rot_only, c2w (12), 4 timers
 
 struct IcpResult {
   PoseD pose;
@@ -35,12 +40,12 @@ struct IcpArgs {
   const float4* normals;
   IntrD map;
   PoseD* state_pose;
+  const PoseD* initial;  // optional initial world->camera pose (nullptr: the render pose)
+  int update_state;      // 1: write the tracked pose back (pipeline); 0: pure icp_track (stage call)
   IcpResult* result;
   double* partials;
-  void* ctl_scratch;
   double* trace;
   int trace_cap;
-  int small_pixels;
 };
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);

@@ -117,6 +117,10 @@ struct Sampler {
   int stride;           // 32-bit words per voxel: 1 (VoxelS) or 2 (VoxelSRgb)
   BlockCache cache;
 
+  __device__ __forceinline__ uint32_t raw(int slot, int lx, int ly, int lz) const {
+    return __ldg(vox + ((size_t)slot * kBlockVolume + (lx + ly * kBlockSide + lz * kBlockSide * kBlockSide)) * stride);
+  }
+
   // HashSdfSampler::read (raycast.hpp:73-76)
   __device__ __forceinline__ bool read(int vx, int vy, int vz, float& value) {
     const int s = cache.lookup(hv, vx >> 3, vy >> 3, vz >> 3);
@@ -124,26 +128,41 @@ struct Sampler {
       value = 1.0f;  // sdf_to_float(32767)
       return false;
     }
-    const int lin = (vx & 7) + (vy & 7) * kBlockSide + (vz & 7) * kBlockSide * kBlockSide;
-    const uint32_t raw = __ldg(vox + ((size_t)s * kBlockVolume + lin) * stride);
-    value = sdf_to_float((int16_t)(raw & 0xFFFFu));
-    return ((raw >> 16) & 0xFFu) > 0;
+    const uint32_t r = raw(s, vx & 7, vy & 7, vz & 7);
+    value = sdf_to_float((int16_t)(r & 0xFFFFu));
+    return ((r >> 16) & 0xFFu) > 0;
   }
 
-  // trilinear_sdf (raycast.hpp:102-117)
+  // trilinear_sdf (raycast.hpp:102-117).  The eight corners touch at most two
+  // blocks per axis; each distinct block is looked up once, then the corner
+  // values are combined in the reference's corner order.
   __device__ __forceinline__ bool trilinear(F3 p, float& out) {
     const float qx = p.x - 0.5f, qy = p.y - 0.5f, qz = p.z - 0.5f;
-    const int bx = __float2int_rz(floorf(qx)), by = __float2int_rz(floorf(qy)), bz = __float2int_rz(floorf(qz));
-    const float fx = qx - (float)bx, fy = qy - (float)by, fz = qz - (float)bz;
+    const int x0 = __float2int_rz(floorf(qx)), y0 = __float2int_rz(floorf(qy)), z0 = __float2int_rz(floorf(qz));
+    const float fx = qx - (float)x0, fy = qy - (float)y0, fz = qz - (float)z0;
+    const int bx0 = x0 >> 3, by0 = y0 >> 3, bz0 = z0 >> 3;
+    const int lx0 = x0 & 7, ly0 = y0 & 7, lz0 = z0 & 7;
+    uint32_t r[8];
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner) {
+      const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+      const int lx = lx0 + dx, ly = ly0 + dy, lz = lz0 + dz;
+      const int s = cache.lookup(hv, bx0 + (lx >> 3), by0 + (ly >> 3), bz0 + (lz >> 3));
+      if (s < 0) {
+        out = 1.0f;
+        return false;
+      }
+      r[corner] = raw(s, lx & 7, ly & 7, lz & 7);
+    }
     float value = 0.0f;
 #pragma unroll
     for (int corner = 0; corner < 8; ++corner) {
       const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-      float v;
-      if (!read(bx + dx, by + dy, bz + dz, v)) {
+      if (((r[corner] >> 16) & 0xFFu) == 0) {
         out = 1.0f;
         return false;
       }
+      const float v = sdf_to_float((int16_t)(r[corner] & 0xFFFFu));
       const float w = (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz);
       value += w * v;
     }
@@ -153,136 +172,127 @@ struct Sampler {
 
   // sdf_surface_normal (raycast.hpp:147-162)
   __device__ __forceinline__ bool normal(F3 p, F3& n) {
-    float g[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      F3 lo = p, hi = p;
-      if (a == 0) {
-        lo.x -= 1.0f;
-        hi.x += 1.0f;
-      } else if (a == 1) {
-        lo.y -= 1.0f;
-        hi.y += 1.0f;
-      } else {
-        lo.z -= 1.0f;
-        hi.z += 1.0f;
-      }
-      float vlo, vhi;
-      const bool ok_lo = trilinear(lo, vlo);
-      const bool ok_hi = ok_lo && trilinear(hi, vhi);
-      if (!ok_lo || !ok_hi) return false;
-      g[a] = vhi - vlo;
-    }
-    const float len = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    float vlo, vhi;
+    if (!trilinear(F3{p.x - 1.0f, p.y, p.z}, vlo) || !trilinear(F3{p.x + 1.0f, p.y, p.z}, vhi)) return false;
+    const float gx = vhi - vlo;
+    if (!trilinear(F3{p.x, p.y - 1.0f, p.z}, vlo) || !trilinear(F3{p.x, p.y + 1.0f, p.z}, vhi)) return false;
+    const float gy = vhi - vlo;
+    if (!trilinear(F3{p.x, p.y, p.z - 1.0f}, vlo) || !trilinear(F3{p.x, p.y, p.z + 1.0f}, vhi)) return false;
+    const float gz = vhi - vlo;
+    const float len = sqrtf(gx * gx + gy * gy + gz * gz);
     if (len < 1e-12f) return false;
-    n = F3{g[0] / len, g[1] / len, g[2] / len};
+    n = F3{gx / len, gy / len, gz / len};
     return true;
   }
 };
 
+// cast_ray (raycast.hpp:171-263) from the ray's start point and unit
+// direction in voxel units.  Returns the hit in metres.
+__device__ __noinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, float mu_vox, float vs, F3& hw) {
+  const float fine_step = (8.0f < mu_vox) ? 8.0f : mu_vox;
+  int state = 0;  // 0 coarse, 1 fine, 2 surface
+  float t = 0.0f, t_front = -1.0f, sdf_front = 1.0f;
+  while (t <= total) {
+    const F3 p{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
+    float value;
+    const bool found =
+        smp.read(__float2int_rz(floorf(p.x)), __float2int_rz(floorf(p.y)), __float2int_rz(floorf(p.z)), value);
+    if (state == 0) {
+      if (!found) {
+        t += 8.0f;
+        continue;
+      }
+      state = 1;
+      const float tb = t - 8.0f;
+      t = (0.0f < tb) ? tb : 0.0f;
+      continue;
+    }
+    if (!found) {
+      if (state == 2) state = 1;
+      t_front = -1.0f;
+      t += fine_step;
+      continue;
+    }
+    float sdf = value;
+    if (state == 1 && sdf <= 0.0f) return false;  // WRONG_SIDE
+    state = 2;
+    if (sdf <= 0.1f && sdf >= -0.5f) {
+      float tri;
+      if (smp.trilinear(p, tri)) sdf = tri;
+    }
+    if (sdf <= 0.0f) {
+      if (t_front >= 0.0f && sdf_front > sdf && t - t_front <= 2.0f * mu_vox) {
+        t = t + (t_front - t) * sdf / (sdf - sdf_front);
+      } else {
+        t += sdf * mu_vox;
+      }
+      float t_back = t, sdf_back = sdf;
+      for (int i = 0; i < 2; ++i) {
+        float tri;
+        if (!smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t}, tri)) break;
+        const float denom = sdf_back - tri;
+        if (fabsf(denom) > 1e-12f && fabsf(t_back - t) > 1e-6f) {
+          const float slope = denom / (t_back - t);
+          t_back = t;
+          sdf_back = tri;
+          t -= tri / (fabsf(slope) > 1e-6f ? slope : 1.0f / mu_vox);
+        } else {
+          t += tri * mu_vox;
+        }
+      }
+      const F3 h{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
+      hw = F3{h.x * vs, h.y * vs, h.z * vs};
+      return true;
+    }
+    t_front = t;
+    sdf_front = sdf;
+    const float a = sdf * mu_vox;
+    const float b = (a < 1.0f) ? 1.0f : a;
+    t += (mu_vox < b) ? mu_vox : b;
+  }
+  return false;
+}
+
 }  // namespace
 
-// K3b: render_maps (raycast.hpp:415-435) with cast_ray (:171-263) per pixel.
-__global__ void __launch_bounds__(256) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
-                                                 const float2* __restrict__ ranges, const FrameParams* __restrict__ fp,
-                                                 IntrD in, float vs, float mu, float4* __restrict__ points,
-                                                 float4* __restrict__ normals) {
-  __shared__ PoseD s_c2w;
-  if (threadIdx.x < sizeof(PoseD) / sizeof(double))
-    reinterpret_cast<double*>(&s_c2w)[threadIdx.x] = reinterpret_cast<const double*>(&fp->c2w)[threadIdx.x];
-  __syncthreads();
-  const int x = blockIdx.x * kFragmentSize + (threadIdx.x & 15);
-  const int y = blockIdx.y * kFragmentSize + (threadIdx.x >> 4);
+// K3b: render_maps (raycast.hpp:415-435).  128-thread CTAs cover half a
+// 16x16 fragment (16 x 8 pixels), so every CTA reads one range.
+__global__ void __launch_bounds__(128, 8) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
+                                                    const float2* __restrict__ ranges,
+                                                    const FrameParams* __restrict__ fp, IntrD in, float vs, float mu,
+                                                    float4* __restrict__ points, float4* __restrict__ normals) {
+  const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
+  const int x = fxi * kFragmentSize + (threadIdx.x & 15);
+  const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (threadIdx.x >> 4);
   if (x >= in.width || y >= in.height) return;
   const size_t pix = (size_t)y * in.width + x;
-  float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float2 range = ranges[blockIdx.y * gridDim.x + blockIdx.x];
-  Sampler smp{hv, vox, vstride, {}};
-  smp.cache.init();
-  bool hit = false;
-  F3 hw{0.f, 0.f, 0.f};
+  const float2 range = __ldg(ranges + fyi * gridDim.x + fxi);
+  F3 start, dir;
+  float total = 0.0f;
   if (range.x <= range.y) {  // RangeImage::valid
+    const PoseD& c2w = fp->c2w;
     const double inv_vox = 1.0 / (double)vs;
-    const D3 dir_cam = mk((x - in.cx) / in.fx, (y - in.cy) / in.fy, 1.0);
+    const double dx = (x - in.cx) / in.fx, dy = (y - in.cy) / in.fy;
     const double r0 = range.x, r1 = range.y;
-    const D3 s0 = apply(s_c2w, mk(dir_cam.x * r0, dir_cam.y * r0, dir_cam.z * r0));
-    const D3 e0 = apply(s_c2w, mk(dir_cam.x * r1, dir_cam.y * r1, dir_cam.z * r1));
-    const F3 start{(float)(s0.x * inv_vox), (float)(s0.y * inv_vox), (float)(s0.z * inv_vox)};
+    const D3 s0 = apply(c2w, mk(dx * r0, dy * r0, 1.0 * r0));
+    const D3 e0 = apply(c2w, mk(dx * r1, dy * r1, 1.0 * r1));
+    start = F3{(float)(s0.x * inv_vox), (float)(s0.y * inv_vox), (float)(s0.z * inv_vox)};
     const F3 end{(float)(e0.x * inv_vox), (float)(e0.y * inv_vox), (float)(e0.z * inv_vox)};
-    F3 dir{end.x - start.x, end.y - start.y, end.z - start.z};
-    const float total = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
-    if (total > 0) {
-      dir = F3{dir.x / total, dir.y / total, dir.z / total};
-      const float mu_vox = mu / vs;
-      const float fine_step = (8.0f < mu_vox) ? 8.0f : mu_vox;
-      int state = 0;  // 0 coarse, 1 fine, 2 surface
-      float t = 0.0f, t_front = -1.0f, sdf_front = 1.0f;
-      while (t <= total) {
-        const F3 p{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
-        float value;
-        const bool found = smp.read(__float2int_rz(floorf(p.x)), __float2int_rz(floorf(p.y)),
-                                    __float2int_rz(floorf(p.z)), value);
-        if (state == 0) {
-          if (!found) {
-            t += 8.0f;
-            continue;
-          }
-          state = 1;
-          const float tb = t - 8.0f;
-          t = (0.0f < tb) ? tb : 0.0f;
-          continue;
-        }
-        if (!found) {
-          if (state == 2) state = 1;
-          t_front = -1.0f;
-          t += fine_step;
-          continue;
-        }
-        float sdf = value;
-        if (state == 1 && sdf <= 0.0f) break;  // WRONG_SIDE
-        state = 2;
-        if (sdf <= 0.1f && sdf >= -0.5f) {
-          float tri;
-          if (smp.trilinear(p, tri)) sdf = tri;
-        }
-        if (sdf <= 0.0f) {
-          if (t_front >= 0.0f && sdf_front > sdf && t - t_front <= 2.0f * mu_vox) {
-            t = t + (t_front - t) * sdf / (sdf - sdf_front);
-          } else {
-            t += sdf * mu_vox;
-          }
-          float t_back = t, sdf_back = sdf;
-          for (int i = 0; i < 2; ++i) {
-            float tri;
-            if (!smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t}, tri)) break;
-            const float denom = sdf_back - tri;
-            if (fabsf(denom) > 1e-12f && fabsf(t_back - t) > 1e-6f) {
-              const float slope = denom / (t_back - t);
-              t_back = t;
-              sdf_back = tri;
-              t -= tri / (fabsf(slope) > 1e-6f ? slope : 1.0f / mu_vox);
-            } else {
-              t += tri * mu_vox;
-            }
-          }
-          const F3 h{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
-          hw = F3{h.x * vs, h.y * vs, h.z * vs};
-          hit = true;
-          break;
-        }
-        t_front = t;
-        sdf_front = sdf;
-        const float a = sdf * mu_vox;
-        const float b = (a < 1.0f) ? 1.0f : a;
-        t += (mu_vox < b) ? mu_vox : b;
-      }
-    }
+    dir = F3{end.x - start.x, end.y - start.y, end.z - start.z};
+    total = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
   }
-  if (hit) {
-    F3 n;
-    if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
-      out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
-      out_n = make_float4(n.x, n.y, n.z, 1.0f);
+  float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (total > 0) {
+    dir = F3{dir.x / total, dir.y / total, dir.z / total};
+    Sampler smp{hv, vox, vstride, {}};
+    smp.cache.init();
+    F3 hw;
+    if (march(smp, start, dir, total, mu / vs, vs, hw)) {
+      F3 n;
+      if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
+        out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
+        out_n = make_float4(n.x, n.y, n.z, 1.0f);
+      }
     }
   }
   points[pix] = out_p;

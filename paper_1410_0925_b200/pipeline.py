@@ -328,19 +328,22 @@ class Pipeline:
         p = _pose(pose)
         self._chk("vf_stage_raycast", self._L.vf_stage_raycast(self._h, p.ctypes.data_as(C.POINTER(C.c_double))))
 
-    def icp_track(self, depth_m):
-        """build_depth_pyramid + icp_track against the current maps and pose."""
+    def icp_track(self, depth_m, initial=None):
+        """build_depth_pyramid + icp_track(pyramid, state, settings, initial) against the current maps."""
         d = _f32(depth_m, (self.height, self.width))
         pose = np.zeros(12)
+        init = None if initial is None else _pose(initial)
         it, valid, ok = C.c_int(), C.c_int(), C.c_int()
         cost = C.c_double()
-        self._chk("vf_stage_icp", self._L.vf_stage_icp(self._h, _ptr(d), pose.ctypes.data_as(C.POINTER(C.c_double)),
-                                                       C.byref(it), C.byref(cost), C.byref(valid), C.byref(ok)))
+        self._chk("vf_stage_icp", self._L.vf_stage_icp(
+            self._h, _ptr(d), None if init is None else init.ctypes.data_as(C.POINTER(C.c_double)),
+            pose.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it), C.byref(cost), C.byref(valid), C.byref(ok)))
         return dict(pose=pose, ok=bool(ok.value), iterations=it.value, cost=cost.value, valid_points=valid.value)
 
     def icp_trace(self) -> np.ndarray:
+        """Rows of 48: level, iter, 21 H, 6 g, cost, count, rotation_only, eval cam->world pose (12), 4 timers."""
         n = self._L.vf_icp_trace(self._h, None, 0)
-        out = np.zeros((max(n, 0), 32))
+        out = np.zeros((max(n, 0), 48))
         if n > 0:
             self._L.vf_icp_trace(self._h, _ptr(out), n)
         return out
