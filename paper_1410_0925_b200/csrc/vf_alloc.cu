@@ -156,36 +156,63 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_
                                                      int* __restrict__ req_list, int* __restrict__ req_excess_rank,
                                                      int max_requests, AllocMeta* __restrict__ meta,
                                                      Counters* __restrict__ ctr, float2* __restrict__ ranges, int n_frag) {
-  __shared__ int s_scan[1024];
+  __shared__ int s_scan[64];
   __shared__ int s_total;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int f = tid; f < n_frag; f += nt) ranges[f] = make_float2(3.402823466e+38f, 0.0f);
-  const int chunk = (n_words + nt - 1) / nt;
-  const int w0 = min(tid * chunk, n_words), w1 = min(w0 + chunk, n_words);
+  // Words are read as uint4 with all of a thread's loads in flight at once
+  // (n_words is a multiple of 4 whenever bucket_count >= 128; smaller tables
+  // take the scalar path).
+  const bool vec = (n_words & 3) == 0;
+  const int units = vec ? n_words >> 2 : n_words;
+  const int chunk = (units + nt - 1) / nt;
+  const int u0 = min(tid * chunk, units), u1 = min(u0 + chunk, units);
   int cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(__ldcg(req_bits + w));
-  // block exclusive scan (Hillis-Steele over 1024 entries)
-  s_scan[tid] = cnt;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    const int v = tid >= off ? s_scan[tid - off] : 0;
-    __syncthreads();
-    s_scan[tid] += v;
-    __syncthreads();
+  if (vec) {
+    const uint4* bits4 = reinterpret_cast<const uint4*>(req_bits);
+#pragma unroll 8
+    for (int u = u0; u < u1; ++u) {
+      const uint4 b = __ldcg(bits4 + u);
+      cnt += __popc(b.x) + __popc(b.y) + __popc(b.z) + __popc(b.w);
+    }
+  } else {
+    for (int u = u0; u < u1; ++u) cnt += __popc(__ldcg(req_bits + u));
   }
-  int base = s_scan[tid] - cnt;
-  if (tid == nt - 1) s_total = s_scan[tid];
+  // block exclusive scan: warp shuffles, then one warp over the warp totals
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((tid & 31) >= o) incl += v;
+  }
+  if ((tid & 31) == 31) s_scan[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    int w = tid < (nt >> 5) ? s_scan[tid] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, w, o);
+      if (tid >= o) w += v;
+    }
+    s_scan[32 + tid] = w;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  int base = incl - cnt + ((tid >> 5) ? s_scan[32 + (tid >> 5) - 1] : 0);
+  if (tid == nt - 1) s_total = base + cnt;
   __syncthreads();
   const int n = min(s_total, max_requests);
-  for (int w = w0; w < w1; ++w) {
-    uint32_t bits = __ldcg(req_bits + w);
-    if (!bits) continue;
-    req_bits[w] = 0u;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1u;
-      if (base < max_requests) req_list[base] = w * 32 + b;
-      ++base;
+  if (cnt) {
+    const int w0 = vec ? u0 * 4 : u0, w1 = vec ? u1 * 4 : u1;
+    for (int w = w0; w < w1; ++w) {
+      uint32_t bits = __ldcg(req_bits + w);
+      if (!bits) continue;
+      req_bits[w] = 0u;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        if (base < max_requests) req_list[base] = w * 32 + b;
+        ++base;
+      }
     }
   }
   __syncthreads();
@@ -204,19 +231,30 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_
     req_excess_rank[k] = has_free ? -1 : 0;
     ex += has_free ? 0 : 1;
   }
-  s_scan[tid] = ex;
   __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    const int v = tid >= off ? s_scan[tid - off] : 0;
-    __syncthreads();
-    s_scan[tid] += v;
-    __syncthreads();
+  int eincl = ex;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, eincl, o);
+    if ((tid & 31) >= o) eincl += v;
   }
-  int ebase = s_scan[tid] - ex;
+  if ((tid & 31) == 31) s_scan[tid >> 5] = eincl;
+  __syncthreads();
+  if (tid < 32) {
+    int w = tid < (nt >> 5) ? s_scan[tid] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, w, o);
+      if (tid >= o) w += v;
+    }
+    s_scan[32 + tid] = w;
+  }
+  __syncthreads();
+  int ebase = eincl - ex + ((tid >> 5) ? s_scan[32 + (tid >> 5) - 1] : 0);
   for (int k = r0; k < r1; ++k)
     if (req_excess_rank[k] == 0) req_excess_rank[k] = ebase++;
   if (tid == nt - 1) {
-    const int n_ex = s_scan[tid];
+    const int n_ex = ebase;
     Counters c = *ctr;
     AllocMeta m;
     m.n = n;

@@ -80,50 +80,41 @@ __global__ void __launch_bounds__(256) k_ranges(const HashEntry* __restrict__ en
 
 namespace {
 
-// Register-resident 4-entry cache of block position -> VBA slot (or -1).
-struct BlockCache {
-  int bx[4], by[4], bz[4], slot[4];
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      bx[i] = 0x7fffffff;
-      by[i] = bz[i] = 0;
-      slot[i] = -1;
-    }
-  }
-  __device__ __forceinline__ int lookup(const HashView& hv, int x, int y, int z) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (bx[i] == x && by[i] == y && bz[i] == z) return slot[i];
-    const int s = find_slot(hv, x, y, z);
-#pragma unroll
-    for (int i = 3; i > 0; --i) {
-      bx[i] = bx[i - 1];
-      by[i] = by[i - 1];
-      bz[i] = bz[i - 1];
-      slot[i] = slot[i - 1];
-    }
-    bx[0] = x;
-    by[0] = y;
-    bz[0] = z;
-    slot[0] = s;
-    return s;
-  }
-};
+constexpr int kRayThreads = 128;
+constexpr int kCacheWays = 8;
 
+__device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { return find_slot(hv, x, y, z); }
+
+// Per-thread direct-mapped cache of block position -> VBA slot (misses
+// included), in shared memory laid out [way][thread] so that a warp's
+// 16-byte lookups are conflict-free.  The way is the parity of the block
+// coordinates, so the 2x2x2 blocks a trilinear stencil can straddle never
+// evict each other.
 struct Sampler {
   HashView hv;
   const uint32_t* vox;  // first 4 bytes of each voxel: sdf (lo 16), w_depth (byte 2)
   int stride;           // 32-bit words per voxel: 1 (VoxelS) or 2 (VoxelSRgb)
-  BlockCache cache;
+  int4* cache;          // this thread's column of the shared cache
 
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int w = 0; w < kCacheWays; ++w) cache[w * kRayThreads] = make_int4(0x7fffffff, 0, 0, -1);
+  }
+  __device__ __forceinline__ int lookup(int x, int y, int z) {
+    const int w = (x & 1) | ((y & 1) << 1) | ((z & 1) << 2);
+    const int4 c = cache[w * kRayThreads];
+    if (c.x == x && c.y == y && c.z == z) return c.w;
+    const int s = probe(hv, x, y, z);
+    cache[w * kRayThreads] = make_int4(x, y, z, s);
+    return s;
+  }
   __device__ __forceinline__ uint32_t raw(int slot, int lx, int ly, int lz) const {
     return __ldg(vox + ((size_t)slot * kBlockVolume + (lx + ly * kBlockSide + lz * kBlockSide * kBlockSide)) * stride);
   }
 
   // HashSdfSampler::read (raycast.hpp:73-76)
   __device__ __forceinline__ bool read(int vx, int vy, int vz, float& value) {
-    const int s = cache.lookup(hv, vx >> 3, vy >> 3, vz >> 3);
+    const int s = lookup(vx >> 3, vy >> 3, vz >> 3);
     if (s < 0) {
       value = 1.0f;  // sdf_to_float(32767)
       return false;
@@ -133,10 +124,10 @@ struct Sampler {
     return ((r >> 16) & 0xFFu) > 0;
   }
 
-  // trilinear_sdf (raycast.hpp:102-117).  The eight corners touch at most two
-  // blocks per axis; each distinct block is looked up once, then the corner
-  // values are combined in the reference's corner order.
-  __device__ __forceinline__ bool trilinear(F3 p, float& out) {
+  // trilinear_sdf (raycast.hpp:102-117): the value, or NaN when a corner is
+  // unallocated / unobserved.  Out of line: eight inlined copies blow the
+  // instruction cache (ncu: no_instruction stalls).
+  __device__ __noinline__ float trilinear(F3 p) {
     const float qx = p.x - 0.5f, qy = p.y - 0.5f, qz = p.z - 0.5f;
     const int x0 = __float2int_rz(floorf(qx)), y0 = __float2int_rz(floorf(qy)), z0 = __float2int_rz(floorf(qz));
     const float fx = qx - (float)x0, fy = qy - (float)y0, fz = qz - (float)z0;
@@ -145,40 +136,38 @@ struct Sampler {
     uint32_t r[8];
 #pragma unroll
     for (int corner = 0; corner < 8; ++corner) {
-      const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-      const int lx = lx0 + dx, ly = ly0 + dy, lz = lz0 + dz;
-      const int s = cache.lookup(hv, bx0 + (lx >> 3), by0 + (ly >> 3), bz0 + (lz >> 3));
-      if (s < 0) {
-        out = 1.0f;
-        return false;
-      }
+      const int lx = lx0 + (corner & 1), ly = ly0 + ((corner >> 1) & 1), lz = lz0 + ((corner >> 2) & 1);
+      const int s = lookup(bx0 + (lx >> 3), by0 + (ly >> 3), bz0 + (lz >> 3));
+      if (s < 0) return __int_as_float(0x7fffffff);
       r[corner] = raw(s, lx & 7, ly & 7, lz & 7);
     }
     float value = 0.0f;
 #pragma unroll
     for (int corner = 0; corner < 8; ++corner) {
       const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-      if (((r[corner] >> 16) & 0xFFu) == 0) {
-        out = 1.0f;
-        return false;
-      }
+      if (((r[corner] >> 16) & 0xFFu) == 0) return __int_as_float(0x7fffffff);
       const float v = sdf_to_float((int16_t)(r[corner] & 0xFFFFu));
       const float w = (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz);
       value += w * v;
     }
-    out = value;
-    return true;
+    return value;
   }
 
   // sdf_surface_normal (raycast.hpp:147-162)
-  __device__ __forceinline__ bool normal(F3 p, F3& n) {
-    float vlo, vhi;
-    if (!trilinear(F3{p.x - 1.0f, p.y, p.z}, vlo) || !trilinear(F3{p.x + 1.0f, p.y, p.z}, vhi)) return false;
-    const float gx = vhi - vlo;
-    if (!trilinear(F3{p.x, p.y - 1.0f, p.z}, vlo) || !trilinear(F3{p.x, p.y + 1.0f, p.z}, vhi)) return false;
-    const float gy = vhi - vlo;
-    if (!trilinear(F3{p.x, p.y, p.z - 1.0f}, vlo) || !trilinear(F3{p.x, p.y, p.z + 1.0f}, vhi)) return false;
-    const float gz = vhi - vlo;
+  __device__ __noinline__ bool normal(F3 p, F3& n) {
+    const float xl = trilinear(F3{p.x - 1.0f, p.y, p.z});
+    if (xl != xl) return false;
+    const float xh = trilinear(F3{p.x + 1.0f, p.y, p.z});
+    if (xh != xh) return false;
+    const float yl = trilinear(F3{p.x, p.y - 1.0f, p.z});
+    if (yl != yl) return false;
+    const float yh = trilinear(F3{p.x, p.y + 1.0f, p.z});
+    if (yh != yh) return false;
+    const float zl = trilinear(F3{p.x, p.y, p.z - 1.0f});
+    if (zl != zl) return false;
+    const float zh = trilinear(F3{p.x, p.y, p.z + 1.0f});
+    if (zh != zh) return false;
+    const float gx = xh - xl, gy = yh - yl, gz = zh - zl;
     const float len = sqrtf(gx * gx + gy * gy + gz * gz);
     if (len < 1e-12f) return false;
     n = F3{gx / len, gy / len, gz / len};
@@ -188,7 +177,7 @@ struct Sampler {
 
 // cast_ray (raycast.hpp:171-263) from the ray's start point and unit
 // direction in voxel units.  Returns the hit in metres.
-__device__ __noinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, float mu_vox, float vs, F3& hw) {
+__device__ __forceinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, float mu_vox, float vs, F3& hw) {
   const float fine_step = (8.0f < mu_vox) ? 8.0f : mu_vox;
   int state = 0;  // 0 coarse, 1 fine, 2 surface
   float t = 0.0f, t_front = -1.0f, sdf_front = 1.0f;
@@ -217,8 +206,8 @@ __device__ __noinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, 
     if (state == 1 && sdf <= 0.0f) return false;  // WRONG_SIDE
     state = 2;
     if (sdf <= 0.1f && sdf >= -0.5f) {
-      float tri;
-      if (smp.trilinear(p, tri)) sdf = tri;
+      const float tri = smp.trilinear(p);
+      if (tri == tri) sdf = tri;
     }
     if (sdf <= 0.0f) {
       if (t_front >= 0.0f && sdf_front > sdf && t - t_front <= 2.0f * mu_vox) {
@@ -228,8 +217,8 @@ __device__ __noinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, 
       }
       float t_back = t, sdf_back = sdf;
       for (int i = 0; i < 2; ++i) {
-        float tri;
-        if (!smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t}, tri)) break;
+        const float tri = smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t});
+        if (tri != tri) break;
         const float denom = sdf_back - tri;
         if (fabsf(denom) > 1e-12f && fabsf(t_back - t) > 1e-6f) {
           const float slope = denom / (t_back - t);
@@ -257,13 +246,14 @@ __device__ __noinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, 
 
 // K3b: render_maps (raycast.hpp:415-435).  128-thread CTAs cover half a
 // 16x16 fragment (16 x 8 pixels), so every CTA reads one range.
-__global__ void __launch_bounds__(128, 8) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
+__global__ void __launch_bounds__(kRayThreads, 8) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
                                                     const float2* __restrict__ ranges,
                                                     const FrameParams* __restrict__ fp, IntrD in, float vs, float mu,
                                                     float4* __restrict__ points, float4* __restrict__ normals) {
   const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
   const int x = fxi * kFragmentSize + (threadIdx.x & 15);
   const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (threadIdx.x >> 4);
+  __shared__ int4 s_cache[kCacheWays * kRayThreads];
   if (x >= in.width || y >= in.height) return;
   const size_t pix = (size_t)y * in.width + x;
   const float2 range = __ldg(ranges + fyi * gridDim.x + fxi);
@@ -284,8 +274,8 @@ __global__ void __launch_bounds__(128, 8) k_raycast(HashView hv, const uint32_t*
   float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
   if (total > 0) {
     dir = F3{dir.x / total, dir.y / total, dir.z / total};
-    Sampler smp{hv, vox, vstride, {}};
-    smp.cache.init();
+    Sampler smp{hv, vox, vstride, s_cache + threadIdx.x};
+    smp.init();
     F3 hw;
     if (march(smp, start, dir, total, mu / vs, vs, hw)) {
       F3 n;
