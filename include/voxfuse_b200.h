@@ -114,6 +114,9 @@ typedef struct vf_ctx vf_ctx;
 
 /* --- lifecycle (make_pipeline, pipeline.hpp:86; src/pipeline_factory.cpp:18-30) --- */
 int vf_abi_version(void);
+/* sizeof of the ABI structs, for FFI layout checks: 0 vf_settings, 1 vf_calib,
+ * 2 vf_frame_stats, 3 vf_alloc_stats, 4 vf_intrinsics; -1 otherwise. */
+long vf_struct_size(int which);
 void vf_default_settings(vf_settings* s);
 int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out);
 int vf_destroy(vf_ctx* ctx);

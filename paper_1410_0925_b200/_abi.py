@@ -29,7 +29,7 @@ STATUS_NAMES = {
 
 # Every symbol include/voxfuse_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "vf_abi_version", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
+    "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
     "vf_process_frame", "vf_process_frame_device", "vf_synchronize", "vf_read_stats",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
     "vf_entry_count", "vf_voxel_bytes", "vf_export_entries", "vf_export_voxels", "vf_export_free_stacks",
@@ -129,6 +129,7 @@ def load() -> C.CDLL:
     vp, ip, dp, fp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_float)
     sig = {
         "vf_abi_version": (C.c_int, []),
+        "vf_struct_size": (C.c_long, [C.c_int]),
         "vf_default_settings": (None, [C.POINTER(VfSettings)]),
         "vf_create": (C.c_int, [C.POINTER(VfSettings), C.POINTER(VfCalib), C.c_int, C.POINTER(C.c_void_p)]),
         "vf_destroy": (C.c_int, [vp]),

@@ -434,6 +434,17 @@ extern "C" {
 
 int vf_abi_version(void) { return VF_ABI_VERSION; }
 
+long vf_struct_size(int which) {
+  switch (which) {
+    case 0: return (long)sizeof(vf_settings);
+    case 1: return (long)sizeof(vf_calib);
+    case 2: return (long)sizeof(vf_frame_stats);
+    case 3: return (long)sizeof(vf_alloc_stats);
+    case 4: return (long)sizeof(vf_intrinsics);
+    default: return -1;
+  }
+}
+
 void vf_default_settings(vf_settings* s) {
   std::memset(s, 0, sizeof(*s));
   s->voxel_type = VF_VOXEL_S;

@@ -1,0 +1,144 @@
+"""CPU suite: the oracle against the reference's golden vectors and against
+the reference itself (oracle/_ref) where it is built; known-answer values.
+No GPU needed."""
+import ctypes as C
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import vf_py
+from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, trajectory
+
+GOLD = json.loads((Path(__file__).parent / "golden" / "golden_ref.json").read_text())
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_hash_block_pos_known_answers(olib):
+    ka = GOLD["known_answers"]["hash_block_pos_mask_0xFFFFF"]
+    for key, want in ka.items():
+        x, y, z = (int(v) for v in key.split(","))
+        assert olib.lib.vfo_hash_block_pos(x, y, z, 0xFFFFF) == want
+        # the same arithmetic restated in Python (hash_volume.hpp:32-37)
+        h = (((x & 0xFFFFFFFF) * 73856093) ^ ((y & 0xFFFFFFFF) * 19349669) ^ ((z & 0xFFFFFFFF) * 83492791))
+        assert (h & 0xFFFFFFFF) & 0xFFFFF == want
+    assert olib.lib.vfo_hash_block_pos(1, 0, 0, 0xFFFFF) != 471389  # SPEC.md:171 is wrong
+
+
+def test_sdf_quantisation_known_answers():
+    # sdf_float_to_value (voxel.hpp:16-19): clamp, then truncate toward zero
+    for f, want in GOLD["known_answers"]["sdf_float_to_value"].items():
+        v = np.clip(np.float32(float(f)), np.float32(-1), np.float32(1)) * np.float32(32767.0)
+        assert int(np.trunc(v)) == want
+
+
+def test_sdf_to_float_identity():
+    """The device evaluates (float)v / 32767.0f as one FP64 multiply rounded
+    to FP32 (vf_device.cuh); exhaustive proof that the two agree bit for bit."""
+    v = np.arange(-32768, 32768, dtype=np.int64)
+    a = v.astype(np.float32) / np.float32(32767.0)
+    b = (v.astype(np.float64) * (1.0 / 32767.0)).astype(np.float32)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def _check_run(lib, cfg, frames_gold, tracking, rgb=False):
+    poses = trajectory(len(frames_gold))
+    vol = vf_py.Volume(lib, cfg, tracking)
+    vsize = 8 if cfg.voxel_type == 2 else 4
+    for i, g in enumerate(frames_gold):
+        d = vf_py.render_depth(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        assert sha(d) == g["depth_sha"], f"frame {i}: synthetic depth differs"
+        c = None
+        if rgb:
+            c = vf_py.render_rgb(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+            assert sha(c) == g["rgb_sha"]
+        st = vol.process(d, c, None if tracking else poses[i])
+        assert int(st.tracking_ok) == g["tracking_ok"]
+        assert int(st.tracking_iterations) == g["tracking_iterations"]
+        assert int(st.blocks_allocated) == g["blocks_allocated"]
+        assert int(st.visible_blocks) == g["visible_blocks"]
+        assert vol.allocated_blocks() == g["allocated_total"]
+        assert [float(x) for x in vol.pose()] == g["pose"], f"frame {i}: pose"
+        e = vol.entries()
+        e["pad"] = 0
+        assert sha(e) == g["entries_sha"], f"frame {i}: hash entries"
+        assert sha(vol.voxels().reshape(-1, vsize)[:, : vsize - 1]) == g["voxels_sha"], f"frame {i}: voxels"
+        pts, nrm = vol.maps()
+        assert sha(pts) == g["points_sha"] and sha(nrm) == g["normals_sha"], f"frame {i}: maps"
+        assert sha(np.sort(vol.visible_list())) == g["visible_sha"]
+        if g.get("volume_digest") is not None and hasattr(lib, "prefix") and lib.prefix == "vfo_":
+            assert str(vol.digest()) == g["volume_digest"], f"frame {i}: FNV volume digest"
+        if g.get("ranges_sha") is not None:
+            assert sha(vol.ranges()) == g["ranges_sha"]
+    vol.close()
+
+
+def test_oracle_golden_tracking_T160(olib):
+    """4 tracked frames: poses bit-identical to the reference's, entries,
+    voxels, maps, visible set and the reference's volume_digest."""
+    _check_run(olib, CONFIGS["T160"], GOLD["T160_tracking"], tracking=True)
+
+
+def test_oracle_golden_known_pose_T320(olib):
+    _check_run(olib, CONFIGS["T320"].with_(tracking=False), GOLD["T320_known_pose"], tracking=False)
+
+
+def test_oracle_golden_known_pose_rgb_C2(olib):
+    _check_run(olib, CONFIGS["C2"], GOLD["C2_known_pose_rgb"], tracking=False, rgb=True)
+
+
+def test_oracle_golden_pyramid(olib):
+    cfg = CONFIGS["C1"]
+    d = vf_py.render_depth(olib, cfg, trajectory(5)[3], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+    d[100:140, 200:260] = 0.0
+    assert sha(d) == GOLD["C1_pyramid"]["depth_sha"]
+    assert [sha(l) for l in vf_py.depth_pyramid(olib, d, 5)] == GOLD["C1_pyramid"]["levels_sha"]
+
+
+def test_oracle_matches_reference_live(olib, rlib):
+    """Where oracle/_ref is built: the restatement and the reference agree bit
+    for bit on 3 tracked C1 frames (entries, voxels, maps, pose, digest)."""
+    cfg = CONFIGS["C1"]
+    poses = trajectory(3)
+    vo, vr = vf_py.Volume(olib, cfg, True), vf_py.Volume(rlib, cfg, True)
+    for i in range(3):
+        d = vf_py.render_depth(olib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        so, sr = vo.process(d), vr.process(d)
+        assert so.tracking_iterations == sr.tracking_iterations
+        assert np.array_equal(vo.pose(), vr.pose())
+        eo, er = vo.entries(), vr.entries()
+        eo["pad"] = er["pad"] = 0
+        assert np.array_equal(eo, er)
+        assert np.array_equal(vo.voxels().reshape(-1, 4)[:, :3], vr.voxels().reshape(-1, 4)[:, :3])
+        for a, b in zip(vo.maps(), vr.maps()):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert vo.digest() == vr.digest()
+
+
+def test_icp_reference_vs_oracle_stage(olib, rlib):
+    """icp_track on identical maps: oracle and the reference agree exactly."""
+    cfg = CONFIGS["T320"]
+    poses = trajectory(3)
+    o = vf_py.Volume(olib, cfg, tracking=False)
+    for i in range(2):
+        o.process(vf_py.render_depth(olib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES), None, poses[i])
+    pts, nrm = o.maps()
+    rp = o.pose()
+    d = vf_py.render_depth(olib, cfg, poses[2], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+    out_o, out_r = np.zeros(12), np.zeros(12)
+    it, cost, valid = C.c_int(), C.c_double(), C.c_int()
+    ok_o = olib.lib.vfo_stage_icp(o.h, d.ctypes.data_as(C.c_void_p), out_o.ctypes.data_as(C.c_void_p), C.byref(it),
+                                  C.byref(cost), C.byref(valid))
+    cfgc = vf_py.make_config(cfg)
+    it2, cost2, valid2 = C.c_int(), C.c_double(), C.c_int()
+    ok_r = rlib.lib.vfr_icp_track(C.byref(cfgc), d.ctypes.data_as(C.c_void_p), pts.ctypes.data_as(C.c_void_p),
+                                  nrm.ctypes.data_as(C.c_void_p), rp.ctypes.data_as(C.c_void_p),
+                                  out_r.ctypes.data_as(C.c_void_p), C.byref(it2), C.byref(cost2), C.byref(valid2))
+    assert bool(ok_o) == bool(ok_r) and it.value == it2.value and valid.value == valid2.value
+    assert np.array_equal(out_o, out_r)
+    assert cost.value == cost2.value
