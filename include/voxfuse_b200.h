@@ -201,6 +201,11 @@ int vf_kernel_launches_per_frame(vf_ctx* ctx, int tracking_frame);
 long vf_readback_bytes(const vf_ctx* ctx);
 /* Evict the L2 by writing `bytes` of scratch on the context's stream (bench hygiene). */
 int vf_flush_l2(vf_ctx* ctx, size_t bytes);
+/* Self-test of the branch-free IEEE division used by integration against the
+ * IEEE operator; returns the mismatch count.  mode 0: divisor p0, a = 0 and
+ * every numerator with p2 <= |a| <= p1; mode 1: n random pairs, |a| <= p0,
+ * p1 <= |b| <= p2. */
+long vf_selftest_division(int device, int mode, float p0, float p1, float p2, long n);
 /* Voxels whose state the last frame's integration changed (roofline accounting). */
 long vf_last_modified_voxels(vf_ctx* ctx);
 

@@ -1,0 +1,107 @@
+// TEST INFRASTRUCTURE ONLY — the drop-in check.
+//
+// Compiled with the UNMODIFIED reference sources (via oracle/eigen_shim) and
+// linked against the product library: runs the same frames through
+//   voxfuse::make_pipeline(...)              (the reference CPU engine)
+//   voxfuse_b200::make_b200_pipeline(...)    (paper_1410_0925_b200/cpp/b200_pipeline.hpp)
+// both used only through the reference's IPipeline interface, and returns
+// poses, stats, FNV volume digests and maps for tests/test_gpu_adapter.py.
+#include <cstdint>
+#include <cstring>
+#include <memory>
+
+#include "b200_pipeline.hpp"
+#include "voxfuse/core/parallel.hpp"
+#include "voxfuse/engine/pipeline.hpp"
+
+using namespace voxfuse;
+
+extern "C" {
+
+struct vfa_config {  // same layout as vfr_config (oracle/ref_driver.cpp)
+  int voxel_type;
+  float voxel_size, mu;
+  int max_weight, stop_integrating_at_max;
+  int bucket_count, bucket_size, excess_count, block_count;
+  float near_clip, far_clip;
+  int margin_px, swap_margin_px;
+  int levels, rotation_only_levels, max_iterations, min_valid_points;
+  float icp_dist_threshold, convergence_eps;
+  double max_condition;
+  double fx, fy, cx, cy;
+  int width, height;
+  double rgb_fx, rgb_fy, rgb_cx, rgb_cy;
+  int rgb_width, rgb_height;
+  double rgb_to_depth[12];
+};
+
+// Runs n frames through IPipeline.  engine: 0 = reference make_pipeline,
+// 1 = make_b200_pipeline.  Outputs per frame: pose (12), iterations, ok,
+// visible blocks, allocated; final FNV digest and maps.
+int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, const std::uint8_t* rgb,
+            double* poses, int* iters, int* ok, int* visible, std::uint64_t* digest, float* points,
+            float* normals) {
+  try {
+    EngineSettings s;
+    s.backend = VolumeBackend::hash;
+    s.voxel_type = c->voxel_type == 2 ? VoxelType::s_rgb : VoxelType::s;
+    s.scene.voxel_size = c->voxel_size;
+    s.scene.mu = c->mu;
+    s.scene.max_weight = c->max_weight;
+    s.hash.bucket_count = c->bucket_count;
+    s.hash.bucket_size = c->bucket_size;
+    s.hash.excess_count = c->excess_count;
+    s.hash.block_count = c->block_count;
+    s.near_clip = c->near_clip;
+    s.far_clip = c->far_clip;
+    s.visibility_margin_px = c->margin_px;
+    s.swap_margin_px = c->swap_margin_px;
+    s.tracker.hierarchy_levels = c->levels;
+    s.tracker.rotation_only_levels = c->rotation_only_levels;
+    s.tracker.max_iterations = c->max_iterations;
+    s.tracker.min_valid_points = c->min_valid_points;
+    s.tracker.icp_dist_threshold = c->icp_dist_threshold;
+    s.tracker.convergence_eps = c->convergence_eps;
+    s.tracker.max_condition = c->max_condition;
+    Calibration k;
+    k.depth.fx = c->fx;
+    k.depth.fy = c->fy;
+    k.depth.cx = c->cx;
+    k.depth.cy = c->cy;
+    k.depth.width = c->width;
+    k.depth.height = c->height;
+    k.rgb = k.depth;
+    std::unique_ptr<IPipeline> p =
+        engine == 1 ? voxfuse_b200::make_b200_pipeline(s, k) : make_pipeline(s, k);
+    const std::size_t npix = static_cast<std::size_t>(c->width) * c->height;
+    for (int f = 0; f < n_frames; ++f) {
+      Image2D<float> d(c->width, c->height, 0.0f);
+      std::memcpy(d.pixels().data(), depth + f * npix, sizeof(float) * npix);
+      Image2D<Vec3u8> col;
+      if (rgb) {
+        col = Image2D<Vec3u8>(c->width, c->height, Vec3u8::Zero());
+        std::memcpy(col.pixels().data(), rgb + f * npix * 3, npix * 3);
+      }
+      const FrameStats st = p->process_frame(rgb ? &col : nullptr, d);
+      const Pose& pose = p->pose();
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) poses[f * 12 + i * 3 + j] = pose.rotation()(i, j);
+      for (int i = 0; i < 3; ++i) poses[f * 12 + 9 + i] = pose.translation()(i);
+      iters[f] = st.tracking_iterations;
+      ok[f] = st.tracking_ok ? 1 : 0;
+      visible[f] = st.visible_blocks;
+    }
+    *digest = p->volume_digest();
+    const TrackingState& ts = p->tracking_state();
+    std::memcpy(points, ts.points.pixels().data(), sizeof(float) * 4 * npix);
+    std::memcpy(normals, ts.normals.pixels().data(), sizeof(float) * 4 * npix);
+    return p->frame_count();
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "vfa_run: %s\n", e.what());
+    return -1;
+  }
+}
+
+void vfa_set_threads(int n) { set_worker_count(n); }
+
+}  // extern "C"

@@ -39,6 +39,7 @@ EXPORTS = [
     "vf_device_alloc", "vf_device_free", "vf_memcpy_h2d", "vf_memcpy_d2h", "vf_host_alloc_pinned",
     "vf_host_free_pinned", "vf_event_record", "vf_event_elapsed_ms", "vf_set_profiling", "vf_stage_times",
     "vf_kernel_launches_per_frame", "vf_readback_bytes", "vf_flush_l2", "vf_last_modified_voxels",
+    "vf_selftest_division",
 ]
 
 
@@ -174,6 +175,7 @@ def load() -> C.CDLL:
         "vf_readback_bytes": (C.c_long, [vp]),
         "vf_flush_l2": (C.c_int, [vp, C.c_size_t]),
         "vf_last_modified_voxels": (C.c_long, [vp]),
+        "vf_selftest_division": (C.c_long, [C.c_int, C.c_int, C.c_float, C.c_float, C.c_float, C.c_long]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -1,0 +1,251 @@
+// voxfuse::IPipeline on the B200 — the C++ host side of the drop-in.
+//
+// A header-only adapter that a user of the reference (/root/reference/proj)
+// includes next to its own headers: it implements the reference's virtual
+// engine interface IPipeline (proj/include/voxfuse/engine/pipeline.hpp:66-84)
+// on top of the C ABI in include/voxfuse_b200.h, so replacing
+//
+//     auto p = voxfuse::make_pipeline(settings, calib);          // CPU engine
+// with
+//     auto p = voxfuse_b200::make_b200_pipeline(settings, calib); // sm_100a engine
+//
+// is the whole integration.  Everything the reference returns by value or
+// reference (FrameStats, Pose, TrackingState, digests) keeps its type and
+// meaning; construction errors are reported with the reference's exception
+// type (std::invalid_argument, pipeline_impl.hpp:55-57), runtime CUDA errors
+// as std::runtime_error.  Scope: hash backend, VoxelS /
+// VoxelSRgb, ICP tracker; the dense backend, float voxels, the colour / Ren
+// trackers and swapping raise std::invalid_argument.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "voxfuse/engine/pipeline.hpp"
+#include "voxfuse/engine/raycast.hpp"
+#include "voxfuse/engine/view.hpp"
+#include "voxfuse_b200.h"
+
+namespace voxfuse_b200 {
+
+namespace detail {
+
+inline void pose_to_array(const voxfuse::Pose& p, double* out) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) out[i * 3 + j] = p.rotation()(i, j);
+  for (int i = 0; i < 3; ++i) out[9 + i] = p.translation()(i);
+}
+
+inline voxfuse::Pose pose_from_array(const double* a) {
+  voxfuse::Mat3d r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r(i, j) = a[i * 3 + j];
+  return voxfuse::Pose(r, voxfuse::Vec3d(a[9], a[10], a[11]));
+}
+
+inline vf_intrinsics to_c(const voxfuse::Intrinsics& in) {
+  vf_intrinsics o;
+  o.fx = in.fx;
+  o.fy = in.fy;
+  o.cx = in.cx;
+  o.cy = in.cy;
+  o.width = in.width;
+  o.height = in.height;
+  return o;
+}
+
+inline void check(int rc, const char* what, const vf_ctx* ctx) {
+  if (rc < 0) {
+    throw std::runtime_error(std::string(what) + " failed (" + std::to_string(rc) + "): " +
+                             (ctx ? vf_last_error(ctx) : ""));
+  }
+}
+
+}  // namespace detail
+
+/// Translates the reference's EngineSettings (pipeline.hpp:19-41) into the
+/// C ABI's settings; throws std::invalid_argument for anything out of scope.
+inline vf_settings to_vf_settings(const voxfuse::EngineSettings& s) {
+  using voxfuse::TrackerType;
+  using voxfuse::VoxelType;
+  if (s.backend != voxfuse::VolumeBackend::hash)
+    throw std::invalid_argument("voxfuse_b200: only the voxel-block hash backend is implemented");
+  if (s.voxel_type != VoxelType::s && s.voxel_type != VoxelType::s_rgb)
+    throw std::invalid_argument("voxfuse_b200: voxel types VoxelS and VoxelSRgb only");
+  if (s.tracker.type != TrackerType::icp)
+    throw std::invalid_argument("voxfuse_b200: only the ICP depth tracker is implemented");
+  if (s.use_swapping) throw std::invalid_argument("voxfuse_b200: host swapping is not implemented yet");
+  vf_settings c;
+  vf_default_settings(&c);
+  c.voxel_type = s.voxel_type == VoxelType::s_rgb ? VF_VOXEL_S_RGB : VF_VOXEL_S;
+  c.voxel_size = s.scene.voxel_size;
+  c.mu = s.scene.mu;
+  c.max_weight = s.scene.max_weight;
+  c.stop_integrating_at_max = s.scene.stop_integrating_at_max ? 1 : 0;
+  c.bucket_count = s.hash.bucket_count;
+  c.bucket_size = s.hash.bucket_size;
+  c.excess_count = s.hash.excess_count;
+  c.block_count = s.hash.block_count;
+  c.near_clip = s.near_clip;
+  c.far_clip = s.far_clip;
+  c.visibility_margin_px = s.visibility_margin_px;
+  c.swap_margin_px = s.swap_margin_px;
+  c.hierarchy_levels = s.tracker.hierarchy_levels;
+  c.rotation_only_levels = s.tracker.rotation_only_levels;
+  c.max_iterations = s.tracker.max_iterations;
+  c.min_valid_points = s.tracker.min_valid_points;
+  c.icp_dist_threshold = s.tracker.icp_dist_threshold;
+  c.convergence_eps = s.tracker.convergence_eps;
+  c.max_condition = s.tracker.max_condition;
+  c.tracking = 1;
+  c.use_graphs = 1;
+  return c;
+}
+
+/// IPipeline backed by one device-resident volume on one GPU.
+class B200Pipeline final : public voxfuse::IPipeline {
+ public:
+  B200Pipeline(const voxfuse::EngineSettings& settings, const voxfuse::Calibration& calib, int device = 0)
+      : settings_(settings), calib_(calib) {
+    const vf_settings s = to_vf_settings(settings);
+    vf_calib c;
+    std::memset(&c, 0, sizeof(c));
+    c.depth = detail::to_c(calib.depth);
+    c.rgb = detail::to_c(calib.rgb);
+    detail::pose_to_array(calib.rgb_to_depth, c.rgb_to_depth);
+    c.disparity_a = calib.disparity.a;
+    c.disparity_b = calib.disparity.b;
+    const int rc = vf_create(&s, &c, device, &ctx_);
+    if (rc == VF_ERR_INVALID) throw std::invalid_argument("voxfuse_b200: invalid settings");
+    detail::check(rc, "vf_create", nullptr);
+  }
+  ~B200Pipeline() override {
+    if (ctx_) vf_destroy(ctx_);
+  }
+  B200Pipeline(const B200Pipeline&) = delete;
+  B200Pipeline& operator=(const B200Pipeline&) = delete;
+
+  // IPipeline::process_frame (pipeline_impl.hpp:65-123): the whole frame runs
+  // on the GPU; depth (and rgb) go up, FrameStats come back.
+  voxfuse::FrameStats process_frame(const voxfuse::Image2D<voxfuse::Vec3u8>* rgb,
+                                    const voxfuse::Image2D<float>& depth_m) override {
+    if (depth_m.width() != calib_.depth.width || depth_m.height() != calib_.depth.height)
+      throw std::invalid_argument("voxfuse_b200: depth image size does not match the calibration");
+    static_assert(sizeof(voxfuse::Vec3u8) == 3, "Vec3u8 must be packed RGB");
+    const std::uint8_t* rgb_ptr = nullptr;
+    if (rgb && !rgb->empty() && settings_.voxel_type == voxfuse::VoxelType::s_rgb)
+      rgb_ptr = reinterpret_cast<const std::uint8_t*>(rgb->pixels().data());
+    vf_frame_stats st;
+    detail::check(vf_process_frame(ctx_, depth_m.pixels().data(), rgb_ptr, &st), "vf_process_frame", ctx_);
+    last_depth_ = depth_m;
+    if (rgb) last_rgb_ = *rgb;
+    pose_ = detail::pose_from_array(st.pose);
+    maps_stale_ = true;
+    voxfuse::FrameStats fs;
+    fs.frame = st.frame;
+    fs.tracking_ok = st.tracking_ok != 0;
+    fs.tracking_iterations = st.tracking_iterations;
+    fs.tracking_cost = st.tracking_cost;
+    fs.blocks_allocated = st.blocks_allocated;
+    fs.allocation_dropped = st.allocation_dropped;
+    fs.visible_blocks = st.visible_blocks;
+    fs.pose = pose_;
+    fs.ms_total = st.ms_total;  // GPU time of the frame (CUDA events)
+    return fs;
+  }
+
+  // IPipeline::process_raw_frame (pipeline_impl.hpp:48-51): disparity -> depth
+  // with the reference's own conversion, then the GPU frame.
+  voxfuse::FrameStats process_raw_frame(const voxfuse::Image2D<voxfuse::Vec3u8>* rgb,
+                                        const voxfuse::Image2D<std::uint16_t>& disparity) override {
+    return process_frame(rgb, voxfuse::disparity_image_to_depth(disparity, calib_, settings_.max_depth));
+  }
+
+  voxfuse::Image2D<voxfuse::Vec3u8> get_image(voxfuse::DisplayMode mode) const override {
+    using voxfuse::Image2D;
+    using voxfuse::Vec3u8;
+    switch (mode) {
+      case voxfuse::DisplayMode::rgb_passthrough:
+        return last_rgb_;
+      case voxfuse::DisplayMode::depth_colourized: {
+        float dmax = 0.0f;
+        for (float d : last_depth_.pixels()) dmax = std::max(dmax, d);
+        Image2D<Vec3u8> out(last_depth_.width(), last_depth_.height(), Vec3u8::Zero());
+        if (dmax <= 0.0f) return out;
+        for (std::size_t i = 0; i < last_depth_.size(); ++i) {
+          const float d = last_depth_.pixels()[i];
+          if (d <= 0.0f) continue;
+          const float t = d / dmax;
+          out.pixels()[i] = Vec3u8(static_cast<std::uint8_t>(255 * (1.0f - t)),
+                                   static_cast<std::uint8_t>(255 * (1.0f - std::abs(2 * t - 1))),
+                                   static_cast<std::uint8_t>(255 * t));
+        }
+        return out;
+      }
+      case voxfuse::DisplayMode::raycast:
+      default: {
+        // shaded-grey rendering of the GPU maps (raycast.hpp:466-490)
+        const voxfuse::TrackingState& st = tracking_state();
+        if (!st.maps_valid) return Image2D<Vec3u8>();
+        Image2D<Vec3u8> out(st.points.width(), st.points.height(), Vec3u8::Zero());
+        const voxfuse::Vec3f axis = st.pose.rotation().row(2).cast<float>();
+        for (int y = 0; y < st.points.height(); ++y)
+          for (int x = 0; x < st.points.width(); ++x) {
+            if (st.points.at(x, y).w() == 0.0f) continue;
+            const voxfuse::Vec3f n = st.normals.at(x, y).head<3>();
+            const float shade = std::abs(n.dot(axis));
+            const auto g = static_cast<std::uint8_t>(std::clamp(shade, 0.0f, 1.0f) * 255.0f);
+            out.at(x, y) = Vec3u8(g, g, g);
+          }
+        return out;
+      }
+    }
+  }
+
+  // TrackingState: the world-space maps are downloaded on demand.
+  const voxfuse::TrackingState& tracking_state() const override {
+    if (maps_stale_) {
+      const int w = calib_.depth.width, h = calib_.depth.height;
+      state_.points = voxfuse::Image2D<voxfuse::Vec4f>(w, h, voxfuse::Vec4f::Zero());
+      state_.normals = voxfuse::Image2D<voxfuse::Vec4f>(w, h, voxfuse::Vec4f::Zero());
+      static_assert(sizeof(voxfuse::Vec4f) == 16, "Vec4f must be 4 packed floats");
+      const int rc = vf_get_maps(ctx_, reinterpret_cast<float*>(state_.points.pixels().data()),
+                                 reinterpret_cast<float*>(state_.normals.pixels().data()));
+      state_.maps_valid = rc == VF_OK;
+      state_.pose = pose_;
+      maps_stale_ = false;
+    }
+    return state_;
+  }
+  const voxfuse::Pose& pose() const override { return pose_; }
+  int frame_count() const override { return vf_frame_count(ctx_); }
+  const voxfuse::EngineSettings& settings() const override { return settings_; }
+  std::uint64_t volume_digest() const override {
+    std::uint64_t h = 0;
+    detail::check(vf_volume_digest(ctx_, &h), "vf_volume_digest", ctx_);
+    return h;
+  }
+
+  vf_ctx* handle() const { return ctx_; }
+
+ private:
+  voxfuse::EngineSettings settings_;
+  voxfuse::Calibration calib_;
+  vf_ctx* ctx_ = nullptr;
+  voxfuse::Pose pose_;
+  voxfuse::Image2D<float> last_depth_;
+  voxfuse::Image2D<voxfuse::Vec3u8> last_rgb_;
+  mutable voxfuse::TrackingState state_;
+  mutable bool maps_stale_ = true;
+};
+
+/// Drop-in for voxfuse::make_pipeline (pipeline.hpp:86).
+inline std::unique_ptr<voxfuse::IPipeline> make_b200_pipeline(const voxfuse::EngineSettings& settings,
+                                                              const voxfuse::Calibration& calib, int device = 0) {
+  return std::make_unique<B200Pipeline>(settings, calib, device);
+}
+
+}  // namespace voxfuse_b200

@@ -933,6 +933,23 @@ int vf_stage_times(vf_ctx* c, double* ms_out, long* frames) {
   if (frames) *frames = c->profiled_frames;
   return VF_OK;
 }
+long vf_selftest_division(int device, int mode, float p0, float p1, float p2, long n) {
+  if (cudaSetDevice(device) != cudaSuccess) return VF_ERR_NO_DEVICE;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return VF_ERR_CUDA;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  if (mode == 0) {  // divisor p0, amin p2 <= |a| <= amax p1
+    const uint32_t lo = __builtin_bit_cast(uint32_t, p2), hi = __builtin_bit_cast(uint32_t, p1);
+    k_divtest_const<<<4096, 256>>>(p0, lo, hi >= lo ? hi - lo + 1u : 0u, d);
+  } else {
+    k_divtest_rand<<<4096, 256>>>(p0, p1, p2, (unsigned long long)n, d);
+  }
+  unsigned long long h = 0;
+  cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? (long)h : VF_ERR_CUDA;
+}
+
 long vf_readback_bytes(const vf_ctx* c) { return c ? (long)sizeof(DevState) : -1; }
 
 int vf_flush_l2(vf_ctx* c, size_t bytes) {

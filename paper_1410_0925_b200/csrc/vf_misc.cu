@@ -122,6 +122,35 @@ __global__ void k_init_ranges(float2* ranges, int n) {
     ranges[i] = make_float2(3.402823466e+38f, 0.0f);
 }
 
+// Self-test of div_rr against the IEEE operator (tests/test_gpu_kernels.py).
+// mode 0: every float a with amin <= |a| <= amax (both signs), and a = 0, for the divisor b.
+__global__ void k_divtest_const(float b, uint32_t lo_bits, uint32_t n_bits, unsigned long long* __restrict__ mism) {
+  const float rb = rcp_refined(b);
+  unsigned long long bad = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) bad += (0.0f / b != div_rr(0.0f, b, rb));
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_bits; i += gridDim.x * blockDim.x) {
+    const float a = __uint_as_float(lo_bits + i);
+    bad += (a / b != div_rr(a, b, rb)) + (-a / b != div_rr(-a, b, rb));
+  }
+  if (bad) atomicAdd(mism, bad);
+}
+// mode 1: n pseudo-random pairs, a uniform in [-amax, amax], b log-uniform in [bmin, bmax].
+__global__ void k_divtest_rand(float amax, float bmin, float bmax, unsigned long long n,
+                               unsigned long long* __restrict__ mism) {
+  unsigned long long bad = 0;
+  const float lb0 = __logf(bmin), lb1 = __logf(bmax);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    unsigned long long x = i * 0x9E3779B97F4A7C15ull + 0x14100925ull;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+    const float ua = (float)(x & 0xFFFFFF) * (1.0f / 16777216.0f), ub = (float)((x >> 24) & 0xFFFFFF) * (1.0f / 16777216.0f);
+    const float a = (2.0f * ua - 1.0f) * amax;
+    const float b = __expf(lb0 + (lb1 - lb0) * ub) * ((x >> 63) ? -1.0f : 1.0f);
+    bad += a / b != div_rr(a, b, rcp_refined(b));
+  }
+  if (bad) atomicAdd(mism, bad);
+}
+
 __global__ void k_reset_visible(Counters* ctr) {
   if (threadIdx.x == 0 && blockIdx.x == 0) ctr->visible_count = 0;
 }

@@ -1,0 +1,69 @@
+"""Drop-in check on the GPU: the same frames through the reference's own
+IPipeline (voxfuse::make_pipeline, CPU) and through
+paper_1410_0925_b200/cpp/b200_pipeline.hpp (make_b200_pipeline, sm_100a),
+both driven only through the reference's IPipeline interface
+(oracle/adapter_check.cpp)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import vf_py
+from helpers import centre_dist, frames, rot_angle
+from paper_1410_0925_b200.scene import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+SO = vf_py.HERE / "_ref" / "libvoxfuse_adapter_check.so"
+
+
+def _run(lib, cfg, engine, fr):
+    n = len(fr)
+    depth = np.ascontiguousarray(np.stack([f[1] for f in fr]), np.float32)
+    c = vf_py.make_config(cfg)
+    poses = np.zeros((n, 12))
+    iters, ok, vis = (np.zeros(n, np.int32) for _ in range(3))
+    dig = C.c_uint64()
+    w, h = cfg.width, cfg.height
+    pts, nrm = np.zeros((h, w, 4), np.float32), np.zeros((h, w, 4), np.float32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = lib.vfa_run(C.byref(c), engine, n, p(depth), None, p(poses), p(iters), p(ok), p(vis), C.byref(dig), p(pts),
+                     p(nrm))
+    assert rc == n
+    return poses, iters, ok, vis, dig.value, pts, nrm
+
+
+@pytest.fixture(scope="module")
+def alib():
+    if not SO.exists():
+        pytest.skip("adapter check not built (make -C oracle adapter needs /root/reference)")
+    lib = C.CDLL(str(SO))
+    lib.vfa_run.restype = C.c_int
+    lib.vfa_run.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 9
+    lib.vfa_set_threads.argtypes = [C.c_int]
+    lib.vfa_set_threads(1)
+    return lib
+
+
+def test_ipipeline_frame0_identical(olib, alib):
+    """One frame through IPipeline: the reference's own volume_digest (FNV over
+    every allocated block) and the maps are identical."""
+    cfg = CONFIGS["C1"]
+    fr = frames(olib, cfg, 1)
+    ref = _run(alib, cfg, 0, fr)
+    gpu = _run(alib, cfg, 1, fr)
+    assert ref[4] == gpu[4], "volume_digest differs"
+    assert np.array_equal(ref[5].view(np.uint32), gpu[5].view(np.uint32))
+    assert np.array_equal(ref[6].view(np.uint32), gpu[6].view(np.uint32))
+
+
+def test_ipipeline_tracked_sequence(olib, alib):
+    cfg = CONFIGS["C1"]
+    fr = frames(olib, cfg, 5)
+    ref = _run(alib, cfg, 0, fr)
+    gpu = _run(alib, cfg, 1, fr)
+    assert np.array_equal(ref[2], gpu[2])  # tracking_ok
+    for i in range(5):
+        assert rot_angle(ref[0][i], gpu[0][i]) <= 1e-4 and centre_dist(ref[0][i], gpu[0][i]) <= 1e-4
+    hit_r, hit_g = ref[5][..., 3] > 0, gpu[5][..., 3] > 0
+    assert (hit_r == hit_g).mean() >= 0.999
