@@ -9,7 +9,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvoxfuse_b200.so"
+LIB_PATH = Path(os.environ.get("VOXFUSE_B200_LIB", Path(__file__).resolve().parent / "lib" / "libvoxfuse_b200.so"))
 
 VF_OK = 0
 VF_ERR_INVALID = -1

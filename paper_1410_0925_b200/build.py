@@ -48,9 +48,13 @@ def _stale(out: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, out_dir: Path | None = None, defines=()) -> Path:
+    """Compile to out_dir (default: the in-tree lib/); `defines` are extra -D
+    flags for tuning experiments (variants go to a separate directory)."""
     nvcc = nvcc_path()
-    obj_dir = OUT_DIR / "obj"
+    out = Path(out_dir) if out_dir else OUT_DIR
+    lib = out / "libvoxfuse_b200.so"
+    obj_dir = out / "obj"
     obj_dir.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [INCLUDE / "voxfuse_b200.h"]
     jobs = []
@@ -58,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         s = CSRC / src
         o = obj_dir / (src + ".o")
         if force or _stale(o, [s, *headers]):
-            cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v", "-c", str(s), "-o", str(o)]
+            cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-Xptxas", "-v", "-c", str(s), "-o", str(o)]
             jobs.append((src, cmd))
     log_lines = []
 
@@ -74,10 +78,10 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 if r.returncode != 0:
                     sys.stderr.write(r.stderr)
                     raise RuntimeError(f"nvcc failed on {src}")
-        (OUT_DIR / "ptxas.log").write_text("\n".join(log_lines))
+        (out / "ptxas.log").write_text("\n".join(log_lines))
     objs = [str(obj_dir / (s + ".o")) for s in SOURCES]
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB), *objs,
+    if force or jobs or _stale(lib, objs):
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib), *objs,
                "-Xcompiler", "-fPIC", "-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -85,7 +89,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             raise RuntimeError("link failed")
     if verbose and log_lines:
         print("\n".join(log_lines))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -436,6 +436,27 @@ __device__ __forceinline__ double warp_reduce32(double (&v)[32]) {
   return v[0];
 }
 
+// The validity / spread test and blend of sample_map_bilinear
+// (depth_tracker.hpp:40-54) on four already-loaded taps a, b, c, d.
+__device__ __forceinline__ bool bilinear_taps(const float4 (&t)[4], double fx, double fy, float max_spread, D3& out) {
+  const float4 a = t[0], b = t[1], c = t[2], d = t[3];
+  if (a.w == 0.0f || b.w == 0.0f || c.w == 0.0f || d.w == 0.0f) return false;
+#define MINF(p, q) ((q) < (p) ? (q) : (p))
+#define MAXF(p, q) ((p) < (q) ? (q) : (p))
+  const float sx = MAXF(MAXF(MAXF(a.x, b.x), c.x), d.x) - MINF(MINF(MINF(a.x, b.x), c.x), d.x);
+  const float sy = MAXF(MAXF(MAXF(a.y, b.y), c.y), d.y) - MINF(MINF(MINF(a.y, b.y), c.y), d.y);
+  const float sz = MAXF(MAXF(MAXF(a.z, b.z), c.z), d.z) - MINF(MINF(MINF(a.z, b.z), c.z), d.z);
+#undef MINF
+#undef MAXF
+  if (sqrtf(sx * sx + sy * sy + sz * sz) > max_spread) return false;
+  const float w0 = (float)((1 - fx) * (1 - fy)), w1 = (float)(fx * (1 - fy));
+  const float w2 = (float)((1 - fx) * fy), w3 = (float)(fx * fy);
+  out.x = (double)(a.x * w0 + b.x * w1 + c.x * w2 + d.x * w3);
+  out.y = (double)(a.y * w0 + b.y * w1 + c.y * w2 + d.y * w3);
+  out.z = (double)(a.z * w0 + b.z * w1 + c.z * w2 + d.z * w3);
+  return true;
+}
+
 struct Ctl {
   PoseD c2w, accepted, render;
   double pending[6];
@@ -452,7 +473,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
+__global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Ctl ctl;
   __shared__ double s_red[kIcpThreads / 32][kAccStride];
@@ -491,38 +512,83 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp(IcpArgs a) {
       double acc[kAcc];
 #pragma unroll
       for (int i = 0; i < kAcc; ++i) acc[i] = 0;
-      for (int p = blockIdx.x * blockDim.x + tid; p < npix; p += gridDim.x * blockDim.x) {
-        const float d = __ldg(lv.depth + p);
-        if (d <= 0.0f) continue;
-        const int y = p / lv.w, x = p - y * lv.w;
-        // unproject (intrinsics.hpp:39-43); (x - cx) / fx is tabulated per level
-        const D3 pc = mk(__ldg(lv.ux + x) * d, __ldg(lv.uy + y) * d, (double)d);
-        const D3 pw = apply(c2w, pc);
-        const D3 q = apply(render, pw);
-        if (q.z <= 0.0) continue;
-        const double u = a.map.fx * q.x / q.z + a.map.cx;
-        const double v = a.map.fy * q.y / q.z + a.map.cy;
-        D3 mp, mn;
-        if (!sample_map(a.points, a.map.width, a.map.height, u, v, a.dist_thr, mp)) continue;
-        if (!sample_map(a.normals, a.map.width, a.map.height, u, v, 1.0f, mn)) continue;
-        const double nlen = sqrt(mn.x * mn.x + mn.y * mn.y + mn.z * mn.z);
-        if (nlen < 1e-6) continue;
-        mn = mk(mn.x / nlen, mn.y / nlen, mn.z / nlen);
-        // icp_point_to_plane_term (depth_tracker.hpp:20-27)
-        const double r = (pw.x - mp.x) * mn.x + (pw.y - mp.y) * mn.y + (pw.z - mp.z) * mn.z;
-        if (fabs(r) > (double)a.dist_thr) continue;
-        const D3 pr = rotation_only ? mk(pw.x - rc.x, pw.y - rc.y, pw.z - rc.z) : pw;
-        const double j[6] = {pr.y * mn.z - pr.z * mn.y, pr.z * mn.x - pr.x * mn.z, pr.x * mn.y - pr.y * mn.x,
-                             mn.x, mn.y, mn.z};
-        int k = 0;
+      // Two pixels per step, each pipeline stage issued for both before it is
+      // consumed, so their memory round trips (depth + tables, then the
+      // eight map taps) overlap.
+      const int gstride = gridDim.x * blockDim.x;
+      for (int p0 = blockIdx.x * blockDim.x + tid; p0 < npix; p0 += 2 * gstride) {
+        int pix[2] = {p0, p0 + gstride};
+        float d[2];
+        double ux[2], uy[2];
 #pragma unroll
-        for (int s = 0; s < 6; ++s) {
-#pragma unroll
-          for (int t = s; t < 6; ++t) acc[k++] += j[s] * j[t];
-          acc[21 + s] += j[s] * r;
+        for (int k = 0; k < 2; ++k) {
+          const bool in = pix[k] < npix;
+          const int y = in ? pix[k] / lv.w : 0, x = in ? pix[k] - y * lv.w : 0;
+          d[k] = in ? __ldg(lv.depth + pix[k]) : 0.0f;
+          ux[k] = __ldg(lv.ux + x);
+          uy[k] = __ldg(lv.uy + y);
         }
-        acc[27] += r * r;
-        acc[28] += 1.0;
+        D3 pw[2];
+        bool ok[2];
+        int ix[2], iy[2];
+        double fx[2], fy[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          // unproject (intrinsics.hpp:39-43); (x - cx) / fx is tabulated per level
+          const D3 pc = mk(ux[k] * d[k], uy[k] * d[k], (double)d[k]);
+          pw[k] = apply(c2w, pc);
+          const D3 q = apply(render, pw[k]);
+          const double u = a.map.fx * q.x / q.z + a.map.cx;
+          const double v = a.map.fy * q.y / q.z + a.map.cy;
+          // sample_map_bilinear's bounds test (depth_tracker.hpp:39)
+          ok[k] = d[k] > 0.0f && q.z > 0.0 &&
+                  !(u < 0 || v < 0 || u > a.map.width - 1.001 || v > a.map.height - 1.001);
+          ix[k] = ok[k] ? (int)u : 0;
+          iy[k] = ok[k] ? (int)v : 0;
+          fx[k] = u - ix[k];
+          fy[k] = v - iy[k];
+        }
+        float4 tp[2][4], tn[2][4];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const size_t i00 = (size_t)iy[k] * a.map.width + ix[k];
+          if (ok[k]) {
+            tp[k][0] = __ldg(a.points + i00);
+            tp[k][1] = __ldg(a.points + i00 + 1);
+            tp[k][2] = __ldg(a.points + i00 + a.map.width);
+            tp[k][3] = __ldg(a.points + i00 + a.map.width + 1);
+            tn[k][0] = __ldg(a.normals + i00);
+            tn[k][1] = __ldg(a.normals + i00 + 1);
+            tn[k][2] = __ldg(a.normals + i00 + a.map.width);
+            tn[k][3] = __ldg(a.normals + i00 + a.map.width + 1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (!ok[k]) continue;
+          D3 mp, mn;
+          if (!bilinear_taps(tp[k], fx[k], fy[k], a.dist_thr, mp)) continue;
+          if (!bilinear_taps(tn[k], fx[k], fy[k], 1.0f, mn)) continue;
+          const double nlen = sqrt(mn.x * mn.x + mn.y * mn.y + mn.z * mn.z);
+          if (nlen < 1e-6) continue;
+          mn = mk(mn.x / nlen, mn.y / nlen, mn.z / nlen);
+          // icp_point_to_plane_term (depth_tracker.hpp:20-27)
+          const D3 w = pw[k];
+          const double r = (w.x - mp.x) * mn.x + (w.y - mp.y) * mn.y + (w.z - mp.z) * mn.z;
+          if (fabs(r) > (double)a.dist_thr) continue;
+          const D3 pr = rotation_only ? mk(w.x - rc.x, w.y - rc.y, w.z - rc.z) : w;
+          const double j[6] = {pr.y * mn.z - pr.z * mn.y, pr.z * mn.x - pr.x * mn.z, pr.x * mn.y - pr.y * mn.x,
+                               mn.x, mn.y, mn.z};
+          int n = 0;
+#pragma unroll
+          for (int s = 0; s < 6; ++s) {
+#pragma unroll
+            for (int t = s; t < 6; ++t) acc[n++] += j[s] * j[t];
+            acc[21 + s] += j[s] * r;
+          }
+          acc[27] += r * r;
+          acc[28] += 1.0;
+        }
       }
       // CTA reduction: transpose butterfly inside each warp, then one warp
       // combines the warp sums.

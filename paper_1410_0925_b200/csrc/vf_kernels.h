@@ -6,7 +6,13 @@
 
 namespace vf {
 
-constexpr int kIcpThreads = 256;
+#ifndef VF_ICP_THREADS
+#define VF_ICP_THREADS 256
+#endif
+#ifndef VF_ICP_MIN_BLOCKS
+#define VF_ICP_MIN_BLOCKS 1
+#endif
+constexpr int kIcpThreads = VF_ICP_THREADS;
 constexpr int kMaxIcpGrid = 512;  // partial-sum loop bound (grid <= 512 CTAs)
 constexpr int kMaxLevels = 6;
 
