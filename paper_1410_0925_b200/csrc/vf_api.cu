@@ -101,6 +101,8 @@ struct vf_ctx {
   double* utab = nullptr;  // per level: (x - cx) / fx then (y - cy) / fy
   std::vector<size_t> utab_off;
   double* trace = nullptr;
+  int icp_slots = 0;
+  size_t icp_smem = 0;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   int icp_grid = 0;
@@ -172,10 +174,11 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
   a.partials = c->partials;
   a.trace = c->trace;
   a.trace_cap = kTraceCap;
+  a.max_slots = c->icp_slots;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c->icp_grid);
   cfg.blockDim = dim3(kIcpThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = c->icp_smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -531,6 +534,17 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_icp, kIcpThreads, 0);
   if (occ < 1) occ = 1;
   c->icp_grid = std::min(c->num_sms * std::min(occ, 2), kMaxIcpGrid);
+  {
+    // stage up to the whole level-0 share of each thread in shared memory,
+    // within a 160 KiB budget per CTA
+    const long threads = (long)c->icp_grid * kIcpThreads;
+    const long need = (c->npix + threads - 1) / threads;
+    const size_t tables = sizeof(double) * (size_t)(c->din.width + c->din.height);
+    const long cap = (long)((160 * 1024 - tables) / (8 * kIcpThreads));
+    c->icp_slots = (int)std::max(1L, std::min(need, cap));
+    c->icp_smem = tables + (size_t)c->icp_slots * kIcpThreads * 8;
+    cudaFuncSetAttribute(k_icp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
+  }
   int rc = VF_OK;
   const size_t nvox = (size_t)s->block_count * kBlockVolume;
   if ((rc = dalloc(c, &c->entries, sizeof(HashEntry) * (size_t)c->entry_count)) ||

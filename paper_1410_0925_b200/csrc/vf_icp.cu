@@ -478,6 +478,13 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
   __shared__ Ctl ctl;
   __shared__ double s_red[kIcpThreads / 32][kAccStride];
   __shared__ double s_tot[kAccStride];
+  // dynamic: unprojection tables (max level-0 width + height doubles), then
+  // max_slots x blockDim pixel slots (float depth, packed x | y << 16)
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  double* s_ux = reinterpret_cast<double*>(s_dyn);
+  double* s_uy = s_ux + a.lv[0].w;
+  float* s_depth = reinterpret_cast<float*>(s_uy + a.lv[0].h);
+  int* s_xy = reinterpret_cast<int*>(s_depth + a.max_slots * blockDim.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const bool timer = blockIdx.x == 0 && tid == 0 && a.trace;
   if (tid == 0) {
@@ -503,6 +510,25 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
       for (int i = 0; i < 6; ++i) ctl.pending[i] = 0;
       ctl.halvings = 0;
     }
+    // Depth and unprojection are iteration-invariant: stage this CTA's pixel
+    // slots (depth + packed x, y) and the level's (x - cx) / fx, (y - cy) / fy
+    // tables in shared memory once per level.
+    const int gstride = gridDim.x * blockDim.x;
+    const int nslots = min((npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride, a.max_slots);
+    for (int i = tid; i < lv.w; i += blockDim.x) s_ux[i] = __ldg(lv.ux + i);
+    for (int i = tid; i < lv.h; i += blockDim.x) s_uy[i] = __ldg(lv.uy + i);
+    for (int k = 0; k < nslots; ++k) {
+      const int pix = blockIdx.x * blockDim.x + tid + k * gstride;
+      float d = 0.0f;
+      int xy = 0;
+      if (pix < npix) {
+        const int y = pix / lv.w, x = pix - y * lv.w;
+        d = __ldg(lv.depth + pix);
+        xy = x | (y << 16);
+      }
+      s_depth[k * blockDim.x + tid] = d;
+      s_xy[k * blockDim.x + tid] = xy;
+    }
     __syncthreads();
     for (int iter = 0; iter < a.max_iterations; ++iter) {
       long long t0 = timer ? clock64() : 0;
@@ -515,18 +541,26 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
       // Two pixels per step, each pipeline stage issued for both before it is
       // consumed, so their memory round trips (depth + tables, then the
       // eight map taps) overlap.
-      const int gstride = gridDim.x * blockDim.x;
-      for (int p0 = blockIdx.x * blockDim.x + tid; p0 < npix; p0 += 2 * gstride) {
-        int pix[2] = {p0, p0 + gstride};
+      const int total_slots = (npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride;
+      for (int k0 = 0; k0 < total_slots; k0 += 2) {
         float d[2];
         double ux[2], uy[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const bool in = pix[k] < npix;
-          const int y = in ? pix[k] / lv.w : 0, x = in ? pix[k] - y * lv.w : 0;
-          d[k] = in ? __ldg(lv.depth + pix[k]) : 0.0f;
-          ux[k] = __ldg(lv.ux + x);
-          uy[k] = __ldg(lv.uy + y);
+          const int slot = k0 + k;
+          const int pix = blockIdx.x * blockDim.x + tid + slot * gstride;
+          if (slot < nslots) {  // staged in shared memory
+            d[k] = s_depth[slot * blockDim.x + tid];
+            const int xy = s_xy[slot * blockDim.x + tid];
+            ux[k] = s_ux[xy & 0xFFFF];
+            uy[k] = s_uy[xy >> 16];
+          } else {  // beyond the staging capacity (very large images)
+            const bool in = slot < total_slots && pix < npix;
+            const int y = in ? pix / lv.w : 0, x = in ? pix - y * lv.w : 0;
+            d[k] = in ? __ldg(lv.depth + pix) : 0.0f;
+            ux[k] = s_ux[x];
+            uy[k] = s_uy[y];
+          }
         }
         D3 pw[2];
         bool ok[2];
@@ -577,16 +611,20 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
           const double r = (w.x - mp.x) * mn.x + (w.y - mp.y) * mn.y + (w.z - mp.z) * mn.z;
           if (fabs(r) > (double)a.dist_thr) continue;
           const D3 pr = rotation_only ? mk(w.x - rc.x, w.y - rc.y, w.z - rc.z) : w;
-          const double j[6] = {pr.y * mn.z - pr.z * mn.y, pr.z * mn.x - pr.x * mn.z, pr.x * mn.y - pr.y * mn.x,
-                               mn.x, mn.y, mn.z};
+          // Jacobian and sums feed only the 29 accumulators, whose reduction
+          // order differs from the reference's anyway (parity bar 1e-9), so
+          // they use fused multiply-adds; everything that decides association
+          // or rejection above keeps the reference's exact rounding.
+          const double j[6] = {fma(pr.y, mn.z, -(pr.z * mn.y)), fma(pr.z, mn.x, -(pr.x * mn.z)),
+                               fma(pr.x, mn.y, -(pr.y * mn.x)), mn.x, mn.y, mn.z};
           int n = 0;
 #pragma unroll
           for (int s = 0; s < 6; ++s) {
 #pragma unroll
-            for (int t = s; t < 6; ++t) acc[n++] += j[s] * j[t];
-            acc[21 + s] += j[s] * r;
+            for (int t = s; t < 6; ++t, ++n) acc[n] = fma(j[s], j[t], acc[n]);
+            acc[21 + s] = fma(j[s], r, acc[21 + s]);
           }
-          acc[27] += r * r;
+          acc[27] = fma(r, r, acc[27]);
           acc[28] += 1.0;
         }
       }

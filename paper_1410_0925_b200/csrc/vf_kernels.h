@@ -52,6 +52,7 @@ struct IcpArgs {
   double* partials;
   double* trace;
   int trace_cap;
+  int max_slots;  // pixel slots per thread staged in shared memory
 };
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);

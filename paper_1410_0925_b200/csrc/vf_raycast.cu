@@ -80,6 +80,9 @@ __global__ void __launch_bounds__(256) k_ranges(const HashEntry* __restrict__ en
 
 namespace {
 
+#ifndef VF_RAY_MIN_BLOCKS
+#define VF_RAY_MIN_BLOCKS 8
+#endif
 constexpr int kRayThreads = 128;
 constexpr int kCacheWays = 8;
 
@@ -125,9 +128,10 @@ struct Sampler {
   }
 
   // trilinear_sdf (raycast.hpp:102-117): the value, or NaN when a corner is
-  // unallocated / unobserved.  Out of line: eight inlined copies blow the
-  // instruction cache (ncu: no_instruction stalls).
-  __device__ __noinline__ float trilinear(F3 p) {
+  // unallocated / unobserved.  Inlined at exactly three sites (band test,
+  // refinement loop, normal loop); more copies blow the instruction cache
+  // (ncu: no_instruction stalls), out-of-line calls pay the ABI spills.
+  __device__ __forceinline__ float trilinear(F3 p) {
     const float qx = p.x - 0.5f, qy = p.y - 0.5f, qz = p.z - 0.5f;
     const int x0 = __float2int_rz(floorf(qx)), y0 = __float2int_rz(floorf(qy)), z0 = __float2int_rz(floorf(qz));
     const float fx = qx - (float)x0, fy = qy - (float)y0, fz = qz - (float)z0;
@@ -153,21 +157,19 @@ struct Sampler {
     return value;
   }
 
-  // sdf_surface_normal (raycast.hpp:147-162)
+  // sdf_surface_normal (raycast.hpp:147-162): six trilinear values at
+  // p -/+ 1 voxel per axis, evaluated by one loop body.
   __device__ __noinline__ bool normal(F3 p, F3& n) {
-    const float xl = trilinear(F3{p.x - 1.0f, p.y, p.z});
-    if (xl != xl) return false;
-    const float xh = trilinear(F3{p.x + 1.0f, p.y, p.z});
-    if (xh != xh) return false;
-    const float yl = trilinear(F3{p.x, p.y - 1.0f, p.z});
-    if (yl != yl) return false;
-    const float yh = trilinear(F3{p.x, p.y + 1.0f, p.z});
-    if (yh != yh) return false;
-    const float zl = trilinear(F3{p.x, p.y, p.z - 1.0f});
-    if (zl != zl) return false;
-    const float zh = trilinear(F3{p.x, p.y, p.z + 1.0f});
-    if (zh != zh) return false;
-    const float gx = xh - xl, gy = yh - yl, gz = zh - zl;
+    float v[6];
+#pragma unroll 1
+    for (int k = 0; k < 6; ++k) {
+      const float sgn = (k & 1) ? 1.0f : -1.0f;
+      const int a = k >> 1;
+      const F3 q{a == 0 ? p.x + sgn : p.x, a == 1 ? p.y + sgn : p.y, a == 2 ? p.z + sgn : p.z};
+      v[k] = trilinear(q);
+      if (v[k] != v[k]) return false;
+    }
+    const float gx = v[1] - v[0], gy = v[3] - v[2], gz = v[5] - v[4];
     const float len = sqrtf(gx * gx + gy * gy + gz * gz);
     if (len < 1e-12f) return false;
     n = F3{gx / len, gy / len, gz / len};
@@ -216,6 +218,7 @@ __device__ __forceinline__ bool march(Sampler& smp, F3 start, F3 dir, float tota
         t += sdf * mu_vox;
       }
       float t_back = t, sdf_back = sdf;
+#pragma unroll 1
       for (int i = 0; i < 2; ++i) {
         const float tri = smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t});
         if (tri != tri) break;
@@ -246,7 +249,7 @@ __device__ __forceinline__ bool march(Sampler& smp, F3 start, F3 dir, float tota
 
 // K3b: render_maps (raycast.hpp:415-435).  128-thread CTAs cover half a
 // 16x16 fragment (16 x 8 pixels), so every CTA reads one range.
-__global__ void __launch_bounds__(kRayThreads, 8) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
+__global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
                                                     const float2* __restrict__ ranges,
                                                     const FrameParams* __restrict__ fp, IntrD in, float vs, float mu,
                                                     float4* __restrict__ points, float4* __restrict__ normals) {
