@@ -22,6 +22,7 @@ namespace vf {
 namespace {
 
 constexpr int kStepBits = 12;
+constexpr int kSortCap = 4096;  // requests sorted in shared memory (steady state)
 constexpr unsigned long long kStepMask = (1ull << kStepBits) - 1ull;
 
 // detail::dda_cells (allocation.hpp:60-96) in FP64.  Visit(cell, step) returns
@@ -95,14 +96,25 @@ __global__ void k_prep(const PoseD* __restrict__ pose, IntrD depth_in, IntrD rgb
   fp->rgb_cam = make_camf(pose_compose(depth_to_rgb, w2c), rgb_in);
 }
 
-// K1a: mark_blocks (allocation.hpp:137-168).  One thread per pixel.
-__global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, IntrD in, const FrameParams* __restrict__ fp,
+// K1a: mark_blocks (allocation.hpp:137-168).  One thread per pixel.  Every
+// CTA derives cam_to_world from the device pose itself; CTA 0 also publishes
+// the frame's camera parameters (k_prep's job) for the later kernels.
+__global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, IntrD in, const PoseD* __restrict__ pose,
+                                              IntrD rgb_in, PoseD depth_to_rgb, FrameParams* __restrict__ fp,
                                               HashView hv, float voxel_size, float mu,
                                               unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
-                                              Counters* __restrict__ ctr) {
+                                              int* __restrict__ req_marked, Counters* __restrict__ ctr) {
   __shared__ PoseD s_c2w;
-  if (threadIdx.x < sizeof(PoseD) / sizeof(double))
-    reinterpret_cast<double*>(&s_c2w)[threadIdx.x] = reinterpret_cast<const double*>(&fp->c2w)[threadIdx.x];
+  if (threadIdx.x == 0) {
+    const PoseD w2c = *pose;
+    s_c2w = pose_inverse(w2c);
+    if (blockIdx.x == 0) {
+      fp->w2c = w2c;
+      fp->c2w = s_c2w;
+      fp->depth_cam = make_camf(w2c, in);
+      fp->rgb_cam = make_camf(pose_compose(depth_to_rgb, w2c), rgb_in);
+    }
+  }
   __syncthreads();
   const int npix = in.width * in.height;
   const int pixel = blockIdx.x * blockDim.x + threadIdx.x;
@@ -121,7 +133,11 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
       }
       const uint32_t bucket = hash_block(cx, cy, cz, hv.mask);
       const unsigned long long old = atomicMax(req_key + bucket, key_base | (unsigned long long)step);
-      if (old == 0ull) atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
+      if (old == 0ull) {
+        atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
+        const int pos = atomicAdd(&ctr->n_marked, 1);
+        if (pos < kSortCap) req_marked[pos] = (int)bucket;
+      }
     }
     return true;
   });
@@ -153,13 +169,46 @@ __device__ __forceinline__ void decode_request(unsigned long long key, const flo
 // prefix sums that fix every request's free-stack pop, and the fast/slow
 // decision.  Also resets the per-frame counters consumed later in the frame.
 __global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_bits, int n_words, HashView hv,
-                                                     int* __restrict__ req_list, int* __restrict__ req_excess_rank,
-                                                     int max_requests, AllocMeta* __restrict__ meta,
-                                                     Counters* __restrict__ ctr, float2* __restrict__ ranges, int n_frag) {
+                                                     const int* __restrict__ req_marked, int* __restrict__ req_list,
+                                                     int* __restrict__ req_excess_rank, int max_requests,
+                                                     AllocMeta* __restrict__ meta, Counters* __restrict__ ctr,
+                                                     float2* __restrict__ ranges, int n_frag) {
   __shared__ int s_scan[64];
   __shared__ int s_total;
+  __shared__ int s_sort[kSortCap];
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int f = tid; f < n_frag; f += nt) ranges[f] = make_float2(3.402823466e+38f, 0.0f);
+  const int n_marked = *(volatile int*)&ctr->n_marked;
+  if (n_marked <= kSortCap) {
+    // Steady state: the few requested buckets were appended by k_mark; sort
+    // them ascending (bitonic, in shared memory) and clear their bits.
+    int P = 2;
+    while (P < n_marked) P <<= 1;
+    for (int i = tid; i < P; i += nt) s_sort[i] = i < n_marked ? __ldcg(req_marked + i) : 0x7fffffff;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < P; i += nt) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int x = s_sort[i], y = s_sort[ixj];
+            if ((x > y) == ((i & k) == 0)) {
+              s_sort[i] = y;
+              s_sort[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = tid; i < n_marked; i += nt) {
+      const int b = s_sort[i];
+      if (i < max_requests) req_list[i] = b;
+      req_bits[b >> 5] = 0u;  // every set bit of this frame is in the list
+    }
+    if (tid == 0) s_total = n_marked;
+    __syncthreads();
+  } else {
   // Words are read as uint4 with all of a thread's loads in flight at once
   // (n_words is a multiple of 4 whenever bucket_count >= 128; smaller tables
   // take the scalar path).
@@ -200,7 +249,6 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_
   int base = incl - cnt + ((tid >> 5) ? s_scan[32 + (tid >> 5) - 1] : 0);
   if (tid == nt - 1) s_total = base + cnt;
   __syncthreads();
-  const int n = min(s_total, max_requests);
   if (cnt) {
     const int w0 = vec ? u0 * 4 : u0, w1 = vec ? u1 * 4 : u1;
     for (int w = w0; w < w1; ++w) {
@@ -215,7 +263,9 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_
       }
     }
   }
+  }
   __syncthreads();
+  const int n = min(s_total, max_requests);
   // bucket-full test -> excess ranks, in list order
   const int c2 = (n + nt - 1) / nt;
   const int r0 = min(tid * c2, n), r1 = min(r0 + c2, n);
@@ -274,6 +324,7 @@ __global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_
     ctr->n_requests = n;
     ctr->visible_count = 0;
     ctr->modified_voxels = 0;
+    ctr->n_marked = 0;
     *meta = m;
   }
 }

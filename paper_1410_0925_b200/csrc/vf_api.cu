@@ -67,6 +67,8 @@ struct vf_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // parallel graph branch (k_ranges)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
 
   int vsize = 4;
@@ -86,6 +88,7 @@ struct vf_ctx {
   unsigned long long* req_key = nullptr;
   uint32_t* req_bits = nullptr;
   int* req_list = nullptr;
+  int* req_marked = nullptr;
   int* req_excess_rank = nullptr;
   int* alloc_list = nullptr;
   int alloc_cap = 0;
@@ -230,13 +233,12 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     ++launches;
   }
   stage_mark(c, 1);
-  k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
-  VF_LAUNCHED(c, "k_prep");
-  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, hash_view(c), s.voxel_size, s.mu,
-                                                c->req_key, c->req_bits, &c->dstate->ctr);
+  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
+                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->req_key,
+                                                c->req_bits, c->req_marked, &c->dstate->ctr);
   VF_LAUNCHED(c, "k_mark");
-  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_list, c->req_excess_rank,
-                                   s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
+  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
+                                   c->req_excess_rank, s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
                                    c->frag_w * c->frag_h);
   VF_LAUNCHED(c, "k_alloc_scan");
   k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
@@ -250,6 +252,17 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   VF_LAUNCHED(c, "k_visible");
   launches += 5;
   stage_mark(c, 2);
+  // k_ranges needs only the visible list and the pose: it runs on a side
+  // stream concurrently with integration (a parallel branch of the graph).
+  const bool fork = !c->profiling;
+  if (fork) {
+    VF_CUDA(c, cudaEventRecord(c->ev_fork, st));
+    VF_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    k_ranges<<<c->num_sms * 2, 256, 0, c->side>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp,
+                                                  c->din, s.voxel_size, s.near_clip, s.far_clip, c->ranges,
+                                                  c->frag_w);
+    VF_CUDA(c, cudaEventRecord(c->ev_join, c->side));
+  }
   const bool color = c->vsize == 8;
   if (color)
     k_integrate_rgb<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
@@ -262,12 +275,16 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   VF_LAUNCHED(c, "k_integrate");
   ++launches;
   stage_mark(c, 3);
-  k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
-                                           s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
+  if (fork) {
+    VF_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+  } else {
+    k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
+                                             s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
+  }
   VF_LAUNCHED(c, "k_ranges");
   k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
-                                                         c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
-                                                         s.voxel_size, s.mu, c->points, c->normals);
+                                                             c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
+                                                             s.voxel_size, s.mu, c->points, c->normals);
   VF_LAUNCHED(c, "k_raycast");
   launches += 2;
   stage_mark(c, 4);
@@ -277,7 +294,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
 }
 
 int run_frame(vf_ctx* c, bool track, bool with_rgb) {
-  if (c->s.use_graphs && c->graphs_ok && !c->profiling) {
+  if (c->s.use_graphs && c->graphs_ok && !c->profiling && !debug_sync()) {
     cudaGraphExec_t& g = c->graph[track][with_rgb];
     if (!g) {
       cudaGraph_t graph = nullptr;
@@ -378,7 +395,7 @@ void free_all(vf_ctx* c) {
   for (auto& row : c->graph)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
-  void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list,
+  void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list, c->req_marked,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
                   c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf};
   for (void* p : ptrs)
@@ -389,6 +406,9 @@ void free_all(vf_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->ev_frame0) cudaEventDestroy(c->ev_frame0);
   if (c->ev_frame1) cudaEventDestroy(c->ev_frame1);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -498,7 +518,10 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   c->calib = *calib;
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
-  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return VF_ERR_CUDA;
   }
@@ -554,6 +577,7 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->req_key, sizeof(unsigned long long) * (size_t)s->bucket_count)) ||
       (rc = dalloc(c, &c->req_bits, sizeof(uint32_t) * (size_t)(s->bucket_count / 32))) ||
       (rc = dalloc(c, &c->req_list, sizeof(int) * (size_t)s->bucket_count)) ||
+      (rc = dalloc(c, &c->req_marked, sizeof(int) * (size_t)kMarkedCap)) ||
       (rc = dalloc(c, &c->req_excess_rank, sizeof(int) * (size_t)s->bucket_count)) ||
       (rc = dalloc(c, &c->alloc_list, sizeof(int) * (size_t)c->alloc_cap)) ||
       (rc = dalloc(c, &c->visible_list, sizeof(int) * (size_t)c->alloc_cap)) ||
@@ -738,11 +762,11 @@ int vf_stage_allocate(vf_ctx* c, const float* depth_m, const double pose[12], vf
   cudaStream_t st = c->stream;
   if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
   if (int rc = set_pose_dev(c, pose)) return rc;
-  k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
-  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, hash_view(c), s.voxel_size, s.mu,
-                                                c->req_key, c->req_bits, &c->dstate->ctr);
-  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_list, c->req_excess_rank,
-                                   s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
+  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
+                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->req_key,
+                                                c->req_bits, c->req_marked, &c->dstate->ctr);
+  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
+                                   c->req_excess_rank, s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
                                    c->frag_w * c->frag_h);
   k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
                                                 c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
@@ -987,7 +1011,7 @@ long vf_last_modified_voxels(vf_ctx* c) {
 
 int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
   if (!c) return VF_ERR_INVALID;
-  return 8 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 2 : 1) : 0);
+  return 7 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 2 : 1) : 0);
 }
 
 }  // extern "C"

@@ -56,10 +56,13 @@ struct IcpArgs {
 };
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);
-__global__ void k_mark(const float* depth, IntrD in, const FrameParams* fp, HashView hv, float voxel_size, float mu,
-                       unsigned long long* req_key, uint32_t* req_bits, Counters* ctr);
-__global__ void k_alloc_scan(uint32_t* req_bits, int n_words, HashView hv, int* req_list, int* req_excess_rank,
-                             int max_requests, AllocMeta* meta, Counters* ctr, float2* ranges, int n_frag);
+constexpr int kMarkedCap = 4096;  // == kSortCap in vf_alloc.cu
+__global__ void k_mark(const float* depth, IntrD in, const PoseD* pose, IntrD rgb_in, PoseD depth_to_rgb,
+                       FrameParams* fp, HashView hv, float voxel_size, float mu, unsigned long long* req_key,
+                       uint32_t* req_bits, int* req_marked, Counters* ctr);
+__global__ void k_alloc_scan(uint32_t* req_bits, int n_words, HashView hv, const int* req_marked, int* req_list,
+                             int* req_excess_rank, int max_requests, AllocMeta* meta, Counters* ctr, float2* ranges,
+                             int n_frag);
 __global__ void k_alloc_apply(const float* depth, IntrD in, const FrameParams* fp, float voxel_size, float mu,
                               HashEntry* entries, uint32_t mask, int bucket_size, int ordered,
                               unsigned long long* req_key, const int* req_list, const int* req_excess_rank,
