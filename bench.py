@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--l2-flush-mib", type=int, default=256)
+    ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
+                    help="N>1: shard one volume across the GPUs (config 5) or run independent replicas")
     return ap.parse_args()
 
 
@@ -251,9 +253,22 @@ def run_ours(args, dist: Dist):
                          c_frames[i].ptr if rgb else None, device=device)
     settings, calib = settings_from_config(cfg)
     flush = args.l2_flush_mib << 20
+    sharded = dist.world > 1 and args.mode == "shard"
+    if sharded:
+        from dataclasses import replace
+
+        settings = replace(settings, shard_count=dist.world, shard_index=dist.rank)
+
+    def new_pipeline():
+        p = make_pipeline(settings, calib, device=device)
+        if sharded:  # NCCL nearest-depth composite inside the frame graph
+            from paper_1410_0925_b200.sharding import attach_nccl
+
+            attach_nccl(p, dist.rank, dist.world, dist.pg)
+        return p
 
     def run_device(collect_stages=False):
-        p = make_pipeline(settings, calib, device=device)
+        p = new_pipeline()
         hctx = p.handle
         ms_frames, vis_blocks, modified = [], [], []
         stage = np.zeros(8)
@@ -293,12 +308,13 @@ def run_ours(args, dist: Dist):
     clk = clocks.stop()
     t_local = float(ms_frames.sum()) / 1000.0
     t_max = dist.max(t_local)
-    frames_total = dist.sum(float(args.steps))
+    # sharded: all ranks cooperate on the same frames; replicas: each rank its own
+    frames_total = float(args.steps) if sharded else dist.sum(float(args.steps))
     value = frames_total / t_max
     vox_updates = dist.sum(float(vis.sum() * 512)) / t_max
 
     # --- e2e pass: host pinned buffers through vf_process_frame ---
-    p = make_pipeline(settings, calib, device=device)
+    p = new_pipeline()
     hctx = p.handle
     npix = w * h
     host_depth = []
@@ -369,7 +385,8 @@ def run_ours(args, dist: Dist):
                         f"{'VoxelSRgb' if rgb else 'VoxelS'}, hash {cfg.hash.bucket_count}x{cfg.hash.bucket_size}"
                         f"+{cfg.hash.excess_count} / {cfg.hash.block_count} blocks, "
                         f"{'ICP tracking on' if cfg.tracking else 'known poses'}",
-            "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single GPU",
+            "parallelism": (f"volume sharded by block hash over {dist.world} GPUs (NCCL map composite)" if sharded
+                            else f"replicas x{dist.world}" if dist.world > 1 else "single GPU"),
             "l2": f"flushed between frames ({args.l2_flush_mib} MiB write, outside the timed intervals)",
             "graphs": True,
         },

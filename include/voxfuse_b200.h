@@ -75,6 +75,12 @@ typedef struct vf_settings {
   double max_condition;
   int tracking; /* 1: ICP tracker (reference behaviour); 0: known poses via vf_set_pose (config 2) */
   int use_graphs; /* 1: replay each frame as one CUDA graph */
+  /* Spatial sharding (config 5): this context owns the blocks whose super-block
+   * (2^shard_shift blocks per axis) hashes to shard_index mod shard_count. */
+  int shard_count;
+  int shard_index;
+  int shard_shift;
+  int shard_halo; /* 1: also fuse surfaces within one block of this shard's territory */
 } vf_settings;
 
 typedef struct vf_intrinsics { /* Intrinsics (core/intrinsics.hpp:10-32) */
@@ -180,6 +186,19 @@ int vf_depth_pyramid(vf_ctx* ctx, const float* depth_m, float* out);
 int vf_render_synthetic(int device, int n_spheres, const double* spheres, int n_planes, const double* planes,
                         const double world_to_cam[12], const vf_intrinsics* intr, double near_clip,
                         double far_clip, float* d_depth, uint8_t* d_rgb);
+
+/* --- spatial sharding ---
+ * Owner shard of a block position (the device rule, for hosts and tests). */
+int vf_shard_owner(int bx, int by, int bz, int shard_shift, int shard_count);
+/* One process per GPU: rank 0 creates an NCCL unique id (128 bytes), every
+ * rank attaches with it; each frame then ends with the nearest-depth map
+ * composite (all-reduce MIN of depth keys, masked all-reduce SUM of the maps)
+ * inside the frame graph, and the replicated ICP needs no collective. */
+int vf_shard_nccl_unique_id(void* out128);
+int vf_shard_attach_nccl(vf_ctx* ctx, const void* unique_id128, int nranks, int rank);
+/* Several shards in one process on the same device (tests, single-GPU
+ * boxes): composite the n contexts' maps after each frame. */
+int vf_shard_composite_local(vf_ctx** ctxs, int n);
 
 /* --- device memory helpers for callers without a CUDA runtime of their own --- */
 void* vf_device_alloc(size_t bytes);

@@ -36,6 +36,7 @@ EXPORTS = [
     "vf_import_state", "vf_export_visible_list", "vf_export_ranges",
     "vf_stage_allocate", "vf_stage_integrate", "vf_stage_raycast", "vf_stage_icp", "vf_icp_trace",
     "vf_depth_pyramid", "vf_render_synthetic",
+    "vf_shard_owner", "vf_shard_nccl_unique_id", "vf_shard_attach_nccl", "vf_shard_composite_local",
     "vf_device_alloc", "vf_device_free", "vf_memcpy_h2d", "vf_memcpy_d2h", "vf_host_alloc_pinned",
     "vf_host_free_pinned", "vf_event_record", "vf_event_elapsed_ms", "vf_set_profiling", "vf_stage_times",
     "vf_kernel_launches_per_frame", "vf_readback_bytes", "vf_flush_l2", "vf_last_modified_voxels",
@@ -67,6 +68,10 @@ class VfSettings(C.Structure):
         ("max_condition", C.c_double),
         ("tracking", C.c_int),
         ("use_graphs", C.c_int),
+        ("shard_count", C.c_int),
+        ("shard_index", C.c_int),
+        ("shard_shift", C.c_int),
+        ("shard_halo", C.c_int),
     ]
 
 
@@ -161,6 +166,10 @@ def load() -> C.CDLL:
         "vf_depth_pyramid": (C.c_int, [vp, vp, vp]),
         "vf_render_synthetic": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, vp, dp, C.POINTER(VfIntrinsics),
                                           C.c_double, C.c_double, vp, vp]),
+        "vf_shard_owner": (C.c_int, [C.c_int] * 5),
+        "vf_shard_nccl_unique_id": (C.c_int, [vp]),
+        "vf_shard_attach_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+        "vf_shard_composite_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
         "vf_device_alloc": (C.c_void_p, [C.c_size_t]),
         "vf_device_free": (C.c_int, [vp]),
         "vf_memcpy_h2d": (C.c_int, [vp, vp, C.c_size_t]),

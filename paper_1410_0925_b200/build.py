@@ -25,7 +25,7 @@ OUT_DIR = PKG / "lib"
 LIB = OUT_DIR / "libvoxfuse_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["vf_alloc.cu", "vf_integrate.cu", "vf_raycast.cu", "vf_icp.cu", "vf_misc.cu", "vf_api.cu"]
+SOURCES = ["vf_alloc.cu", "vf_integrate.cu", "vf_raycast.cu", "vf_icp.cu", "vf_misc.cu", "vf_shard.cu", "vf_api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",
@@ -82,7 +82,7 @@ def build(verbose: bool = False, force: bool = False, out_dir: Path | None = Non
     objs = [str(obj_dir / (s + ".o")) for s in SOURCES]
     if force or jobs or _stale(lib, objs):
         cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib), *objs,
-               "-Xcompiler", "-fPIC", "-cudart", "static"]
+               "-Xcompiler", "-fPIC", "-cudart", "static", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stderr)

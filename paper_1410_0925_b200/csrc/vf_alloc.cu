@@ -101,7 +101,7 @@ __global__ void k_prep(const PoseD* __restrict__ pose, IntrD depth_in, IntrD rgb
 // the frame's camera parameters (k_prep's job) for the later kernels.
 __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, IntrD in, const PoseD* __restrict__ pose,
                                               IntrD rgb_in, PoseD depth_to_rgb, FrameParams* __restrict__ fp,
-                                              HashView hv, float voxel_size, float mu,
+                                              HashView hv, float voxel_size, float mu, ShardSpec shard,
                                               unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
                                               int* __restrict__ req_marked, Counters* __restrict__ ctr) {
   __shared__ PoseD s_c2w;
@@ -124,6 +124,23 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
   const int y = pixel / in.width, x = pixel - y * in.width;
   D3 p0, p1;
   pixel_segment(x, y, d, in, s_c2w, voxel_size, mu, p0, p1);
+  if (shard.count > 1) {
+    // A pixel belongs to the shard owning the block of its observed surface
+    // point; that shard allocates the whole +-mu band of the pixel, so every
+    // surface is fused and raycast with its full band in one shard (blocks of
+    // bands that straddle a seam are allocated by both neighbours).
+    const double inv_block = 1.0 / (double)(voxel_size * (float)kBlockSide);
+    const D3 dir = mk((x - in.cx) / in.fx, (y - in.cy) / in.fy, 1.0);
+    const D3 ps = apply(s_c2w, mk(dir.x * (double)d, dir.y * (double)d, dir.z * (double)d));
+    const int sbx = __double2int_rz(floor(ps.x * inv_block)), sby = __double2int_rz(floor(ps.y * inv_block)),
+              sbz = __double2int_rz(floor(ps.z * inv_block));
+    // ... and, with the halo, every shard owning a block within one block of
+    // it, so trilinear / normal stencils never straddle a seam.
+    bool mine = shard_owner(sbx, sby, sbz, shard) == shard.index;
+    for (int k = 0; k < 27 && !mine && shard.halo; ++k)
+      mine = shard_owner(sbx + k % 3 - 1, sby + (k / 3) % 3 - 1, sbz + k / 9 - 1, shard) == shard.index;
+    if (!mine) return;
+  }
   const unsigned long long key_base = (unsigned long long)(pixel + 1) << kStepBits;
   dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
     if (find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0) {

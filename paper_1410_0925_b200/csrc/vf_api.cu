@@ -108,6 +108,10 @@ struct vf_ctx {
   size_t icp_smem = 0;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
+  // sharding
+  ShardSpec shard{1, 0, 2, 1};
+  void* nccl_comm = nullptr;
+  unsigned long long* shard_keys = nullptr;
   int icp_grid = 0;
 
   // host state
@@ -234,7 +238,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   }
   stage_mark(c, 1);
   k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
-                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->req_key,
+                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
                                                 c->req_bits, c->req_marked, &c->dstate->ctr);
   VF_LAUNCHED(c, "k_mark");
   k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
@@ -287,6 +291,14 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
                                                              s.voxel_size, s.mu, c->points, c->normals);
   VF_LAUNCHED(c, "k_raycast");
   launches += 2;
+  if (c->nccl_comm) {  // nearest-depth composite across the GPUs (vf_shard.cu)
+    if (nccl_composite(c->nccl_comm, st, &c->dstate->fp, c->points, c->normals, c->shard_keys, c->npix,
+                       c->shard.index) != 0) {
+      c->err = "NCCL composite failed";
+      return VF_ERR_CUDA;
+    }
+    launches += 2;
+  }
   stage_mark(c, 4);
   c->launches_last = launches;
   VF_CUDA(c, cudaGetLastError());
@@ -392,12 +404,13 @@ int dalloc(vf_ctx* c, T** p, size_t bytes) {
 }
 
 void free_all(vf_ctx* c) {
+  if (c->nccl_comm) nccl_comm_destroy(c->nccl_comm);
   for (auto& row : c->graph)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list, c->req_marked,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
-                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf};
+                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -492,6 +505,10 @@ void vf_default_settings(vf_settings* s) {
   s->max_condition = 1e8;
   s->tracking = 1;
   s->use_graphs = 1;
+  s->shard_count = 1;
+  s->shard_index = 0;
+  s->shard_shift = 3;
+  s->shard_halo = 1;
 }
 
 int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out) {
@@ -526,6 +543,15 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     return VF_ERR_CUDA;
   }
   c->vsize = s->voxel_type == VF_VOXEL_S_RGB ? 8 : 4;
+  if (s->shard_count > 1) {
+    if (s->shard_count > kMaxShards || s->shard_index < 0 || s->shard_index >= s->shard_count || s->shard_shift < 0 ||
+        s->shard_shift > 8) {
+      free_all(c);
+      delete c;
+      return VF_ERR_INVALID;
+    }
+    c->shard = ShardSpec{s->shard_count, s->shard_index, s->shard_shift, s->shard_halo};
+  }
   c->ordered = s->bucket_count * s->bucket_size;
   c->entry_count = c->ordered + s->excess_count;
   c->mask = (uint32_t)(s->bucket_count - 1);
@@ -589,7 +615,8 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->points, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->normals, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->partials, sizeof(double) * 2 * 32 * (size_t)c->icp_grid)) ||
-      (rc = dalloc(c, &c->trace, sizeof(double) * kTraceRow * kTraceCap))) {
+      (rc = dalloc(c, &c->trace, sizeof(double) * kTraceRow * kTraceCap)) ||
+      (rc = dalloc(c, &c->shard_keys, sizeof(unsigned long long) * (size_t)c->npix))) {
     free_all(c);
     delete c;
     return rc;
@@ -763,7 +790,7 @@ int vf_stage_allocate(vf_ctx* c, const float* depth_m, const double pose[12], vf
   if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
   if (int rc = set_pose_dev(c, pose)) return rc;
   k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
-                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->req_key,
+                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
                                                 c->req_bits, c->req_marked, &c->dstate->ctr);
   k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
                                    c->req_excess_rank, s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
@@ -986,6 +1013,52 @@ long vf_selftest_division(int device, int mode, float p0, float p1, float p2, lo
   cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
   cudaFree(d);
   return e == cudaSuccess ? (long)h : VF_ERR_CUDA;
+}
+
+int vf_shard_owner(int bx, int by, int bz, int shard_shift, int shard_count) {
+  return shard_owner(bx, by, bz, ShardSpec{shard_count, 0, shard_shift, 0});
+}
+
+int vf_shard_nccl_unique_id(void* out128) {
+  if (!out128) return VF_ERR_INVALID;
+  return nccl_unique_id(out128) == 0 ? VF_OK : VF_ERR_NO_DEVICE;
+}
+
+int vf_shard_attach_nccl(vf_ctx* c, const void* id, int nranks, int rank) {
+  if (!c || !id || nranks != c->shard.count || rank != c->shard.index) return VF_ERR_INVALID;
+  cudaSetDevice(c->device);
+  if (nccl_comm_init(&c->nccl_comm, id, nranks, rank) != 0) {
+    c->err = "ncclCommInitRank failed";
+    return VF_ERR_CUDA;
+  }
+  for (auto& row : c->graph)  // the frame graph now ends with the composite
+    for (auto& g : row)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+  return VF_OK;
+}
+
+int vf_shard_composite_local(vf_ctx** ctxs, int n) {
+  if (!ctxs || n < 1 || n > kMaxShards) return VF_ERR_INVALID;
+  const int npix = ctxs[0]->npix;
+  ShardGroupArgs g{};
+  g.n = n;
+  for (int i = 0; i < n; ++i) {
+    vf_ctx* c = ctxs[i];
+    if (!c || c->npix != npix || c->device != ctxs[0]->device || c->shard.index != i) return VF_ERR_INVALID;
+    k_shard_keys<<<(npix + 255) / 256, 256, 0, c->stream>>>(c->points, &c->dstate->fp, npix, i, c->shard_keys);
+    VF_CUDA(c, cudaGetLastError());
+    VF_CUDA(c, cudaStreamSynchronize(c->stream));
+    g.keys[i] = c->shard_keys;
+    g.points[i] = c->points;
+    g.normals[i] = c->normals;
+  }
+  k_shard_group_composite<<<(npix + 255) / 256, 256, 0, ctxs[0]->stream>>>(g, npix);
+  VF_CUDA(ctxs[0], cudaGetLastError());
+  VF_CUDA(ctxs[0], cudaStreamSynchronize(ctxs[0]->stream));
+  return VF_OK;
 }
 
 long vf_readback_bytes(const vf_ctx* c) { return c ? (long)sizeof(DevState) : -1; }

@@ -57,9 +57,21 @@ struct IcpArgs {
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);
 constexpr int kMarkedCap = 4096;  // == kSortCap in vf_alloc.cu
+struct ShardSpec {
+  int count, index, shift;  // G shards, this shard, super-block shift s
+  int halo;                 // also fuse bands whose surface block neighbours this shard's territory
+};
+// Owner of a block: hash of its super-block (2^s blocks per axis) mod G.
+__host__ __device__ inline int shard_owner(int bx, int by, int bz, const ShardSpec& sp) {
+  if (sp.count <= 1) return 0;
+  const uint32_t h = ((uint32_t)(bx >> sp.shift) * 73856093u) ^ ((uint32_t)(by >> sp.shift) * 19349669u) ^
+                     ((uint32_t)(bz >> sp.shift) * 83492791u);
+  return (int)(h % (uint32_t)sp.count);
+}
+
 __global__ void k_mark(const float* depth, IntrD in, const PoseD* pose, IntrD rgb_in, PoseD depth_to_rgb,
-                       FrameParams* fp, HashView hv, float voxel_size, float mu, unsigned long long* req_key,
-                       uint32_t* req_bits, int* req_marked, Counters* ctr);
+                       FrameParams* fp, HashView hv, float voxel_size, float mu, ShardSpec shard,
+                       unsigned long long* req_key, uint32_t* req_bits, int* req_marked, Counters* ctr);
 __global__ void k_alloc_scan(uint32_t* req_bits, int n_words, HashView hv, const int* req_marked, int* req_list,
                              int* req_excess_rank, int max_requests, AllocMeta* meta, Counters* ctr, float2* ranges,
                              int n_frag);
@@ -91,5 +103,21 @@ __global__ void k_init_ranges(float2* ranges, int n);
 __global__ void k_reset_visible(Counters* ctr);
 __global__ void k_divtest_const(float b, uint32_t lo_bits, uint32_t n_bits, unsigned long long* mism);
 __global__ void k_divtest_rand(float amax, float bmin, float bmax, unsigned long long n, unsigned long long* mism);
+
+constexpr int kMaxShards = 16;
+struct ShardGroupArgs {
+  int n;
+  const unsigned long long* keys[kMaxShards];
+  float4* points[kMaxShards];
+  float4* normals[kMaxShards];
+};
+__global__ void k_shard_keys(const float4* points, const FrameParams* fp, int npix, int rank, unsigned long long* keys);
+__global__ void k_shard_select(const unsigned long long* keys_min, int npix, int rank, float4* points, float4* normals);
+__global__ void k_shard_group_composite(ShardGroupArgs g, int npix);
+int nccl_unique_id(void* out);
+int nccl_comm_init(void** comm, const void* id_bytes, int nranks, int rank);
+void nccl_comm_destroy(void* comm);
+int nccl_composite(void* comm, cudaStream_t st, const FrameParams* fp, float4* points, float4* normals,
+                   unsigned long long* keys, int npix, int rank);
 
 }  // namespace vf

@@ -95,6 +95,10 @@ class EngineSettings:
     max_condition: float = 1e8
     tracking: bool = True
     use_graphs: bool = True
+    shard_count: int = 1   # spatial sharding (config 5): G shards ...
+    shard_index: int = 0   # ... this context's shard ...
+    shard_shift: int = 3   # ... owning super-blocks of 2^shift blocks per axis
+    shard_halo: bool = True  # ... and fusing surfaces within one block of them
 
     def to_c(self) -> VfSettings:
         s = VfSettings()

@@ -1,0 +1,107 @@
+"""Spatial sharding of the volume across GPUs (BASELINE config 5).
+
+Host-side mirror of the device rules in csrc/vf_shard.cu plus the drivers:
+
+* ``shard_owner`` — block -> shard: hash of the super-block (2^s blocks per
+  axis) mod G (same arithmetic as ``vf_shard_owner``);
+* ``composite_keys`` / ``composite`` — the per-frame nearest-depth exchange,
+  written against ``torch.distributed`` so the protocol is testable on CPU
+  with gloo (tests/test_multi_rank.py); on GPUs the same exchange runs as
+  NCCL collectives inside the frame graph (``vf_shard_attach_nccl``);
+* ``LocalShardGroup`` — G shards in one process on one device (tests,
+  single-GPU boxes), composited by ``vf_shard_composite_local``;
+* ``attach_nccl`` — one process per GPU: NCCL unique id from rank 0 over the
+  host process group, then every rank's context attaches.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from .pipeline import Pipeline, make_pipeline
+
+NO_HIT = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def shard_owner(bx, by, bz, shift: int, count: int):
+    """Owner shard of block positions (numpy arrays or ints)."""
+    if count <= 1:
+        return np.zeros(np.broadcast(bx, by, bz).shape, np.int64) if np.ndim(bx) else 0
+    sx = (np.asarray(bx, np.int64) >> shift).astype(np.uint32)
+    sy = (np.asarray(by, np.int64) >> shift).astype(np.uint32)
+    sz = (np.asarray(bz, np.int64) >> shift).astype(np.uint32)
+    with np.errstate(over="ignore"):
+        h = (sx * np.uint32(73856093)) ^ (sy * np.uint32(19349669)) ^ (sz * np.uint32(83492791))
+    return (h % np.uint32(count)).astype(np.int64)
+
+
+def composite_keys(points: np.ndarray, w2c: np.ndarray, rank: int) -> np.ndarray:
+    """Per-pixel key float_bits(camera z of the hit) << 32 | rank, NO_HIT
+    where the shard has no hit (k_shard_keys)."""
+    p = points.reshape(-1, 4).astype(np.float64)
+    r = np.asarray(w2c, np.float64)
+    z = r[6] * p[:, 0] + r[7] * p[:, 1] + r[8] * p[:, 2] + r[11]
+    zf = np.where(z > 0, z, 0).astype(np.float32)
+    keys = (zf.view(np.uint32).astype(np.uint64) << np.uint64(32)) | np.uint64(rank)
+    return np.where(points.reshape(-1, 4)[:, 3] != 0, keys, NO_HIT)
+
+
+def composite(points: np.ndarray, normals: np.ndarray, w2c: np.ndarray, rank: int, dist) -> tuple:
+    """The exchange over a torch.distributed process group: all_reduce(MIN)
+    of the keys, mask to the winner, all_reduce(SUM) of the maps.  Exact:
+    every pixel sums one non-zero contribution with zeros."""
+    import torch
+
+    keys = composite_keys(points, w2c, rank)
+    kt = torch.from_numpy(keys.view(np.int64).copy())
+    # uint64 keys compare like int64 once the sign bit is flipped
+    kt ^= torch.tensor(np.int64(-(2 ** 63)))
+    dist.all_reduce(kt, op=dist.ReduceOp.MIN)
+    kt ^= torch.tensor(np.int64(-(2 ** 63)))
+    kmin = kt.numpy().view(np.uint64)
+    won = (kmin != NO_HIT) & ((kmin & np.uint64(0xFFFFFFFF)) == np.uint64(rank))
+    p = np.where(won[:, None], points.reshape(-1, 4), 0).astype(np.float32)
+    n = np.where(won[:, None], normals.reshape(-1, 4), 0).astype(np.float32)
+    pt, nt = torch.from_numpy(p), torch.from_numpy(n)
+    dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+    dist.all_reduce(nt, op=dist.ReduceOp.SUM)
+    return pt.numpy().reshape(points.shape), nt.numpy().reshape(normals.shape)
+
+
+class LocalShardGroup:
+    """G shards of one volume in this process on one device."""
+
+    def __init__(self, settings, calib, count: int, shift: int = 3, device: int = 0, halo: bool = True):
+        from dataclasses import replace
+
+        self.shards = [make_pipeline(replace(settings, shard_count=count, shard_index=i, shard_shift=shift, shard_halo=halo), calib,
+                                     device) for i in range(count)]
+        self._handles = (C.c_void_p * count)(*[s.handle.value for s in self.shards])
+
+    def set_pose(self, pose):
+        for s in self.shards:
+            s.set_pose(pose)
+
+    def process_frame(self, rgb, depth_m):
+        stats = [s.process_frame(rgb, depth_m) for s in self.shards]
+        _abi.check("vf_shard_composite_local",
+                   _abi.load().vf_shard_composite_local(self._handles, len(self.shards)))
+        return stats
+
+    def close(self):
+        for s in self.shards:
+            s.close()
+
+
+def attach_nccl(pipe: Pipeline, rank: int, world: int, dist) -> None:
+    """One process per GPU: share rank 0's NCCL id over `dist` and attach."""
+    L = _abi.load()
+    buf = (C.c_uint8 * 128)()
+    if rank == 0:
+        _abi.check("vf_shard_nccl_unique_id", L.vf_shard_nccl_unique_id(buf))
+    obj = [bytes(buf)]
+    dist.broadcast_object_list(obj, src=0)
+    idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+    _abi.check("vf_shard_attach_nccl", L.vf_shard_attach_nccl(pipe.handle, idb, world, rank))

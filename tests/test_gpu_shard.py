@@ -1,0 +1,108 @@
+"""GPU: spatial sharding (config 5) with G shards of one volume on one device
+(vf_shard_composite_local), against the unsharded pipeline.  The cross-GPU
+transport (NCCL) carries the identical exchange; its protocol is tested over
+gloo in tests/test_multi_rank.py and its plumbing with one rank below."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import vf_py
+from helpers import allocated_blocks, centre_dist, frames, rot_angle
+from paper_1410_0925_b200 import _abi, make_pipeline, settings_from_config
+from paper_1410_0925_b200.scene import CONFIGS
+from paper_1410_0925_b200.sharding import LocalShardGroup, shard_owner
+
+pytestmark = pytest.mark.gpu
+
+
+def _maps_agreement(ref, shard, vs):
+    pr, nr = ref.tracking_state()
+    pg, ng = shard.tracking_state()
+    hr, hg = pr[..., 3] > 0, pg[..., 3] > 0
+    both = hr & hg
+    dp = np.linalg.norm(pr[..., :3] - pg[..., :3], axis=-1)[both]
+    ang = np.degrees(np.arccos(np.clip((nr[..., :3] * ng[..., :3]).sum(-1)[both], -1, 1)))
+    return np.mean(hr == hg), np.mean(dp <= 0.5 * vs), np.mean(ang <= 1.0)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_known_pose_matches_unsharded(olib, G):
+    cfg = CONFIGS["C1"].with_(tracking=False)
+    s, c = settings_from_config(cfg)
+    ref = make_pipeline(s, c)
+    grp = LocalShardGroup(s, c, G, shift=3)
+    for pose, d, _ in frames(olib, cfg, 3):
+        ref.set_pose(pose)
+        grp.set_pose(pose)
+        ref.process_frame(None, d)
+        grp.process_frame(None, d)
+    # every shard holds the identical composited maps
+    p0, n0 = grp.shards[0].tracking_state()
+    for g in grp.shards[1:]:
+        p1, n1 = g.tracking_state()
+        assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+        assert np.array_equal(n0.view(np.uint32), n1.view(np.uint32))
+    # the shards together hold every block the single volume holds
+    br = allocated_blocks(ref.entries(), ref.voxels(), 4)
+    union = set()
+    for g in grp.shards:
+        union |= set(allocated_blocks(g.entries(), g.voxels(), 4))
+    assert set(br) <= union
+    # ownership: a shard's blocks are its own territory or within one block of it
+    hit, pts, nrm = _maps_agreement(ref, grp.shards[0], cfg.voxel_size)
+    assert hit >= 0.99 and pts >= 0.995 and nrm >= 0.98, (hit, pts, nrm)
+    grp.close()
+    ref.close()
+
+
+def test_sharded_tracking_replicated_icp(olib):
+    """Replicated ICP on the composited maps: every shard computes the same
+    pose bit for bit; poses stay within tracking tolerance of the unsharded run."""
+    cfg = CONFIGS["C1"]
+    s, c = settings_from_config(cfg)
+    ref = make_pipeline(s, c)
+    grp = LocalShardGroup(s, c, 2, shift=3)
+    for pose, d, _ in frames(olib, cfg, 6):
+        sr = ref.process_frame(None, d)
+        st = grp.process_frame(None, d)
+        assert all(x.tracking_ok for x in st)
+        ps = [g.pose() for g in grp.shards]
+        assert all(np.array_equal(ps[0], p) for p in ps[1:])
+        assert rot_angle(ref.pose(), ps[0]) < 1e-3 and centre_dist(ref.pose(), ps[0]) < 1e-3
+    hit, pts, _ = _maps_agreement(ref, grp.shards[0], cfg.voxel_size)
+    assert hit >= 0.99 and pts >= 0.99
+    grp.close()
+    ref.close()
+
+
+def test_owner_rule_matches_device():
+    L = _abi.load()
+    rng = np.random.default_rng(7)
+    b = rng.integers(-500, 500, size=(2000, 3))
+    for shift, g in [(0, 2), (3, 4), (3, 8), (2, 3)]:
+        dev = [L.vf_shard_owner(int(x), int(y), int(z), shift, g) for x, y, z in b]
+        assert np.array_equal(dev, shard_owner(b[:, 0], b[:, 1], b[:, 2], shift, g))
+
+
+def test_nccl_composite_plumbing_single_rank(olib):
+    """NCCL path with one rank: unique id, communicator, collectives captured
+    in the frame graph; with one rank the composite must be the identity."""
+    L = _abi.load()
+    cfg = CONFIGS["T320"].with_(tracking=False)
+    s, c = settings_from_config(cfg)
+    ref = make_pipeline(s, c)
+    p = make_pipeline(s, c)
+    buf = (C.c_uint8 * 128)()
+    rc = L.vf_shard_nccl_unique_id(buf)
+    if rc != 0:
+        pytest.skip("libnccl not loadable")
+    assert L.vf_shard_attach_nccl(p.handle, buf, 1, 0) == 0
+    for pose, d, _ in frames(olib, cfg, 3):
+        ref.set_pose(pose)
+        p.set_pose(pose)
+        ref.process_frame(None, d)
+        p.process_frame(None, d)
+    a, b = ref.tracking_state(), p.tracking_state()
+    assert np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+    assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
