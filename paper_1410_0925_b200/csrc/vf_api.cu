@@ -106,6 +106,9 @@ struct vf_ctx {
   double* trace = nullptr;
   int icp_slots = 0;
   size_t icp_smem = 0;
+  int icp_cluster = 0;      // CTAs of the coarse-level cluster (0: no cluster path)
+  int icp_coarse_levels = 0;  // levels run by the cluster kernel
+  void* icp_ctl = nullptr;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   // sharding
@@ -182,6 +185,34 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
   a.trace = c->trace;
   a.trace_cap = kTraceCap;
   a.max_slots = c->icp_slots;
+  a.ctl_io = c->icp_ctl;
+  const int coarse = c->icp_cluster ? c->icp_coarse_levels : 0;
+  if (coarse > 0) {
+    // coarse levels in one thread-block cluster (cluster barrier + DSMEM)
+    IcpArgs ac = a;
+    ac.level_hi = L - 1;
+    ac.level_lo = L - coarse;
+    ac.ctl_in = 0;
+    ac.is_last = ac.level_lo == 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c->icp_cluster);
+    cfg.blockDim = dim3(kIcpThreads);
+    cfg.dynamicSmemBytes = c->icp_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c->icp_cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VF_CUDA(c, cudaLaunchKernelEx(&cfg, k_icp_cluster, ac));
+    if (ac.is_last) return VF_OK;
+  }
+  a.level_hi = L - 1 - coarse;
+  a.level_lo = 0;
+  a.ctl_in = coarse > 0 ? 1 : 0;
+  a.is_last = 1;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c->icp_grid);
   cfg.blockDim = dim3(kIcpThreads);
@@ -410,7 +441,7 @@ void free_all(vf_ctx* c) {
       if (g) cudaGraphExecDestroy(g);
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list, c->req_marked,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
-                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys};
+                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -593,6 +624,35 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     c->icp_slots = (int)std::max(1L, std::min(need, cap));
     c->icp_smem = tables + (size_t)c->icp_slots * kIcpThreads * 8;
     cudaFuncSetAttribute(k_icp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
+    cudaFuncSetAttribute(k_icp_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
+    // Coarse levels (<= kClusterPixels pixels) go to one cluster of 16 CTAs
+    // (non-portable size) or 8 if the device cannot co-schedule 16.
+    constexpr int kClusterPixels = 8192;
+    cudaFuncSetAttribute(k_icp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int cs : {16, 8}) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(cs);
+      q.blockDim = dim3(kIcpThreads);
+      q.dynamicSmemBytes = c->icp_smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, k_icp_cluster, &q) == cudaSuccess && nclusters > 0) {
+        c->icp_cluster = cs;
+        break;
+      }
+      cudaGetLastError();
+    }
+    for (int l = (int)c->levels.size() - 1; l >= 0; --l) {
+      if ((long)c->levels[l].width * c->levels[l].height > kClusterPixels) break;
+      ++c->icp_coarse_levels;
+    }
+    if (std::getenv("VF_ICP_NO_CLUSTER")) c->icp_cluster = 0;
   }
   int rc = VF_OK;
   const size_t nvox = (size_t)s->block_count * kBlockVolume;
@@ -616,7 +676,8 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->normals, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->partials, sizeof(double) * 2 * 32 * (size_t)c->icp_grid)) ||
       (rc = dalloc(c, &c->trace, sizeof(double) * kTraceRow * kTraceCap)) ||
-      (rc = dalloc(c, &c->shard_keys, sizeof(unsigned long long) * (size_t)c->npix))) {
+      (rc = dalloc(c, &c->shard_keys, sizeof(unsigned long long) * (size_t)c->npix)) ||
+      (rc = dalloc(c, &c->icp_ctl, 1024))) {
     free_all(c);
     delete c;
     return rc;
@@ -1084,7 +1145,8 @@ long vf_last_modified_voxels(vf_ctx* c) {
 
 int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
   if (!c) return VF_ERR_INVALID;
-  return 7 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 2 : 1) : 0);
+  int icp = 1 + ((c->icp_cluster && c->icp_coarse_levels > 0 && c->icp_coarse_levels < c->s.hierarchy_levels) ? 1 : 0);
+  return 7 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 1 : 0) + icp : 0) + (c->nccl_comm ? 2 : 0);
 }
 
 }  // extern "C"

@@ -102,6 +102,29 @@ namespace {
 constexpr int kAcc = 29;  // 21 H (upper triangle) + 6 g + cost + count
 constexpr int kAccStride = 32;
 
+// Controller-only FP64 reciprocal / square root: hardware approximation plus
+// Newton steps (relative error ~1 ulp).  The controller's results already
+// differ from the reference's Eigen LDLT by rounding, so it does not need the
+// IEEE-rounded (and ~10x longer-latency) division; the per-pixel terms, which
+// decide association and rejection, keep IEEE arithmetic.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+__device__ __forceinline__ double sqrt_fast(double x) {
+  if (!(x > 0)) return sqrt(x);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  const double s0 = x * y;
+  return fma(fma(-s0, s0, x), 0.5 * y, s0);  // one Newton step on the square root
+}
+
+
 // Pivoted LDL^T of a symmetric n x n (row-major input) and solve, restating
 // Eigen's LDLT as the reference calls it (depth_tracker.hpp:209,214).  Also
 // returns the factor so the inverse can be formed for the condition bound.
@@ -286,8 +309,8 @@ __device__ bool well_conditioned(const double* h, int n, Ldlt& f, double max_con
 // R = I + K / s + K^2 / (s (s + 1)),  K = [w]x,  s = sqrt(1 + |w|^2).
 __device__ void rot_from_omega(const double* w, double* r) {
   const double th2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
-  const double s = sqrt(1.0 + th2);
-  const double a = 1.0 / s, b = 1.0 / (s * (s + 1.0));
+  const double s = sqrt_fast(1.0 + th2);
+  const double a = rcp_fast(s), b = a * rcp_fast(s + 1.0);
   const double K[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
   double K2[9];
   for (int i = 0; i < 3; ++i)
@@ -353,7 +376,7 @@ __device__ __forceinline__ bool spd_solve_fast(const double* __restrict__ tot, d
         H[s][t] = tot[k];
         H[t][s] = tot[k];
       }
-  double L[N][N], D[N];
+  double L[N][N], D[N], Dinv[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     double d = H[j][j];
@@ -361,12 +384,13 @@ __device__ __forceinline__ bool spd_solve_fast(const double* __restrict__ tot, d
     for (int k = 0; k < j; ++k) d -= (L[j][k] * L[j][k]) * D[k];
     if (!(d > 0)) return false;
     D[j] = d;
+    Dinv[j] = rcp_fast(d);
 #pragma unroll
     for (int i = j + 1; i < N; ++i) {
       double sum = H[i][j];
 #pragma unroll
       for (int k = 0; k < j; ++k) sum -= (L[i][k] * L[j][k]) * D[k];
-      L[i][j] = sum / d;
+      L[i][j] = sum * Dinv[j];
     }
   }
   // Linv = L^-1 (unit lower triangular)
@@ -391,9 +415,9 @@ __device__ __forceinline__ bool spd_solve_fast(const double* __restrict__ tot, d
     double row = 1.0;  // Li[k][k] = 1
 #pragma unroll
     for (int i = 0; i < k; ++i) row += Li[k][i] * Li[k][i];
-    tr += row / D[k];
+    tr += row * Dinv[k];
   }
-  const double bound = sqrt(hf) * tr;
+  const double bound = sqrt_fast(hf) * tr;
   if (!(bound * (1.0 + 1e-6) < max_condition)) return false;
   // solve H x = -g
   double y[N];
@@ -405,7 +429,7 @@ __device__ __forceinline__ bool spd_solve_fast(const double* __restrict__ tot, d
     y[i] = v;
   }
 #pragma unroll
-  for (int i = 0; i < N; ++i) y[i] /= D[i];
+  for (int i = 0; i < N; ++i) y[i] *= Dinv[i];
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
     double v = y[i];
@@ -463,7 +487,10 @@ struct Ctl {
   double accepted_cost, final_cost;
   int halvings, iterations, any_solved, valid_points, fail;
   int decision;  // 0 continue, 1 leave level, 2 abort
+  int trace_rows;
 };
+
+static_assert(sizeof(Ctl) <= 1024, "Ctl must fit the ctl_io buffer");
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -473,11 +500,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs a) {
-  cg::grid_group grid = cg::this_grid();
+// The ICP loop over levels [a.level_hi .. a.level_lo].  kCluster: the grid is
+// one thread-block cluster and partials travel through distributed shared
+// memory behind a hardware cluster barrier (coarse levels); otherwise the
+// grid is cooperative and partials go through global memory behind a grid
+// barrier (fine levels).  The controller state enters / leaves through
+// a.ctl_io when the loop is split between the two kernels.
+template <bool kCluster>
+__device__ __forceinline__ void icp_body(const IcpArgs& a) {
   __shared__ Ctl ctl;
   __shared__ double s_red[kIcpThreads / 32][kAccStride];
   __shared__ double s_tot[kAccStride];
+  __shared__ double s_part[2][kAccStride];  // cluster exchange (double-buffered)
   // dynamic: unprojection tables (max level-0 width + height doubles), then
   // max_slots x blockDim pixel slots (float depth, packed x | y << 16)
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -488,19 +522,24 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const bool timer = blockIdx.x == 0 && tid == 0 && a.trace;
   if (tid == 0) {
-    ctl.render = *a.state_pose;
-    // icp_track(..., initial) (depth_tracker.hpp:117): start from `initial` if given
-    ctl.c2w = pose_inverse(a.initial ? *a.initial : ctl.render);
-    ctl.iterations = 0;
-    ctl.any_solved = 0;
-    ctl.valid_points = 0;
-    ctl.final_cost = 0;
-    ctl.fail = 0;
+    if (a.ctl_in) {
+      ctl = *reinterpret_cast<const Ctl*>(a.ctl_io);
+    } else {
+      ctl.render = *a.state_pose;
+      // icp_track(..., initial) (depth_tracker.hpp:117): start from `initial` if given
+      ctl.c2w = pose_inverse(a.initial ? *a.initial : ctl.render);
+      ctl.iterations = 0;
+      ctl.any_solved = 0;
+      ctl.valid_points = 0;
+      ctl.final_cost = 0;
+      ctl.fail = 0;
+      ctl.trace_rows = 0;
+    }
   }
   __syncthreads();
   int buf = 0;
-  int trace_rows = 0;
-  for (int level = a.levels - 1; level >= 0 && !ctl.fail; --level) {
+  int trace_rows = ctl.trace_rows;
+  for (int level = a.level_hi; level >= a.level_lo && !ctl.fail; --level) {
     const IcpLevel lv = a.lv[level];
     const int npix = lv.w * lv.h;
     const bool rotation_only = level >= a.levels - a.rotation_only_levels;
@@ -638,41 +677,58 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
         s_red[warp][lane] = mine;  // lane l holds value index l
       }
       __syncthreads();
-      double* part = a.partials + ((size_t)buf * gridDim.x + blockIdx.x) * kAccStride;
-      if (tid < kAcc) {
-        double sum = 0;
-        for (int w = 0; w < nwarps; ++w) sum += s_red[w][tid];
-        part[tid] = sum;
-      }
-      long long t1 = timer ? clock64() : 0;
-      grid.sync();
-      long long t2 = timer ? clock64() : 0;
-      // every CTA sums all partials in the same fixed order
-      {
-        // thread t < 32 * ... : value index i = t & 31 over CTA subset t >> 5;
-        // all loads independent, then a fixed-order combine
+      long long t1 = 0, t2 = 0;
+      if (kCluster) {
+        cg::cluster_group cluster = cg::this_cluster();
+        if (tid < kAcc) {
+          double sum = 0;
+          for (int w = 0; w < nwarps; ++w) sum += s_red[w][tid];
+          s_part[buf][tid] = sum;
+        }
+        t1 = timer ? clock64() : 0;
+        cluster.sync();
+        t2 = timer ? clock64() : 0;
+        if (tid < kAcc) {  // every CTA sums the cluster's partials in rank order
+          double t = 0;
+          for (unsigned r = 0; r < cluster.num_blocks(); ++r) t += cluster.map_shared_rank(&s_part[buf][0], r)[tid];
+          s_tot[tid] = t;
+        }
+        buf ^= 1;
+      } else {
+        cg::grid_group grid = cg::this_grid();
+        double* part = a.partials + ((size_t)buf * gridDim.x + blockIdx.x) * kAccStride;
+        if (tid < kAcc) {
+          double sum = 0;
+          for (int w = 0; w < nwarps; ++w) sum += s_red[w][tid];
+          part[tid] = sum;
+        }
+        t1 = timer ? clock64() : 0;
+        grid.sync();
+        t2 = timer ? clock64() : 0;
+        // every CTA sums all partials in the same fixed order:
+        // thread (i = tid & 31, part = tid >> 5) over CTAs part, part + 8, ...
         const double* base = a.partials + (size_t)buf * gridDim.x * kAccStride;
-        const int i = tid & 31, part = tid >> 5;  // 8 groups of CTAs
+        const int i = tid & 31, grp = tid >> 5;
         double sum = 0;
         if (i < kAcc) {
           double vals[kMaxIcpGrid / 8];
 #pragma unroll
           for (int k = 0; k < kMaxIcpGrid / 8; ++k) {
-            const int b = part + 8 * k;
+            const int b = grp + 8 * k;
             vals[k] = b < (int)gridDim.x ? __ldcg(base + (size_t)b * kAccStride + i) : 0.0;
           }
 #pragma unroll
           for (int k = 0; k < kMaxIcpGrid / 8; ++k) sum += vals[k];
         }
-        s_red[part][i] = sum;
+        s_red[grp][i] = sum;
         __syncthreads();
         if (tid < kAcc) {
           double t = 0;
           for (int w = 0; w < nwarps; ++w) t += s_red[w][tid];
           s_tot[tid] = t;
         }
+        buf ^= 1;
       }
-      buf ^= 1;
       __syncthreads();
       long long t3 = timer ? clock64() : 0;
       if (tid == 0) {
@@ -746,7 +802,7 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
               ctl.valid_points = (int)count;
               double tn = 0;
               for (int i = 0; i < 6; ++i) tn = (i == 0) ? twist[0] * twist[0] : tn + twist[i] * twist[i];
-              if (sqrt(tn) < (double)a.conv_eps) {
+              if (tn < (double)a.conv_eps * (double)a.conv_eps) {  // |twist| < eps
                 ctl.accepted = ctl.c2w;
                 ctl.decision = 1;
               }
@@ -765,17 +821,26 @@ __global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs 
       if (ctl.decision != 0) break;
     }
   }
+  if (kCluster) cg::this_cluster().sync();  // no CTA leaves while others read its shared memory
   if (blockIdx.x == 0 && tid == 0) {
-    IcpResult res;
-    res.ok = (!ctl.fail && ctl.any_solved) ? 1 : 0;
-    res.iterations = res.ok ? ctl.iterations : 0;  // depth_tracker.hpp:208,234,237
-    res.valid_points = ctl.valid_points;
-    res.final_cost = ctl.final_cost;
-    res.trace_rows = trace_rows;
-    res.pose = res.ok ? pose_inverse(ctl.c2w) : (a.initial ? *a.initial : ctl.render);
-    if (res.ok && a.update_state) *a.state_pose = res.pose;  // pipeline_impl.hpp:83 — hold the pose on failure
-    *a.result = res;
+    ctl.trace_rows = trace_rows;
+    if (!a.is_last) {
+      *reinterpret_cast<Ctl*>(a.ctl_io) = ctl;
+    } else {
+      IcpResult res;
+      res.ok = (!ctl.fail && ctl.any_solved) ? 1 : 0;
+      res.iterations = res.ok ? ctl.iterations : 0;  // depth_tracker.hpp:208,234,237
+      res.valid_points = ctl.valid_points;
+      res.final_cost = ctl.final_cost;
+      res.trace_rows = trace_rows;
+      res.pose = res.ok ? pose_inverse(ctl.c2w) : (a.initial ? *a.initial : ctl.render);
+      if (res.ok && a.update_state) *a.state_pose = res.pose;  // pipeline_impl.hpp:83 — hold the pose on failure
+      *a.result = res;
+    }
   }
 }
+
+__global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp(IcpArgs a) { icp_body<false>(a); }
+__global__ void __launch_bounds__(kIcpThreads, VF_ICP_MIN_BLOCKS) k_icp_cluster(IcpArgs a) { icp_body<true>(a); }
 
 }  // namespace vf

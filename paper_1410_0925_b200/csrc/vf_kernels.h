@@ -53,6 +53,10 @@ struct IcpArgs {
   double* trace;
   int trace_cap;
   int max_slots;  // pixel slots per thread staged in shared memory
+  int level_hi, level_lo;  // levels run by this launch (coarse to fine)
+  void* ctl_io;            // controller state handed from the cluster to the grid kernel
+  int ctl_in;              // 1: start from *ctl_io instead of the pose
+  int is_last;             // 1: write the IcpResult (and the tracked pose)
 };
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);
@@ -95,6 +99,7 @@ __global__ void k_raycast(HashView hv, const uint32_t* vox, int vstride, const f
                           IntrD in, float vs, float mu, float4* points, float4* normals);
 __global__ void k_pyramid(const float* depth0, int w0, int h0, int levels, float* out);
 __global__ void k_icp(IcpArgs a);
+__global__ void k_icp_cluster(IcpArgs a);
 __global__ void k_synth(int n_spheres, const double* spheres, int n_planes, const double* planes, PoseD c2w,
                         IntrD in, double near_clip, double far_clip, float* depth, uint8_t* rgb);
 __global__ void k_fill_voxels(uint32_t* vox, size_t n_voxels, int words_per_voxel);
