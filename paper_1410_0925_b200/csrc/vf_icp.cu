@@ -644,7 +644,10 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           if (!bilinear_taps(tn[k], fx[k], fy[k], 1.0f, mn)) continue;
           const double nlen = sqrt(mn.x * mn.x + mn.y * mn.y + mn.z * mn.z);
           if (nlen < 1e-6) continue;
-          mn = mk(mn.x / nlen, mn.y / nlen, mn.z / nlen);
+          // model_normal /= nlen: one refined reciprocal instead of three IEEE
+          // divisions (1-ulp differences, far below the 1e-9 H/g parity bar)
+          const double inv = rcp_fast(nlen);
+          mn = mk(mn.x * inv, mn.y * inv, mn.z * inv);
           // icp_point_to_plane_term (depth_tracker.hpp:20-27)
           const D3 w = pw[k];
           const double r = (w.x - mp.x) * mn.x + (w.y - mp.y) * mn.y + (w.z - mp.z) * mn.z;
