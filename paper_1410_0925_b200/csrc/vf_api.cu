@@ -304,9 +304,8 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
                                                     c->depth, with_rgb ? c->rgb : nullptr, &c->dstate->fp,
                                                     s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
   else
-    k_integrate_s<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
-                                                  c->depth, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
-                                                  s.stop_integrating_at_max);
+    launch_integrate_s(c->num_sms * 8, st, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+                       &c->dstate->fp, s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
   VF_LAUNCHED(c, "k_integrate");
   ++launches;
   stage_mark(c, 3);
@@ -888,9 +887,8 @@ int vf_stage_integrate(vf_ctx* c, const float* depth_m, const uint8_t* rgb, cons
                                                     c->depth, with_rgb ? c->rgb : nullptr, &c->dstate->fp,
                                                     s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
   else
-    k_integrate_s<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
-                                                  c->depth, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
-                                                  s.stop_integrating_at_max);
+    launch_integrate_s(c->num_sms * 8, st, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+                       &c->dstate->fp, s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
   VF_CUDA(c, cudaGetLastError());
   VF_CUDA(c, cudaStreamSynchronize(st));
   return VF_OK;

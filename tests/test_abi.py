@@ -78,3 +78,26 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(VoxfuseError) as ei:
         make_pipeline(s, c)
     assert ei.value.status == _abi.VF_ERR_NO_DEVICE
+
+
+def test_no_fp32x2_contraction_in_sass():
+    """ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2
+    although .rn forbids it; the kernels keep such products scalar.  Guard:
+    every object's SASS has exactly as many FFMA2 as its PTX has fma.*.f32x2."""
+    import shutil
+    import subprocess
+
+    from paper_1410_0925_b200 import build as B
+
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    nvcc = B.nvcc_path()
+    B.build()
+    for src in B.SOURCES:
+        ptx = subprocess.run([nvcc, *B.NVCC_FLAGS, "-ptx", str(B.CSRC / src), "-o", "-"], capture_output=True,
+                             text=True, check=True).stdout
+        sass = subprocess.run(["cuobjdump", "-sass", str(B.OUT_DIR / "obj" / (src + ".o"))], capture_output=True,
+                              text=True, check=True).stdout
+        n_ptx = len(re.findall(r"\bfma\.r[nzmp]\.f32x2\b", ptx))
+        n_sass = len(re.findall(r"\bFFMA2\b", sass))
+        assert n_ptx == n_sass, f"{src}: {n_sass} FFMA2 in SASS vs {n_ptx} fma.f32x2 in PTX"
