@@ -299,13 +299,9 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     VF_CUDA(c, cudaEventRecord(c->ev_join, c->side));
   }
   const bool color = c->vsize == 8;
-  if (color)
-    k_integrate_rgb<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
-                                                    c->depth, with_rgb ? c->rgb : nullptr, &c->dstate->fp,
-                                                    s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
-  else
-    launch_integrate_s(c->num_sms * 8, st, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
-                       &c->dstate->fp, s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
+  launch_integrate(c->num_sms * 8, st, color, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+                   with_rgb ? c->rgb : nullptr, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
+                   s.stop_integrating_at_max);
   VF_LAUNCHED(c, "k_integrate");
   ++launches;
   stage_mark(c, 3);
@@ -882,13 +878,9 @@ int vf_stage_integrate(vf_ctx* c, const float* depth_m, const uint8_t* rgb, cons
   if (with_rgb && upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, false)) return VF_ERR_CUDA;
   if (int rc = set_pose_dev(c, pose)) return rc;
   k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
-  if (c->vsize == 8)
-    k_integrate_rgb<<<c->num_sms * 8, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, c->voxels,
-                                                    c->depth, with_rgb ? c->rgb : nullptr, &c->dstate->fp,
-                                                    s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
-  else
-    launch_integrate_s(c->num_sms * 8, st, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
-                       &c->dstate->fp, s.voxel_size, s.mu, s.max_weight, s.stop_integrating_at_max);
+  launch_integrate(c->num_sms * 8, st, c->vsize == 8, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+                   with_rgb ? c->rgb : nullptr, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
+                   s.stop_integrating_at_max);
   VF_CUDA(c, cudaGetLastError());
   VF_CUDA(c, cudaStreamSynchronize(st));
   return VF_OK;
