@@ -146,6 +146,25 @@ int vf_frame_count(const vf_ctx* ctx);
 /* World-space point / normal maps (TrackingState::points/normals): width*height float4 each. */
 int vf_get_maps(vf_ctx* ctx, float* points, float* normals);
 int vf_set_maps(vf_ctx* ctx, const float* points, const float* normals, const double render_pose[12]);
+/* Colour-tracker surface list (TrackingState::surface_points / surface_colors,
+ * tracking_state.hpp:30-31), filled at the end of every VoxelSRgb frame by
+ * forward_project_points (raycast.hpp:495-509, stride 4, pipeline_impl.hpp:218-221):
+ * n x float3 world points and n x float3 colours in [0,1], raster order.
+ * Returns n (points/colors may be NULL to query it); cap is in points. */
+long vf_get_surface_points(vf_ctx* ctx, float* points, float* colors, long cap);
+/* forward_project_points over the current maps and volume (stage entry point). */
+int vf_stage_forward_project(vf_ctx* ctx);
+/* IPipeline::get_image (pipeline.hpp:74, pipeline_impl.hpp:125-137) into a
+ * width*height*3 u8 host buffer: DisplayMode (pipeline.hpp:60) raycast ->
+ * render_image (raycast.hpp:466-490) in colour for VoxelSRgb, shaded grey
+ * otherwise; VF_DISPLAY_RAYCAST_GREY forces RenderMode::shaded_grey. */
+enum vf_display_mode {
+  VF_DISPLAY_RAYCAST = 0,
+  VF_DISPLAY_DEPTH_COLOURIZED = 1,
+  VF_DISPLAY_RGB_PASSTHROUGH = 2,
+  VF_DISPLAY_RAYCAST_GREY = 3
+};
+int vf_render_image(vf_ctx* ctx, int mode, uint8_t* out);
 /* FNV-1a volume digest (IPipeline::volume_digest, pipeline_impl.hpp:144-164). */
 int vf_volume_digest(vf_ctx* ctx, uint64_t* out);
 

@@ -40,7 +40,7 @@ struct vfa_config {  // same layout as vfr_config (oracle/ref_driver.cpp)
 // visible blocks, allocated; final FNV digest and maps.
 int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, const std::uint8_t* rgb,
             double* poses, int* iters, int* ok, int* visible, std::uint64_t* digest, float* points,
-            float* normals) {
+            float* normals, std::uint8_t* image, std::uint8_t* image_depth) {
   try {
     EngineSettings s;
     s.backend = VolumeBackend::hash;
@@ -95,6 +95,14 @@ int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, c
     const TrackingState& ts = p->tracking_state();
     std::memcpy(points, ts.points.pixels().data(), sizeof(float) * 4 * npix);
     std::memcpy(normals, ts.normals.pixels().data(), sizeof(float) * 4 * npix);
+    // get_image (pipeline_impl.hpp:125-137): raycast render and colourised depth
+    const Image2D<Vec3u8> img = p->get_image(DisplayMode::raycast);
+    const Image2D<Vec3u8> dimg = p->get_image(DisplayMode::depth_colourized);
+    for (std::size_t i = 0; i < npix; ++i)
+      for (int ch = 0; ch < 3; ++ch) {
+        if (image) image[3 * i + ch] = img.empty() ? 0 : img.pixels()[i](ch);
+        if (image_depth) image_depth[3 * i + ch] = dimg.empty() ? 0 : dimg.pixels()[i](ch);
+      }
     return p->frame_count();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "vfa_run: %s\n", e.what());

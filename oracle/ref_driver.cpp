@@ -123,7 +123,14 @@ struct CtxBase {
   virtual std::uint64_t digest() const = 0;
   virtual long allocated_blocks() const = 0;
   virtual long export_ranges(float* out) const { (void)out; return -1; }
+  // get_image (pipeline_impl.hpp:125-137) / render_image (raycast.hpp:466-490)
+  virtual int image(int mode, std::uint8_t* out) const = 0;
 };
+
+void copy_image(const Image2D<Vec3u8>& img, std::uint8_t* out) {
+  for (std::size_t i = 0; i < img.size(); ++i)
+    for (int c = 0; c < 3; ++c) out[3 * i + c] = img.pixels()[i](c);
+}
 
 Image2D<float> depth_image(const float* d, int w, int h) {
   Image2D<float> img(w, h, 0.0f);
@@ -192,6 +199,20 @@ struct PipelineCtx final : CtxBase {
   }
   std::uint64_t digest() const override { return p.volume_digest(); }
   long allocated_blocks() const override { return p.volume().allocated_block_count(); }
+  int image(int mode, std::uint8_t* out) const override {
+    // mode: DisplayMode (pipeline.hpp:60); 3 = render_image in shaded grey
+    Image2D<Vec3u8> img;
+    if (mode == 3) {
+      const TrackingState& s = p.tracking_state();
+      if (!s.maps_valid) return -1;
+      img = render_image(p.volume(), s.points, s.normals, s.pose, p.settings().scene, RenderMode::shaded_grey);
+    } else {
+      img = p.get_image(static_cast<DisplayMode>(mode));
+    }
+    if (img.empty()) return -1;
+    copy_image(img, out);
+    return 0;
+  }
 };
 
 // Known-pose mode: stage templates in pipeline order (pipeline_impl.hpp:88-117).
@@ -230,6 +251,9 @@ struct StagesCtx final : CtxBase {
                                    s.near_clip, s.far_clip);
     render_maps(volume, range, st.pose, calib.depth, s.scene, st.points, st.normals);
     st.maps_valid = true;
+    if constexpr (TVoxel::has_color) {  // pipeline_impl.hpp:218-221
+      forward_project_points(volume, st.points, s.scene, 4, st.surface_points, st.surface_colors);
+    }
     const double ms_ray = detail::ms_since(t0);
     if (out) {
       out->frame = frame;
@@ -259,6 +283,12 @@ struct StagesCtx final : CtxBase {
   }
   std::uint64_t digest() const override { return 0; }
   long allocated_blocks() const override { return volume.allocated_block_count(); }
+  int image(int mode, std::uint8_t* out) const override {
+    if (!st.maps_valid || (mode != 0 && mode != 3)) return -1;
+    const RenderMode rm = (mode == 0 && TVoxel::has_color) ? RenderMode::color : RenderMode::shaded_grey;
+    copy_image(render_image(volume, st.points, st.normals, st.pose, s.scene, rm), out);
+    return 0;
+  }
   long export_ranges(float* out) const override {
     const long n = static_cast<long>(range.fragments_x()) * range.fragments_y();
     if (out) {
@@ -332,6 +362,17 @@ long vfr_export_entries(void* ctx, void* out) { return static_cast<CtxBase*>(ctx
 long vfr_export_voxels(void* ctx, void* out) { return static_cast<CtxBase*>(ctx)->export_voxels(out); }
 long vfr_visible_list(void* ctx, int* out) { return static_cast<CtxBase*>(ctx)->visible_list(out); }
 long vfr_export_ranges(void* ctx, float* out) { return static_cast<CtxBase*>(ctx)->export_ranges(out); }
+long vfr_surface_points(void* ctx, float* points, float* colors) {
+  const TrackingState& s = static_cast<CtxBase*>(ctx)->state();
+  const long n = static_cast<long>(s.surface_points.size());
+  for (long i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) {
+      if (points) points[3 * i + c] = s.surface_points[static_cast<std::size_t>(i)](c);
+      if (colors) colors[3 * i + c] = s.surface_colors[static_cast<std::size_t>(i)](c);
+    }
+  return n;
+}
+int vfr_image(void* ctx, int mode, std::uint8_t* out) { return static_cast<CtxBase*>(ctx)->image(mode, out); }
 std::uint64_t vfr_digest(void* ctx) { return static_cast<CtxBase*>(ctx)->digest(); }
 long vfr_allocated_blocks(void* ctx) { return static_cast<CtxBase*>(ctx)->allocated_blocks(); }
 

@@ -419,6 +419,10 @@ struct vfo_ctx {
   /* ICP trace */
   double* trace;
   long trace_rows, trace_cap;
+  /* TrackingState::surface_points / surface_colors (tracking_state.hpp:30-31) */
+  f3* surf_points;
+  f3* surf_colors;
+  long n_surface;
 };
 
 static uint8_t* vox_bytes(vfo_ctx* c, long slot, int lin) {
@@ -976,6 +980,87 @@ static void render_maps(vfo_ctx* c, const pose_t* w2c) {
     }
 }
 
+/* sample_voxel_color (raycast.hpp:441-464) */
+static f3 sample_voxel_color(vfo_ctx* c, f3 p) {
+  if (!c->has_color) return f3m(0.0f, 0.0f, 0.0f);
+  const f3 q = f3m(p.x - 0.5f, p.y - 0.5f, p.z - 0.5f);
+  const i3 base = {(int)floorf(q.x), (int)floorf(q.y), (int)floorf(q.z)};
+  const f3 f = f3m(q.x - (float)base.x, q.y - (float)base.y, q.z - (float)base.z);
+  f3 sum = f3m(0.0f, 0.0f, 0.0f);
+  float wsum = 0.0f;
+  for (int corner = 0; corner < 8; ++corner) {
+    const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+    const i3 v = {base.x + dx, base.y + dy, base.z + dz};
+    const uint8_t* vox = volume_read(c, v);
+    if (!vox || vox[6] == 0) continue;
+    const float w = (dx ? f.x : 1 - f.x) * (dy ? f.y : 1 - f.y) * (dz ? f.z : 1 - f.z);
+    sum = f3m(sum.x + (float)vox[3] * w, sum.y + (float)vox[4] * w, sum.z + (float)vox[5] * w);
+    wsum += w;
+  }
+  return wsum > 0.0f ? f3m(sum.x / wsum, sum.y / wsum, sum.z / wsum) : f3m(0.0f, 0.0f, 0.0f);
+}
+
+/* forward_project_points (raycast.hpp:495-509) */
+static void forward_project_points(vfo_ctx* c, int stride) {
+  const intr_t* in = &c->depth_intr;
+  const float vs = c->cfg.voxel_size;
+  c->n_surface = 0;
+  for (int y = 0; y < in->height; y += stride)
+    for (int x = 0; x < in->width; x += stride) {
+      const f4 p = c->points[(size_t)y * in->width + x];
+      if (p.w == 0.0f) continue;
+      const f3 col = sample_voxel_color(c, f3m(p.x / vs, p.y / vs, p.z / vs));
+      c->surf_points[c->n_surface] = f3m(p.x, p.y, p.z);
+      c->surf_colors[c->n_surface] = f3m(col.x / 255.0f, col.y / 255.0f, col.z / 255.0f);
+      ++c->n_surface;
+    }
+}
+
+static float clampf(float v, float lo, float hi) { return v < lo ? lo : (hi < v ? hi : v); } /* std::clamp */
+
+/* render_image (raycast.hpp:466-490): color 0 shaded grey, 1 colour */
+static void render_image(vfo_ctx* c, int color, uint8_t* out) {
+  const intr_t* in = &c->depth_intr;
+  const float ax = (float)c->pose.r[6], ay = (float)c->pose.r[7], az = (float)c->pose.r[8];
+  const float vs = c->cfg.voxel_size;
+  memset(out, 0, (size_t)in->width * in->height * 3);
+  for (int y = 0; y < in->height; ++y)
+    for (int x = 0; x < in->width; ++x) {
+      const size_t i = (size_t)y * in->width + x;
+      const f4 p = c->points[i];
+      if (p.w == 0.0f) continue;
+      const f4 n = c->normals[i];
+      const float shade = fabsf(n.x * ax + n.y * ay + n.z * az);
+      if (!color || !c->has_color) {
+        const uint8_t g = (uint8_t)(clampf(shade, 0.0f, 1.0f) * 255.0f);
+        out[3 * i] = out[3 * i + 1] = out[3 * i + 2] = g;
+      } else {
+        const f3 s = sample_voxel_color(c, f3m(p.x / vs, p.y / vs, p.z / vs));
+        const f3 col = f3m(s.x * shade, s.y * shade, s.z * shade);
+        out[3 * i + 0] = (uint8_t)clampf(col.x, 0.0f, 255.0f);
+        out[3 * i + 1] = (uint8_t)clampf(col.y, 0.0f, 255.0f);
+        out[3 * i + 2] = (uint8_t)clampf(col.z, 0.0f, 255.0f);
+      }
+    }
+}
+
+/* Pipeline::colourize_depth (pipeline_impl.hpp:225-239) */
+void vfo_colourize_depth(const float* depth, int w, int h, uint8_t* out) {
+  const size_t n = (size_t)w * h;
+  float dmax = 0.0f;
+  for (size_t i = 0; i < n; ++i) dmax = (dmax < depth[i]) ? depth[i] : dmax; /* std::max */
+  memset(out, 0, n * 3);
+  if (dmax <= 0.0f) return;
+  for (size_t i = 0; i < n; ++i) {
+    const float d = depth[i];
+    if (d <= 0.0f) continue;
+    const float t = d / dmax;
+    out[3 * i + 0] = (uint8_t)(255 * (1.0f - t));
+    out[3 * i + 1] = (uint8_t)(255 * (1.0f - fabsf(2 * t - 1)));
+    out[3 * i + 2] = (uint8_t)(255 * t);
+  }
+}
+
 /* ------------------------------------------------------------------------ */
 /* depth pyramid (engine/pyramid.hpp)                                        */
 /* ------------------------------------------------------------------------ */
@@ -1276,6 +1361,8 @@ vfo_ctx* vfo_create(const vfo_config* cfg, int tracking) {
   c->ranges = (float*)calloc((size_t)c->frag_w * c->frag_h * 2, sizeof(float));
   c->points = (f4*)calloc((size_t)cfg->width * cfg->height, sizeof(f4));
   c->normals = (f4*)calloc((size_t)cfg->width * cfg->height, sizeof(f4));
+  c->surf_points = (f3*)calloc((size_t)((cfg->width + 3) / 4) * ((cfg->height + 3) / 4), sizeof(f3));
+  c->surf_colors = (f3*)calloc((size_t)((cfg->width + 3) / 4) * ((cfg->height + 3) / 4), sizeof(f3));
   c->pose = pose_identity();
   c->render_pose = pose_identity();
   return c;
@@ -1296,6 +1383,8 @@ void vfo_destroy(vfo_ctx* c) {
   free(c->points);
   free(c->normals);
   free(c->trace);
+  free(c->surf_points);
+  free(c->surf_colors);
   free(c);
 }
 
@@ -1325,6 +1414,21 @@ int vfo_stage_raycast(vfo_ctx* c, const double* pose) {
   c->maps_valid = 1;
   c->render_pose = p;
   c->pose = p;
+  if (c->has_color) forward_project_points(c, 4); /* pipeline_impl.hpp:218-221 */
+  return 0;
+}
+int vfo_stage_forward_project(vfo_ctx* c) {
+  forward_project_points(c, 4);
+  return 0;
+}
+long vfo_surface_points(const vfo_ctx* c, float* points, float* colors) {
+  if (points) memcpy(points, c->surf_points, sizeof(f3) * (size_t)c->n_surface);
+  if (colors) memcpy(colors, c->surf_colors, sizeof(f3) * (size_t)c->n_surface);
+  return c->n_surface;
+}
+int vfo_render_image(vfo_ctx* c, int color, uint8_t* out) {
+  if (!c->maps_valid) return -1;
+  render_image(c, color, out);
   return 0;
 }
 
@@ -1401,6 +1505,7 @@ int vfo_process(vfo_ctx* c, const float* depth, const uint8_t* rgb, const double
   render_maps(c, &c->pose);
   c->maps_valid = 1;
   c->render_pose = c->pose;
+  if (c->has_color) forward_project_points(c, 4); /* pipeline_impl.hpp:218-221 */
   s.ms_raycast = now_ms() - t0;
   pose_to(&c->pose, s.pose);
   s.ms_total = now_ms() - t_start;

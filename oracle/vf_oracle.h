@@ -86,6 +86,13 @@ long vfo_raycast_counters(long* out);
 /* last ICP solve trace: rows of 48 doubles (level, iter, 21 H, 6 g, cost, count,
  * rotation_only, evaluation camera-to-world pose (12), 4 unused) */
 long vfo_icp_trace(const vfo_ctx* c, double* out, long max_rows);
+/* raycast epilogues (raycast.hpp:441-509): surface list of the last render
+ * (n x float3 points, n x float3 colours; returns n), forward_project_points
+ * over the current maps, render_image (color 0: shaded grey, 1: colour). */
+long vfo_surface_points(const vfo_ctx* c, float* points, float* colors);
+int vfo_stage_forward_project(vfo_ctx* c);
+int vfo_render_image(vfo_ctx* c, int color, uint8_t* out);
+void vfo_colourize_depth(const float* depth, int w, int h, uint8_t* out);
 
 /* Free functions. */
 uint32_t vfo_hash_block_pos(int x, int y, int z, uint32_t mask);

@@ -152,6 +152,8 @@ class _Lib:
             getattr(L, p + fn).argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p] + [C.c_double] * 4 + [
                 C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p]
         getattr(L, p + "depth_pyramid").argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        getattr(L, p + "surface_points").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        getattr(L, p + "surface_points").restype = C.c_long
 
 
 class OracleLib(_Lib):
@@ -176,6 +178,10 @@ class OracleLib(_Lib):
         L.vfo_icp_trace.restype = C.c_long
         L.vfo_hash_block_pos.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint32]
         L.vfo_hash_block_pos.restype = C.c_uint32
+        L.vfo_stage_forward_project.argtypes = [C.c_void_p]
+        L.vfo_render_image.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.vfo_render_image.restype = C.c_int
+        L.vfo_colourize_depth.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
 
 
 class RefLib(_Lib):
@@ -189,6 +195,8 @@ class RefLib(_Lib):
         L.vfr_icp_track.argtypes = [C.POINTER(Config)] + [C.c_void_p] * 5 + [
             C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.vfr_icp_track.restype = C.c_int
+        L.vfr_image.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.vfr_image.restype = C.c_int
         assert L.vfr_sizeof_config() == C.sizeof(Config), "vfr_config layout mismatch"
         assert L.vfr_sizeof_stats() == C.sizeof(Stats), "vfr_stats layout mismatch"
 
@@ -291,6 +299,25 @@ class Volume:
     def digest(self) -> int:
         return int(self._f("digest")(self.h))
 
+    def surface_points(self):
+        """TrackingState::surface_points / surface_colors (n x 3 float32 each)."""
+        n = self._f("surface_points")(self.h, None, None)
+        pts = np.zeros((n, 3), np.float32)
+        cols = np.zeros((n, 3), np.float32)
+        if n:
+            self._f("surface_points")(self.h, _p(pts, C.c_float), _p(cols, C.c_float))
+        return pts, cols
+
+    def image(self, mode: int = 0) -> np.ndarray | None:
+        """render_image of the current maps: mode 0 raycast (colour for VoxelSRgb),
+        3 shaded grey (vf_display_mode numbering)."""
+        out = np.zeros((self.height, self.width, 3), np.uint8)
+        if self.p == "vfo_":
+            rc = self.L.lib.vfo_render_image(self.h, 1 if mode == 0 else 0, out.ctypes.data_as(C.c_void_p))
+        else:
+            rc = self.L.lib.vfr_image(self.h, mode, out.ctypes.data_as(C.c_void_p))
+        return out if rc == 0 else None
+
     def allocated_blocks(self) -> int:
         return int(self._f("allocated_blocks")(self.h))
 
@@ -316,6 +343,15 @@ def render_rgb(lib: _Lib, cfg, pose: np.ndarray, spheres, planes, near=0.05, far
     getattr(lib.lib, lib.prefix + "render_rgb")(len(sp), _p(sp, C.c_double), len(pl), _p(pl, C.c_double),
                                                  _p(pose, C.c_double), fx, fy, cx, cy, w, h, near, far,
                                                  _p(out, C.c_uint8))
+    return out
+
+
+def colourize_depth(depth: np.ndarray) -> np.ndarray:
+    """Pipeline::colourize_depth (pipeline_impl.hpp:225-239), oracle restatement."""
+    depth = np.ascontiguousarray(depth, dtype=np.float32)
+    h, w = depth.shape
+    out = np.zeros((h, w, 3), np.uint8)
+    oracle_lib().lib.vfo_colourize_depth(depth.ctypes.data_as(C.c_void_p), w, h, out.ctypes.data_as(C.c_void_p))
     return out
 
 

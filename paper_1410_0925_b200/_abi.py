@@ -32,6 +32,7 @@ EXPORTS = [
     "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
     "vf_process_frame", "vf_process_frame_device", "vf_synchronize", "vf_read_stats",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
+    "vf_get_surface_points", "vf_stage_forward_project", "vf_render_image",
     "vf_entry_count", "vf_voxel_bytes", "vf_export_entries", "vf_export_voxels", "vf_export_free_stacks",
     "vf_import_state", "vf_export_visible_list", "vf_export_ranges",
     "vf_stage_allocate", "vf_stage_integrate", "vf_stage_raycast", "vf_stage_icp", "vf_icp_trace",
@@ -150,6 +151,9 @@ def load() -> C.CDLL:
         "vf_get_maps": (C.c_int, [vp, vp, vp]),
         "vf_set_maps": (C.c_int, [vp, vp, vp, dp]),
         "vf_volume_digest": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+        "vf_get_surface_points": (C.c_long, [vp, vp, vp, C.c_long]),
+        "vf_stage_forward_project": (C.c_int, [vp]),
+        "vf_render_image": (C.c_int, [vp, C.c_int, vp]),
         "vf_entry_count": (C.c_long, [vp]),
         "vf_voxel_bytes": (C.c_long, [vp]),
         "vf_export_entries": (C.c_int, [vp, vp]),

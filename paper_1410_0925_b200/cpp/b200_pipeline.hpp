@@ -140,7 +140,6 @@ class B200Pipeline final : public voxfuse::IPipeline {
       rgb_ptr = reinterpret_cast<const std::uint8_t*>(rgb->pixels().data());
     vf_frame_stats st;
     detail::check(vf_process_frame(ctx_, depth_m.pixels().data(), rgb_ptr, &st), "vf_process_frame", ctx_);
-    last_depth_ = depth_m;
     if (rgb) last_rgb_ = *rgb;
     pose_ = detail::pose_from_array(st.pose);
     maps_stale_ = true;
@@ -164,45 +163,19 @@ class B200Pipeline final : public voxfuse::IPipeline {
     return process_frame(rgb, voxfuse::disparity_image_to_depth(disparity, calib_, settings_.max_depth));
   }
 
+  // IPipeline::get_image (pipeline_impl.hpp:125-137): rendered on the GPU
+  // (render_image / colourize_depth, raycast.hpp:466-490) and downloaded.
   voxfuse::Image2D<voxfuse::Vec3u8> get_image(voxfuse::DisplayMode mode) const override {
     using voxfuse::Image2D;
     using voxfuse::Vec3u8;
-    switch (mode) {
-      case voxfuse::DisplayMode::rgb_passthrough:
-        return last_rgb_;
-      case voxfuse::DisplayMode::depth_colourized: {
-        float dmax = 0.0f;
-        for (float d : last_depth_.pixels()) dmax = std::max(dmax, d);
-        Image2D<Vec3u8> out(last_depth_.width(), last_depth_.height(), Vec3u8::Zero());
-        if (dmax <= 0.0f) return out;
-        for (std::size_t i = 0; i < last_depth_.size(); ++i) {
-          const float d = last_depth_.pixels()[i];
-          if (d <= 0.0f) continue;
-          const float t = d / dmax;
-          out.pixels()[i] = Vec3u8(static_cast<std::uint8_t>(255 * (1.0f - t)),
-                                   static_cast<std::uint8_t>(255 * (1.0f - std::abs(2 * t - 1))),
-                                   static_cast<std::uint8_t>(255 * t));
-        }
-        return out;
-      }
-      case voxfuse::DisplayMode::raycast:
-      default: {
-        // shaded-grey rendering of the GPU maps (raycast.hpp:466-490)
-        const voxfuse::TrackingState& st = tracking_state();
-        if (!st.maps_valid) return Image2D<Vec3u8>();
-        Image2D<Vec3u8> out(st.points.width(), st.points.height(), Vec3u8::Zero());
-        const voxfuse::Vec3f axis = st.pose.rotation().row(2).cast<float>();
-        for (int y = 0; y < st.points.height(); ++y)
-          for (int x = 0; x < st.points.width(); ++x) {
-            if (st.points.at(x, y).w() == 0.0f) continue;
-            const voxfuse::Vec3f n = st.normals.at(x, y).head<3>();
-            const float shade = std::abs(n.dot(axis));
-            const auto g = static_cast<std::uint8_t>(std::clamp(shade, 0.0f, 1.0f) * 255.0f);
-            out.at(x, y) = Vec3u8(g, g, g);
-          }
-        return out;
-      }
-    }
+    if (mode == voxfuse::DisplayMode::rgb_passthrough) return last_rgb_;
+    const int vm = mode == voxfuse::DisplayMode::depth_colourized ? VF_DISPLAY_DEPTH_COLOURIZED : VF_DISPLAY_RAYCAST;
+    Image2D<Vec3u8> out(calib_.depth.width, calib_.depth.height, Vec3u8::Zero());
+    static_assert(sizeof(Vec3u8) == 3, "Vec3u8 must be packed RGB");
+    const int rc = vf_render_image(ctx_, vm, reinterpret_cast<std::uint8_t*>(out.pixels().data()));
+    if (rc == VF_ERR_STATE) return Image2D<Vec3u8>();  // nothing rendered yet (reference: empty image)
+    detail::check(rc, "vf_render_image", ctx_);
+    return out;
   }
 
   // TrackingState: the world-space maps are downloaded on demand.
@@ -216,6 +189,20 @@ class B200Pipeline final : public voxfuse::IPipeline {
                                  reinterpret_cast<float*>(state_.normals.pixels().data()));
       state_.maps_valid = rc == VF_OK;
       state_.pose = pose_;
+      // surface list for the colour tracker (forward_project_points, raycast.hpp:495-509)
+      state_.surface_points.clear();
+      state_.surface_colors.clear();
+      const long n = vf_get_surface_points(ctx_, nullptr, nullptr, 0);
+      if (n > 0) {
+        static_assert(sizeof(voxfuse::Vec3f) == 12, "Vec3f must be 3 packed floats");
+        state_.surface_points.resize(static_cast<std::size_t>(n));
+        state_.surface_colors.resize(static_cast<std::size_t>(n));
+        detail::check((int)vf_get_surface_points(ctx_, reinterpret_cast<float*>(state_.surface_points.data()),
+                                                 reinterpret_cast<float*>(state_.surface_colors.data()), n) < 0
+                          ? VF_ERR_CUDA
+                          : VF_OK,
+                      "vf_get_surface_points", ctx_);
+      }
       maps_stale_ = false;
     }
     return state_;
@@ -236,7 +223,6 @@ class B200Pipeline final : public voxfuse::IPipeline {
   voxfuse::Calibration calib_;
   vf_ctx* ctx_ = nullptr;
   voxfuse::Pose pose_;
-  voxfuse::Image2D<float> last_depth_;
   voxfuse::Image2D<voxfuse::Vec3u8> last_rgb_;
   mutable voxfuse::TrackingState state_;
   mutable bool maps_stale_ = true;

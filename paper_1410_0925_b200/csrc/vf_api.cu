@@ -116,6 +116,13 @@ struct vf_ctx {
   void* nccl_comm = nullptr;
   unsigned long long* shard_keys = nullptr;
   int icp_grid = 0;
+  // colour-tracker surface list (forward_project_points, raycast.hpp:495-509)
+  float* surf_points = nullptr;
+  float* surf_colors = nullptr;
+  unsigned long long* surf_scan = nullptr;  // tile ticket + look-back flags
+  int surf_cap = 0, surf_tiles = 0;
+  uint8_t* image = nullptr;  // get_image output (w*h*3) + depth-max word
+  int* image_dmax = nullptr;
 
   // host state
   DevState* hstate = nullptr;  // pinned
@@ -249,6 +256,17 @@ bool debug_sync() {
     }                                                                                               \
   } while (0)
 
+// forward_project_points (raycast.hpp:495-509) over the current maps
+int launch_forward_project(vf_ctx* c) {
+  cudaStream_t st = c->stream;
+  VF_CUDA(c, cudaMemsetAsync(c->surf_scan, 0, sizeof(unsigned long long) * (1 + (size_t)c->surf_tiles), st));
+  k_forward_project<<<c->surf_tiles, kFpTileItems, 0, st>>>(
+      hash_view(c), c->vsize == 8 ? reinterpret_cast<const uint32_t*>(c->voxels) : nullptr, c->points, c->din,
+      kSurfaceStride, c->s.voxel_size, c->surf_scan, c->surf_points, c->surf_colors, &c->dstate->ctr);
+  VF_CUDA(c, cudaGetLastError());
+  return VF_OK;
+}
+
 // The frame, as stream work.  With track=true the ICP runs first against the
 // maps of the previous frame; the updated pose stays on the device.
 int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
@@ -325,6 +343,12 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     }
     launches += 2;
   }
+  if (c->vsize == 8) {
+    // forward_project_points for the colour tracker (pipeline_impl.hpp:218-221)
+    if (int rc = launch_forward_project(c)) return rc;
+    VF_LAUNCHED(c, "k_forward_project");
+    ++launches;
+  }
   stage_mark(c, 4);
   c->launches_last = launches;
   VF_CUDA(c, cudaGetLastError());
@@ -396,6 +420,7 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
   if (with_rgb) {
     if (int rc = upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, device_inputs)) return rc;
   }
+  c->rgb_valid = with_rgb;
   const bool track = c->s.tracking && c->frame > 0 && c->maps_valid;
   const int frame_index = c->frame;
   if (stats) VF_CUDA(c, cudaEventRecord(c->ev_frame0, c->stream));
@@ -436,7 +461,8 @@ void free_all(vf_ctx* c) {
       if (g) cudaGraphExecDestroy(g);
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list, c->req_marked,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
-                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl};
+                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
+                  c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -605,6 +631,9 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     for (int y = 0; y < in.height; ++y) utab_h.push_back((y - in.cy) / in.fy);
   }
   c->alloc_cap = c->entry_count;
+  c->surf_cap = ((c->din.width + kSurfaceStride - 1) / kSurfaceStride) *
+                ((c->din.height + kSurfaceStride - 1) / kSurfaceStride);
+  c->surf_tiles = (c->surf_cap + kFpTileItems - 1) / kFpTileItems;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_icp, kIcpThreads, 0);
   if (occ < 1) occ = 1;
@@ -672,7 +701,11 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->partials, sizeof(double) * 2 * 32 * (size_t)c->icp_grid)) ||
       (rc = dalloc(c, &c->trace, sizeof(double) * kTraceRow * kTraceCap)) ||
       (rc = dalloc(c, &c->shard_keys, sizeof(unsigned long long) * (size_t)c->npix)) ||
-      (rc = dalloc(c, &c->icp_ctl, 1024))) {
+      (rc = dalloc(c, &c->icp_ctl, 1024)) ||
+      (rc = dalloc(c, &c->surf_points, sizeof(float) * 3 * (size_t)c->surf_cap)) ||
+      (rc = dalloc(c, &c->surf_colors, sizeof(float) * 3 * (size_t)c->surf_cap)) ||
+      (rc = dalloc(c, &c->surf_scan, sizeof(unsigned long long) * (1 + (size_t)c->surf_tiles))) ||
+      (rc = dalloc(c, &c->image, 3 * (size_t)c->npix)) || (rc = dalloc(c, &c->image_dmax, sizeof(int)))) {
     free_all(c);
     delete c;
     return rc;
@@ -765,6 +798,58 @@ int vf_set_maps(vf_ctx* c, const float* points, const float* normals, const doub
   if (int rc = set_pose_dev(c, render_pose)) return rc;
   VF_CUDA(c, cudaStreamSynchronize(c->stream));
   c->maps_valid = true;
+  return VF_OK;
+}
+
+int vf_stage_forward_project(vf_ctx* c) {
+  if (!c) return VF_ERR_INVALID;
+  if (!c->maps_valid) return VF_ERR_STATE;
+  if (int rc = launch_forward_project(c)) return rc;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return VF_OK;
+}
+
+long vf_get_surface_points(vf_ctx* c, float* points, float* colors, long cap) {
+  if (!c) return VF_ERR_INVALID;
+  if (int rc = read_state(c)) return rc;
+  const long n = c->hstate->ctr.surface_count;
+  if (n > 0 && (points || colors)) {
+    if (cap < n) return VF_ERR_INVALID;
+    if (points) VF_CUDA(c, cudaMemcpy(points, c->surf_points, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost));
+    if (colors) VF_CUDA(c, cudaMemcpy(colors, c->surf_colors, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost));
+  }
+  return n;
+}
+
+int vf_render_image(vf_ctx* c, int mode, uint8_t* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  cudaStream_t st = c->stream;
+  const size_t bytes = 3 * (size_t)c->npix;
+  switch (mode) {
+    case VF_DISPLAY_RGB_PASSTHROUGH:
+      if (!c->rgb_valid) return VF_ERR_STATE;
+      VF_CUDA(c, cudaStreamSynchronize(st));
+      VF_CUDA(c, cudaMemcpy(out, c->rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, cudaMemcpyDeviceToHost));
+      return VF_OK;
+    case VF_DISPLAY_DEPTH_COLOURIZED:
+      if (c->frame == 0) return VF_ERR_STATE;
+      VF_CUDA(c, cudaMemsetAsync(c->image_dmax, 0, sizeof(int), st));
+      k_depth_max<<<c->num_sms, 256, 0, st>>>(c->depth, c->npix, c->image_dmax);
+      k_colourize_depth<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->npix, c->image_dmax, c->image);
+      break;
+    case VF_DISPLAY_RAYCAST:
+    case VF_DISPLAY_RAYCAST_GREY:
+      if (!c->maps_valid) return VF_ERR_STATE;
+      k_render_image<<<(c->npix + 255) / 256, 256, 0, st>>>(
+          hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels), c->points, c->normals, &c->dstate->pose, c->din,
+          c->s.voxel_size, (mode == VF_DISPLAY_RAYCAST && c->vsize == 8) ? 1 : 0, c->image);
+      break;
+    default:
+      return VF_ERR_INVALID;
+  }
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaMemcpyAsync(out, c->image, bytes, cudaMemcpyDeviceToHost, st));
+  VF_CUDA(c, cudaStreamSynchronize(st));
   return VF_OK;
 }
 

@@ -113,6 +113,17 @@ __global__ void k_reset_visible(Counters* ctr);
 __global__ void k_divtest_const(float b, uint32_t lo_bits, uint32_t n_bits, unsigned long long* mism);
 __global__ void k_divtest_rand(float amax, float bmin, float bmax, unsigned long long n, unsigned long long* mism);
 
+// raycast epilogues (vf_render.cu)
+__global__ void k_forward_project(HashView hv, const uint32_t* vox, const float4* points, IntrD in, int stride,
+                                  float vs, unsigned long long* scan, float* out_points, float* out_colors,
+                                  Counters* ctr);
+__global__ void k_render_image(HashView hv, const uint32_t* vox, const float4* points, const float4* normals,
+                               const PoseD* w2c, IntrD in, float vs, int color, uint8_t* out);
+__global__ void k_depth_max(const float* depth, int n, int* dmax_bits);
+__global__ void k_colourize_depth(const float* depth, int n, const int* dmax_bits, uint8_t* out);
+constexpr int kSurfaceStride = 4;  // pipeline_impl.hpp:219
+constexpr int kFpTileItems = 256;
+
 constexpr int kMaxShards = 16;
 struct ShardGroupArgs {
   int n;

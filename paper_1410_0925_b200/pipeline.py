@@ -262,6 +262,27 @@ class Pipeline:
         self._chk("vf_set_maps", self._L.vf_set_maps(self._h, _ptr(p), _ptr(n),
                                                      rp.ctypes.data_as(C.POINTER(C.c_double))))
 
+    def surface_points(self):
+        """TrackingState::surface_points / surface_colors (tracking_state.hpp:30-31):
+        the stride-4 surface samples of the last render (colour voxels), n x 3 each."""
+        n = int(self._chk("vf_get_surface_points", self._L.vf_get_surface_points(self._h, None, None, 0)))
+        pts = np.zeros((n, 3), np.float32)
+        cols = np.zeros((n, 3), np.float32)
+        if n:
+            self._chk("vf_get_surface_points", self._L.vf_get_surface_points(self._h, _ptr(pts), _ptr(cols), n))
+        return pts, cols
+
+    def forward_project_points(self) -> None:
+        """forward_project_points (raycast.hpp:495-509) over the current maps."""
+        self._chk("vf_stage_forward_project", self._L.vf_stage_forward_project(self._h))
+
+    def get_image(self, mode: int = 0) -> np.ndarray:
+        """IPipeline::get_image(DisplayMode) (pipeline.hpp:74): 0 raycast, 1 depth
+        colourised, 2 RGB passthrough, 3 raycast in shaded grey; H x W x 3 u8."""
+        out = np.zeros((self.height, self.width, 3), np.uint8)
+        self._chk("vf_render_image", self._L.vf_render_image(self._h, int(mode), _ptr(out)))
+        return out
+
     def volume_digest(self) -> int:
         out = C.c_uint64()
         self._chk("vf_volume_digest", self._L.vf_volume_digest(self._h, C.byref(out)))

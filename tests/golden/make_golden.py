@@ -68,6 +68,15 @@ def run(lib, cfg, n, tracking, rgb=False):
             "volume_digest": str(vol.digest()) if tracking else None,
             "ranges_sha": sha(vol.ranges()) if not tracking else None,
         })
+        # raycast epilogues (raycast.hpp:441-509, pipeline_impl.hpp:125-137, 218-221)
+        sp, sc = vol.surface_points()
+        out[-1]["surface_count"] = int(len(sp))
+        out[-1]["surface_points_sha"] = sha(sp)
+        out[-1]["surface_colors_sha"] = sha(sc)
+        out[-1]["image_sha"] = sha(vol.image(0))
+        out[-1]["image_grey_sha"] = sha(vol.image(3))
+        if tracking:
+            out[-1]["image_depth_sha"] = sha(vol.image(1))
     vol.close()
     return out
 

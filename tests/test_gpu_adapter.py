@@ -26,11 +26,12 @@ def _run(lib, cfg, engine, fr):
     dig = C.c_uint64()
     w, h = cfg.width, cfg.height
     pts, nrm = np.zeros((h, w, 4), np.float32), np.zeros((h, w, 4), np.float32)
+    img, dimg = np.zeros((h, w, 3), np.uint8), np.zeros((h, w, 3), np.uint8)
     p = lambda a: a.ctypes.data_as(C.c_void_p)
     rc = lib.vfa_run(C.byref(c), engine, n, p(depth), None, p(poses), p(iters), p(ok), p(vis), C.byref(dig), p(pts),
-                     p(nrm))
+                     p(nrm), p(img), p(dimg))
     assert rc == n
-    return poses, iters, ok, vis, dig.value, pts, nrm
+    return poses, iters, ok, vis, dig.value, pts, nrm, img, dimg
 
 
 @pytest.fixture(scope="module")
@@ -39,7 +40,7 @@ def alib():
         pytest.skip("adapter check not built (make -C oracle adapter needs /root/reference)")
     lib = C.CDLL(str(SO))
     lib.vfa_run.restype = C.c_int
-    lib.vfa_run.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 9
+    lib.vfa_run.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 11
     lib.vfa_set_threads.argtypes = [C.c_int]
     lib.vfa_set_threads(1)
     return lib
@@ -55,6 +56,8 @@ def test_ipipeline_frame0_identical(olib, alib):
     assert ref[4] == gpu[4], "volume_digest differs"
     assert np.array_equal(ref[5].view(np.uint32), gpu[5].view(np.uint32))
     assert np.array_equal(ref[6].view(np.uint32), gpu[6].view(np.uint32))
+    assert np.array_equal(ref[7], gpu[7]), "get_image(raycast) differs"
+    assert np.array_equal(ref[8], gpu[8]), "get_image(depth_colourized) differs"
 
 
 def test_ipipeline_tracked_sequence(olib, alib):

@@ -301,3 +301,56 @@ def test_render_synthetic_matches_oracle(olib):
     co = vf_py.render_rgb(olib, cfg, pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
     assert np.array_equal(dg.view(np.uint32), do.view(np.uint32))
     assert np.array_equal(cg, co)
+
+
+def _assert_epilogues_equal(p, o, depth=None):
+    """forward_project_points + render_image (raycast.hpp:441-509) bit-exact."""
+    sg, cg = p.surface_points()
+    so, co = o.surface_points()
+    assert len(sg) == len(so), f"surface point count {len(sg)} vs {len(so)}"
+    assert np.array_equal(sg.view(np.uint32), so.view(np.uint32)), "surface points differ"
+    assert np.array_equal(cg.view(np.uint32), co.view(np.uint32)), \
+        f"surface colours differ at {np.count_nonzero((cg != co).any(-1))} points"
+    for mode in (0, 3):
+        ig, io = p.get_image(mode), o.image(mode)
+        assert np.array_equal(ig, io), f"render_image mode {mode} differs at {np.count_nonzero((ig != io).any(-1))} px"
+    if depth is not None:
+        assert np.array_equal(p.get_image(1), vf_py.colourize_depth(depth)), "colourize_depth differs"
+
+
+def test_colour_epilogues_known_pose_bit_exact(olib):
+    """Config 2 frames end with forward_project_points (pipeline_impl.hpp:218-221):
+    the surface list, the colour / grey renders and the depth colourisation
+    match the oracle bit for bit after every frame."""
+    cfg = CONFIGS["C2"].with_(tracking=False)
+    p, o = _pair(olib, cfg, False)
+    for pose, depth, col in frames(olib, cfg, 3, rgb=True):
+        p.set_pose(pose)
+        p.process_frame(col, depth)
+        o.process(depth, col, pose)
+        _assert_epilogues_equal(p, o, depth)
+        assert np.array_equal(p.get_image(2), col), "rgb passthrough"
+    p.close()
+
+
+def test_forward_project_from_oracle_state(olib):
+    """Stage-isolated: the oracle's volume and maps imported, then
+    vf_stage_forward_project; also the VoxelS (grey) render path."""
+    for name in ("C2", "T320"):
+        cfg = CONFIGS[name].with_(tracking=False)
+        rgb = cfg.voxel_type == 2
+        p, o = _pair(olib, cfg, False)
+        for pose, depth, col in frames(olib, cfg, 2, rgb=rgb):
+            o.process(depth, col, pose)
+        vt, vsl, et, esl = _oracle_free_stacks(olib, o, cfg)
+        p.import_state(o.entries(), o.voxels(), vt, vsl, et, esl)
+        pts, nrm = o.maps()
+        p.set_maps(pts, nrm, o.pose())
+        p.forward_project_points()
+        if rgb:
+            _assert_epilogues_equal(p, o)
+        else:
+            sg, cg = p.surface_points()
+            assert len(sg) == int(np.count_nonzero(pts[::4, ::4, 3])) and not cg.any()
+            assert np.array_equal(p.get_image(0), o.image(3))
+        p.close()

@@ -75,6 +75,14 @@ def _check_run(lib, cfg, frames_gold, tracking, rgb=False):
             assert str(vol.digest()) == g["volume_digest"], f"frame {i}: FNV volume digest"
         if g.get("ranges_sha") is not None:
             assert sha(vol.ranges()) == g["ranges_sha"]
+        if "surface_points_sha" in g:  # raycast epilogues (raycast.hpp:441-509)
+            sp, sc = vol.surface_points()
+            assert len(sp) == g["surface_count"], f"frame {i}: surface point count"
+            assert sha(sp) == g["surface_points_sha"] and sha(sc) == g["surface_colors_sha"], f"frame {i}: surface list"
+            assert sha(vol.image(0)) == g["image_sha"], f"frame {i}: render_image"
+            assert sha(vol.image(3)) == g["image_grey_sha"], f"frame {i}: render_image (grey)"
+        if "image_depth_sha" in g:
+            assert sha(vf_py.colourize_depth(d)) == g["image_depth_sha"], f"frame {i}: colourize_depth"
     vol.close()
 
 
