@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <vector>
 
 #include "voxfuse/core/parallel.hpp"
@@ -42,6 +43,7 @@ struct vfr_config {
   double rgb_fx, rgb_fy, rgb_cx, rgb_cy;
   int rgb_width, rgb_height;
   double rgb_to_depth[12];  // row-major R (9) then t (3)
+  int use_swapping, swap_buffer_blocks;
 };
 
 struct vfr_stats {
@@ -49,6 +51,9 @@ struct vfr_stats {
   double tracking_cost;
   double pose[12];
   double ms_tracking, ms_allocation, ms_integration, ms_raycast, ms_total;
+  int swapped_in, swapped_out;
+  std::uint64_t bytes_in, bytes_out;
+  double ms_swapping;
 };
 
 }  // extern "C"
@@ -91,6 +96,8 @@ EngineSettings settings_from(const vfr_config& c) {
   s.tracker.icp_dist_threshold = c.icp_dist_threshold;
   s.tracker.convergence_eps = c.convergence_eps;
   s.tracker.max_condition = c.max_condition;
+  s.use_swapping = c.use_swapping != 0;
+  s.swap_buffer_blocks = c.swap_buffer_blocks;
   return s;
 }
 
@@ -125,7 +132,17 @@ struct CtxBase {
   virtual long export_ranges(float* out) const { (void)out; return -1; }
   // get_image (pipeline_impl.hpp:125-137) / render_image (raycast.hpp:466-490)
   virtual int image(int mode, std::uint8_t* out) const = 0;
+  // swap engine state (swap.hpp:45-91); nullptr without swapping
+  virtual const void* cache_ptr() const { return nullptr; }
+  virtual int voxel_type() const = 0;
 };
+
+void fill_swap(const SwapMetrics& m, vfr_stats* st) {
+  st->swapped_in = m.swapped_in;
+  st->swapped_out = m.swapped_out;
+  st->bytes_in = m.bytes_in;
+  st->bytes_out = m.bytes_out;
+}
 
 void copy_image(const Image2D<Vec3u8>& img, std::uint8_t* out) {
   for (std::size_t i = 0; i < img.size(); ++i)
@@ -185,9 +202,13 @@ struct PipelineCtx final : CtxBase {
       st->ms_integration = fs.ms_integration;
       st->ms_raycast = fs.ms_raycast;
       st->ms_total = fs.ms_total;
+      st->ms_swapping = fs.ms_swapping;
+      fill_swap(fs.swap, st);
     }
     return 0;
   }
+  const void* cache_ptr() const override { return const_cast<Pipeline<TVoxel, VolumeBackend::hash>&>(p).cache(); }
+  int voxel_type() const override { return TVoxel::has_color ? 2 : 1; }
   Pose pose() const override { return p.pose(); }
   const TrackingState& state() const override { return p.tracking_state(); }
   long export_entries(void* out) const override { return export_volume_entries(p.volume(), out); }
@@ -225,10 +246,15 @@ struct StagesCtx final : CtxBase {
   TrackingState st;
   RangeImage range;
   vfr_config cfg;
+  std::optional<GlobalCache<TVoxel>> cache;
   int frame = 0;
   StagesCtx(const vfr_config& c) : s(settings_from(c)), calib(calib_from(c)), volume(s.hash), cfg(c) {
     scratch.reset(volume.entry_count());
+    if (s.use_swapping)  // pipeline_impl.hpp:42-51 (in-memory store)
+      cache.emplace(GlobalCache<TVoxel>::in_memory(volume.entry_count(), s.swap_buffer_blocks));
   }
+  const void* cache_ptr() const override { return cache ? &*cache : nullptr; }
+  int voxel_type() const override { return TVoxel::has_color ? 2 : 1; }
   int process(const float* depth, const std::uint8_t* rgb, const double* pose, vfr_stats* out) override {
     if (!pose) return -1;
     using clk = std::chrono::steady_clock;
@@ -246,6 +272,15 @@ struct StagesCtx final : CtxBase {
     t0 = clk::now();
     integrate_frame(volume, scratch.visible_list, view, st.pose, s.scene);
     const double ms_int = detail::ms_since(t0);
+    t0 = clk::now();
+    SwapMetrics swap;
+    if (cache) {  // pipeline_impl.hpp:104-113
+      request_swap_ins(volume, scratch, *cache);
+      swap.accumulate(execute_swap_in(volume, *cache, s.scene));
+      request_swap_outs(volume, scratch, *cache);
+      swap.accumulate(execute_swap_out(volume, *cache));
+    }
+    const double ms_swap = detail::ms_since(t0);
     t0 = clk::now();
     range = create_expected_depths(volume, scratch.visible_list, st.pose, calib.depth, s.scene,
                                    s.near_clip, s.far_clip);
@@ -268,6 +303,8 @@ struct StagesCtx final : CtxBase {
       out->ms_allocation = ms_alloc;
       out->ms_integration = ms_int;
       out->ms_raycast = ms_ray;
+      out->ms_swapping = ms_swap;
+      fill_swap(swap, out);
       out->ms_total = detail::ms_since(t_start);
     }
     ++frame;
@@ -326,6 +363,15 @@ SyntheticScene scene_from(int n_spheres, const double* spheres, int n_planes, co
 
 }  // namespace
 
+namespace {
+template <typename TVoxel, typename F>
+long with_cache(const CtxBase* b, F&& f) {
+  const auto* c = static_cast<const GlobalCache<TVoxel>*>(b->cache_ptr());
+  if (!c) return -1;
+  return f(*c);
+}
+}  // namespace
+
 extern "C" {
 
 void vfr_set_threads(int n) { set_worker_count(n); }
@@ -373,6 +419,30 @@ long vfr_surface_points(void* ctx, float* points, float* colors) {
   return n;
 }
 int vfr_image(void* ctx, int mode, std::uint8_t* out) { return static_cast<CtxBase*>(ctx)->image(mode, out); }
+
+// Swap engine state: per-entry SwapState codes, host store contents (codec layout).
+long vfr_swap_states(void* ctx, std::uint8_t* out) {
+  const CtxBase* b = static_cast<CtxBase*>(ctx);
+  auto f = [&](const auto& c) -> long {
+    for (int i = 0; i < c.entry_count(); ++i) out[i] = static_cast<std::uint8_t>(c.state(i));
+    return c.entry_count();
+  };
+  return b->voxel_type() == 2 ? with_cache<VoxelSRgb>(b, f) : with_cache<VoxelS>(b, f);
+}
+int vfr_store_read(void* ctx, int idx, std::uint8_t* payload) {
+  const CtxBase* b = static_cast<CtxBase*>(ctx);
+  auto f = [&](const auto& c) -> long {
+    if (!c.has_stored_data(idx)) return 0;
+    if (payload) c.store().read(idx, payload);
+    return 1;
+  };
+  return static_cast<int>(b->voxel_type() == 2 ? with_cache<VoxelSRgb>(b, f) : with_cache<VoxelS>(b, f));
+}
+long vfr_store_count(void* ctx) {
+  const CtxBase* b = static_cast<CtxBase*>(ctx);
+  auto f = [&](const auto& c) -> long { return c.store().stored_count(); };
+  return b->voxel_type() == 2 ? with_cache<VoxelSRgb>(b, f) : with_cache<VoxelS>(b, f);
+}
 std::uint64_t vfr_digest(void* ctx) { return static_cast<CtxBase*>(ctx)->digest(); }
 long vfr_allocated_blocks(void* ctx) { return static_cast<CtxBase*>(ctx)->allocated_blocks(); }
 

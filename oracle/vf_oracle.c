@@ -423,6 +423,11 @@ struct vfo_ctx {
   f3* surf_points;
   f3* surf_colors;
   long n_surface;
+  /* GlobalCache (swap.hpp:45-91): per-entry states + a memory block store
+   * (block_store.cpp:28-56) holding VoxelCodec payloads, NULL = no data */
+  uint8_t* swap_state;
+  uint8_t** store;
+  int payload_bytes;
 };
 
 static uint8_t* vox_bytes(vfo_ctx* c, long slot, int lin) {
@@ -1044,6 +1049,148 @@ static void render_image(vfo_ctx* c, int color, uint8_t* out) {
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* swap engine (engine/swap.hpp)                                             */
+/* ------------------------------------------------------------------------ */
+enum { SW_INACTIVE = 0, SW_NEEDS_IN = 1, SW_IN_TRANSFER = 2, SW_ACTIVE = 3, SW_NEEDS_OUT = 4 };
+
+/* VoxelCodec encode / decode (voxel.hpp:124-155): the first 3 (VoxelS) or 7
+ * (VoxelSRgb) bytes of the oracle's voxel layout are exactly the codec bytes */
+static int codec_bytes(const vfo_ctx* c) { return c->has_color ? 7 : 3; }
+
+/* fuse_voxels (swap.hpp:96-131) on voxel bytes: out = active fused with host */
+static void fuse_voxel(vfo_ctx* c, const uint8_t* host, uint8_t* active) {
+  const int max_weight = c->cfg.max_weight;
+  uint8_t out[8];
+  memcpy(out, active, (size_t)c->vsize);
+  const int wh = host[2], wa = active[2];
+  if (wh + wa > 0) {
+    if (wa == 0) {
+      out[0] = host[0];
+      out[1] = host[1];
+      out[2] = host[2];
+    } else if (wh == 0) {
+      /* keep active */
+    } else {
+      int16_t hs, as;
+      memcpy(&hs, host, 2);
+      memcpy(&as, active, 2);
+      const float f = (sdf_to_float(hs) * (float)wh + sdf_to_float(as) * (float)wa) / (float)(wh + wa);
+      const int16_t q = sdf_from_float(f);
+      memcpy(out, &q, 2);
+      out[2] = (uint8_t)(wh + wa < max_weight ? wh + wa : max_weight);
+    }
+  }
+  if (c->has_color) {
+    const int ch = host[6], ca = active[6];
+    if (ca == 0) {
+      out[3] = host[3], out[4] = host[4], out[5] = host[5], out[6] = host[6];
+    } else if (ch == 0) {
+      /* active colour kept */
+    } else {
+      for (int k = 0; k < 3; ++k) {
+        const float v = ((float)host[3 + k] * (float)ch + (float)active[3 + k] * (float)ca) / (float)(ch + ca);
+        out[3 + k] = (uint8_t)v;
+      }
+      out[6] = (uint8_t)(ch + ca < max_weight ? ch + ca : max_weight);
+    }
+  }
+  memcpy(active, out, (size_t)c->vsize);
+}
+
+/* request_swap_ins (swap.hpp:136-149) */
+static void request_swap_ins(vfo_ctx* c) {
+  for (int i = 0; i < c->entry_count; ++i) {
+    const int visible = c->swap_visibility[i] != 0;
+    if (c->swap_state[i] == SW_NEEDS_IN && !visible) c->swap_state[i] = SW_INACTIVE;
+    if (c->entries[i].block_state == kEntrySwappedOut && c->store[i] && visible) c->swap_state[i] = SW_NEEDS_IN;
+  }
+}
+
+/* execute_swap_in (swap.hpp:151-198) */
+static void execute_swap_in(vfo_ctx* c, vfo_stats* m) {
+  const int cap = c->cfg.swap_buffer_blocks;
+  int staged = 0;
+  for (int i = 0; i < c->entry_count && staged < cap; ++i) {
+    if (c->swap_state[i] != SW_NEEDS_IN) continue;
+    entry_t* e = &c->entries[i];
+    int slot = e->block_state;
+    if (slot < 0) {
+      slot = fs_pop(&c->vba_free);
+      if (slot < 0) break; /* deferred, request stays queued */
+      e->block_state = slot;
+    }
+    c->swap_state[i] = SW_IN_TRANSFER;
+    /* secondary integration of the host block into the active one */
+    const int cb = codec_bytes(c);
+    for (int v = 0; v < kBlockVolume; ++v) {
+      uint8_t host[8] = {0};
+      memcpy(host, c->store[i] + (size_t)v * cb, (size_t)cb);
+      fuse_voxel(c, host, vox_bytes(c, slot, v));
+    }
+    free(c->store[i]); /* store.clear */
+    c->store[i] = NULL;
+    c->swap_state[i] = SW_ACTIVE;
+    ++m->swapped_in;
+    m->bytes_in += (uint64_t)c->payload_bytes + 4;
+    ++staged;
+  }
+}
+
+/* request_swap_outs (swap.hpp:204-227) */
+static void request_swap_outs(vfo_ctx* c) {
+  for (int i = 0; i < c->entry_count; ++i) {
+    if (c->entries[i].block_state < 0) continue;
+    const int visible = c->swap_visibility[i] != 0;
+    switch (c->swap_state[i]) {
+      case SW_INACTIVE: c->swap_state[i] = visible ? SW_ACTIVE : SW_NEEDS_OUT; break;
+      case SW_ACTIVE: if (!visible) c->swap_state[i] = SW_NEEDS_OUT; break;
+      case SW_NEEDS_OUT: if (visible) c->swap_state[i] = SW_ACTIVE; break;
+      default: break;
+    }
+  }
+}
+
+/* execute_swap_out (swap.hpp:233-251) */
+static void execute_swap_out(vfo_ctx* c, vfo_stats* m) {
+  const int cap = c->cfg.swap_buffer_blocks;
+  const int cb = codec_bytes(c);
+  int processed = 0;
+  for (int i = 0; i < c->entry_count && processed < cap; ++i) {
+    if (c->swap_state[i] != SW_NEEDS_OUT) continue;
+    entry_t* e = &c->entries[i];
+    if (!c->store[i]) c->store[i] = (uint8_t*)malloc((size_t)c->payload_bytes);
+    for (int v = 0; v < kBlockVolume; ++v) {
+      uint8_t* vb = vox_bytes(c, e->block_state, v);
+      memcpy(c->store[i] + (size_t)v * cb, vb, (size_t)cb);
+      memset(vb, 0, (size_t)c->vsize); /* TVoxel{}: sdf 32767, weights and colour 0 */
+      vb[0] = 0xFF;
+      vb[1] = 0x7F;
+    }
+    fs_push(&c->vba_free, e->block_state);
+    e->block_state = kEntrySwappedOut;
+    c->swap_state[i] = SW_INACTIVE;
+    ++processed;
+    ++m->swapped_out;
+    m->bytes_out += (uint64_t)c->payload_bytes + 4;
+  }
+}
+
+long vfo_swap_states(const vfo_ctx* c, uint8_t* out) {
+  if (out) memcpy(out, c->swap_state, (size_t)c->entry_count);
+  return c->entry_count;
+}
+int vfo_store_read(const vfo_ctx* c, int idx, uint8_t* payload) {
+  if (idx < 0 || idx >= c->entry_count || !c->store[idx]) return 0;
+  if (payload) memcpy(payload, c->store[idx], (size_t)c->payload_bytes);
+  return 1;
+}
+long vfo_store_count(const vfo_ctx* c) {
+  long n = 0;
+  for (int i = 0; i < c->entry_count; ++i) n += c->store[i] != NULL;
+  return n;
+}
+
 /* Pipeline::colourize_depth (pipeline_impl.hpp:225-239) */
 void vfo_colourize_depth(const float* depth, int w, int h, uint8_t* out) {
   const size_t n = (size_t)w * h;
@@ -1365,6 +1512,9 @@ vfo_ctx* vfo_create(const vfo_config* cfg, int tracking) {
   c->surf_colors = (f3*)calloc((size_t)((cfg->width + 3) / 4) * ((cfg->height + 3) / 4), sizeof(f3));
   c->pose = pose_identity();
   c->render_pose = pose_identity();
+  c->swap_state = (uint8_t*)calloc((size_t)c->entry_count, 1);
+  c->store = (uint8_t**)calloc((size_t)c->entry_count, sizeof(uint8_t*));
+  c->payload_bytes = (c->has_color ? 7 : 3) * kBlockVolume;
   return c;
 }
 
@@ -1385,6 +1535,10 @@ void vfo_destroy(vfo_ctx* c) {
   free(c->trace);
   free(c->surf_points);
   free(c->surf_colors);
+  if (c->store)
+    for (int i = 0; i < c->entry_count; ++i) free(c->store[i]);
+  free(c->store);
+  free(c->swap_state);
   free(c);
 }
 
@@ -1500,6 +1654,14 @@ int vfo_process(vfo_ctx* c, const float* depth, const uint8_t* rgb, const double
   t0 = now_ms();
   integrate_frame(c, depth, rgb, &c->pose);
   s.ms_integration = now_ms() - t0;
+  t0 = now_ms();
+  if (c->cfg.use_swapping) { /* pipeline_impl.hpp:104-113 */
+    request_swap_ins(c);
+    execute_swap_in(c, &s);
+    request_swap_outs(c);
+    execute_swap_out(c, &s);
+  }
+  s.ms_swapping = now_ms() - t0;
   t0 = now_ms();
   create_expected_depths(c, &c->pose);
   render_maps(c, &c->pose);

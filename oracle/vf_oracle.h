@@ -37,6 +37,8 @@ typedef struct vfo_config {
   double rgb_fx, rgb_fy, rgb_cx, rgb_cy;
   int rgb_width, rgb_height;
   double rgb_to_depth[12];
+  /* EngineSettings::use_swapping / swap_buffer_blocks (pipeline.hpp:20-23) */
+  int use_swapping, swap_buffer_blocks;
 } vfo_config;
 
 typedef struct vfo_stats {
@@ -44,6 +46,10 @@ typedef struct vfo_stats {
   double tracking_cost;
   double pose[12];
   double ms_tracking, ms_allocation, ms_integration, ms_raycast, ms_total;
+  /* SwapMetrics (swap.hpp:28-40), accumulated over swap-in and swap-out */
+  int swapped_in, swapped_out;
+  uint64_t bytes_in, bytes_out;
+  double ms_swapping;
 } vfo_stats;
 
 typedef struct vfo_alloc_stats {
@@ -93,6 +99,13 @@ long vfo_surface_points(const vfo_ctx* c, float* points, float* colors);
 int vfo_stage_forward_project(vfo_ctx* c);
 int vfo_render_image(vfo_ctx* c, int color, uint8_t* out);
 void vfo_colourize_depth(const float* depth, int w, int h, uint8_t* out);
+/* swap engine (swap.hpp:14-253): per-entry SwapState codes (inactive 0,
+ * needs_swap_in 1, in_transfer 2, active 3, needs_swap_out 4); host store
+ * contents in the VoxelCodec layout (voxel.hpp:93-189, 3 / 7 bytes per voxel):
+ * vfo_store_read returns 1 and fills payload when entry idx holds data. */
+long vfo_swap_states(const vfo_ctx* c, uint8_t* out);
+int vfo_store_read(const vfo_ctx* c, int idx, uint8_t* payload);
+long vfo_store_count(const vfo_ctx* c);
 
 /* Free functions. */
 uint32_t vfo_hash_block_pos(int x, int y, int z, uint32_t mask);

@@ -62,6 +62,8 @@ class Config(C.Structure):
         ("rgb_width", C.c_int),
         ("rgb_height", C.c_int),
         ("rgb_to_depth", C.c_double * 12),
+        ("use_swapping", C.c_int),
+        ("swap_buffer_blocks", C.c_int),
     ]
 
 
@@ -80,6 +82,11 @@ class Stats(C.Structure):
         ("ms_integration", C.c_double),
         ("ms_raycast", C.c_double),
         ("ms_total", C.c_double),
+        ("swapped_in", C.c_int),
+        ("swapped_out", C.c_int),
+        ("bytes_in", C.c_uint64),
+        ("bytes_out", C.c_uint64),
+        ("ms_swapping", C.c_double),
     ]
 
 
@@ -117,6 +124,8 @@ def make_config(cfg) -> Config:
     ident = [1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0]
     for i, v in enumerate(ident):
         c.rgb_to_depth[i] = v
+    c.use_swapping = 1 if getattr(cfg, "use_swapping", False) else 0
+    c.swap_buffer_blocks = getattr(cfg, "swap_buffer_blocks", 100)
     return c
 
 
@@ -154,6 +163,12 @@ class _Lib:
         getattr(L, p + "depth_pyramid").argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         getattr(L, p + "surface_points").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         getattr(L, p + "surface_points").restype = C.c_long
+        getattr(L, p + "swap_states").argtypes = [C.c_void_p, C.c_void_p]
+        getattr(L, p + "swap_states").restype = C.c_long
+        getattr(L, p + "store_read").argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        getattr(L, p + "store_read").restype = C.c_int
+        getattr(L, p + "store_count").argtypes = [C.c_void_p]
+        getattr(L, p + "store_count").restype = C.c_long
 
 
 class OracleLib(_Lib):
@@ -298,6 +313,34 @@ class Volume:
 
     def digest(self) -> int:
         return int(self._f("digest")(self.h))
+
+    def swap_states(self) -> np.ndarray:
+        """Per-entry SwapState codes (swap.hpp:19-25)."""
+        out = np.zeros(self.cfg.hash.entry_count, np.uint8)
+        if self._f("swap_states")(self.h, out.ctypes.data_as(C.c_void_p)) < 0:
+            return None
+        return out
+
+    def store_count(self) -> int:
+        return int(self._f("store_count")(self.h))
+
+    def store_read(self, idx: int):
+        """Host store payload of entry idx (VoxelCodec bytes), or None."""
+        payload = np.zeros(512 * (7 if self.cfg.voxel_type == 2 else 3), np.uint8)
+        if self._f("store_read")(self.h, int(idx), payload.ctypes.data_as(C.c_void_p)) != 1:
+            return None
+        return payload
+
+    def store(self) -> dict:
+        """{entry index: payload} for every stored block."""
+        st = self.swap_states()
+        out = {}
+        e = self.entries()
+        for i in np.nonzero(e["block_state"] == -1)[0]:
+            p = self.store_read(int(i))
+            if p is not None:
+                out[int(i)] = p
+        return out
 
     def surface_points(self):
         """TrackingState::surface_points / surface_colors (n x 3 float32 each)."""

@@ -107,6 +107,88 @@ def trajectory(n_frames: int, amplitude: float = 1.0) -> np.ndarray:
     return out
 
 
+def pan_trajectory(n_frames: int, max_yaw: float = 1.2) -> np.ndarray:
+    """World-to-camera poses that yaw the camera away (to +max_yaw rad at the
+    middle frame) and back to the start: blocks leave the enlarged swap
+    frustum and return, exercising swap-out and swap-in (swap.hpp)."""
+    out = np.zeros((n_frames, 12))
+    for i in range(n_frames):
+        u = i / max(n_frames - 1, 1)
+        yaw = max_yaw * math.sin(math.pi * u)
+        r_c2w = _rot_y(yaw)
+        centre = np.array([0.0, 0.0, 0.4 * math.sin(math.pi * u)])
+        r_w2c = r_c2w.T
+        out[i, :9] = r_w2c.reshape(-1)
+        out[i, 9:] = -r_w2c @ centre
+    out[0, :9] = np.eye(3).reshape(-1)
+    out[0, 9:] = 0.0
+    return out
+
+
+# Corridor (config 4): walls x = +-1.0, floor y = 1.2, ceiling y = -1.3 (y
+# down), a wall behind the start; pillars (spheres) every 2 m on alternating
+# sides break the corridor's translational symmetry for the tracker
+# (SURVEY.md §8(d) C4).  The sensor range is cut at CORRIDOR_FAR metres.
+CORRIDOR_FAR = 5.0
+CORRIDOR_PLANES = np.array(
+    [
+        [1, 0, 0, 1.0, 0.70, 0.45, 0.40, 1, 0.30],
+        [1, 0, 0, -1.0, 0.40, 0.60, 0.45, 1, 0.30],
+        [0, 1, 0, 1.2, 0.55, 0.55, 0.60, 1, 0.25],
+        [0, 1, 0, -1.3, 0.80, 0.80, 0.75, 0, 0.25],
+        [0, 0, 1, -1.0, 0.60, 0.50, 0.40, 0, 0.40],
+    ],
+    dtype=np.float64,
+)
+
+
+def corridor_spheres(length: float = 60.0) -> np.ndarray:
+    rows = []
+    k = 0
+    z = 1.5
+    while z < length:
+        side = 1.0 if k % 2 == 0 else -1.0
+        rows.append([0.85 * side, 0.35 * math.sin(1.3 * k), z, 0.28, 0.3 + 0.6 * ((k * 37) % 10) / 10.0,
+                     0.3 + 0.6 * ((k * 53) % 10) / 10.0, 0.3 + 0.6 * ((k * 71) % 10) / 10.0])
+        if k % 3 == 0:  # a low obstacle on the floor
+            rows.append([-0.4 * side, 1.05, z + 0.9, 0.18, 0.8, 0.7, 0.3])
+        k += 1
+        z += 2.0
+    return np.array(rows, dtype=np.float64)
+
+
+CORRIDOR_SPHERES = corridor_spheres()
+
+
+def corridor_trajectory(n_frames: int, step: float = 0.05) -> np.ndarray:
+    """World-to-camera poses walking down the corridor (+z) by `step` metres
+    per frame with a gentle sway (at most ~1 deg and ~1 cm per frame)."""
+    out = np.zeros((n_frames, 12))
+    for i in range(n_frames):
+        a = 2.0 * math.pi * i / 80.0
+        centre = np.array([0.15 * math.sin(a), 0.04 * math.sin(2 * a), step * i])
+        r_c2w = _rot_y(0.08 * math.sin(a)) @ _rot_x(0.03 * math.sin(2 * a))
+        r_w2c = r_c2w.T
+        out[i, :9] = r_w2c.reshape(-1)
+        out[i, 9:] = -r_w2c @ centre
+    out[0, :9] = np.eye(3).reshape(-1)
+    out[0, 9:] = 0.0
+    return out
+
+
+def scene_for(cfg):
+    """(spheres, planes, far) of a config's scene."""
+    if getattr(cfg, "scene", "box_room") == "corridor":
+        return CORRIDOR_SPHERES, CORRIDOR_PLANES, CORRIDOR_FAR
+    return BOX_ROOM_SPHERES, BOX_ROOM_PLANES, 100.0
+
+
+def trajectory_for(cfg, n_frames: int) -> np.ndarray:
+    if getattr(cfg, "scene", "box_room") == "corridor":
+        return corridor_trajectory(n_frames)
+    return trajectory(n_frames)
+
+
 @dataclass(frozen=True)
 class HashConfig:
     """HashConfig (proj/include/voxfuse/volume/hash_volume.hpp:49-58)."""
@@ -148,6 +230,9 @@ class BenchConfig:
     icp_dist_threshold: float = 0.1
     convergence_eps: float = 1e-5
     max_condition: float = 1e8
+    use_swapping: bool = False  # EngineSettings::use_swapping (pipeline.hpp:20-23)
+    swap_buffer_blocks: int = 100
+    scene: str = "box_room"  # box_room | corridor
 
     @property
     def intrinsics(self):
@@ -171,6 +256,12 @@ CONFIGS = {
         "T160", 160, 120, 0.02, mu=0.06, frames=6,
         hash=HashConfig(bucket_count=1 << 14, excess_count=1 << 12, block_count=1 << 13),
     ),
+    # configs[3]: ~50 m corridor walk (1000 frames at 5 cm) with host swapping;
+    # B = 512 transfers per frame keeps eviction ahead of the ~400 blocks a
+    # frame allocates at this speed (the reference default B = 100 would
+    # exhaust the 2^18-block pool after ~30 m and drop allocations).
+    "C4": BenchConfig("C4", 640, 480, 0.005, frames=1000, use_swapping=True, swap_buffer_blocks=512,
+                      scene="corridor"),
     "T320": BenchConfig(
         "T320", 320, 240, 0.01, mu=0.03, frames=6,
         hash=HashConfig(bucket_count=1 << 17, excess_count=1 << 14, block_count=1 << 15),

@@ -21,8 +21,10 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "oracle"))
+sys.path.insert(0, str(ROOT / "tests"))
 
 import vf_py  # noqa: E402
+from helpers import SWAP_CASES, swap_config  # noqa: E402
 from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, trajectory  # noqa: E402
 
 
@@ -81,6 +83,39 @@ def run(lib, cfg, n, tracking, rgb=False):
     return out
 
 
+def store_digest(vol) -> str:
+    """sha over (entry index, payload) of every stored block, ascending."""
+    h = hashlib.sha256()
+    for k, v in sorted(vol.store().items()):
+        h.update(np.int32(k).tobytes())
+        h.update(v.tobytes())
+    return h.hexdigest()
+
+
+def run_swap(lib, name, n=24):
+    from paper_1410_0925_b200.scene import pan_trajectory
+    cfg = swap_config(name)
+    poses = pan_trajectory(n)
+    vol = vf_py.Volume(lib, cfg, False)
+    out = []
+    for i in range(n):
+        d = vf_py.render_depth(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        st = vol.process(d, None, poses[i])
+        pts, nrm = vol.maps()
+        out.append({
+            "frame": i, "depth_sha": sha(d),
+            "blocks_allocated": int(st.blocks_allocated), "allocation_dropped": int(st.allocation_dropped),
+            "visible_blocks": int(st.visible_blocks), "allocated_total": int(vol.allocated_blocks()),
+            "swapped_in": int(st.swapped_in), "swapped_out": int(st.swapped_out),
+            "bytes_in": int(st.bytes_in), "bytes_out": int(st.bytes_out),
+            "entries_sha": entries_digest(vol.entries()), "voxels_sha": voxels_digest(vol.voxels(), 4),
+            "states_sha": sha(vol.swap_states()), "store_count": int(vol.store_count()),
+            "store_sha": store_digest(vol), "points_sha": sha(pts), "normals_sha": sha(nrm),
+        })
+    vol.close()
+    return out
+
+
 def main():
     lib = vf_py.ref_lib()
     lib.lib.vfr_set_threads(1)
@@ -96,6 +131,8 @@ def main():
         "T320_known_pose": run(lib, CONFIGS["T320"].with_(tracking=False), 3, tracking=False),
         "C2_known_pose_rgb": run(lib, CONFIGS["C2"], 2, tracking=False, rgb=True),
     }
+    for name in SWAP_CASES:
+        gold[name] = run_swap(lib, name)
     cfg = CONFIGS["C1"]
     d = vf_py.render_depth(lib, cfg, trajectory(5)[3], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
     d[100:140, 200:260] = 0.0

@@ -48,3 +48,19 @@ def centre_dist(p, q):
     ra, rb = np.asarray(p[:9]).reshape(3, 3), np.asarray(q[:9]).reshape(3, 3)
     ca, cb = -ra.T @ np.asarray(p[9:]), -rb.T @ np.asarray(q[9:])
     return float(np.linalg.norm(ca - cb))
+
+
+# Swap-engine parity cases (tests/golden/make_golden.py): (block_count,
+# swap_buffer_blocks) on T160 with the pan trajectory — a VBA so small that
+# swap-ins are deferred, and one large enough that blocks come back.
+SWAP_CASES = {
+    "T160_swap_small_vba": (1200, 16),
+    "T160_swap_roundtrip": (6000, 64),
+}
+
+
+def swap_config(name):
+    from paper_1410_0925_b200.scene import CONFIGS, HashConfig
+    blocks, b = SWAP_CASES[name]
+    return CONFIGS["T160"].with_(tracking=False, use_swapping=True, swap_buffer_blocks=b,
+                                 hash=HashConfig(bucket_count=1 << 14, excess_count=1 << 12, block_count=blocks))

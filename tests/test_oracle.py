@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 
 import vf_py
-from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, trajectory
+from helpers import swap_config
+from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, pan_trajectory, trajectory
 
 GOLD = json.loads((Path(__file__).parent / "golden" / "golden_ref.json").read_text())
 
@@ -150,3 +151,37 @@ def test_icp_reference_vs_oracle_stage(olib, rlib):
     assert bool(ok_o) == bool(ok_r) and it.value == it2.value and valid.value == valid2.value
     assert np.array_equal(out_o, out_r)
     assert cost.value == cost2.value
+
+
+def _store_digest(vol):
+    h = hashlib.sha256()
+    for k, v in sorted(vol.store().items()):
+        h.update(np.int32(k).tobytes())
+        h.update(v.tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("name", ["T160_swap_small_vba", "T160_swap_roundtrip"])
+def test_oracle_golden_swap(olib, name):
+    """Swap engine (swap.hpp): the restatement reproduces the reference's
+    entries, voxels, per-entry swap states, host store contents and
+    SwapMetrics on a pan away and back (budget caps, deferred swap-ins)."""
+    cfg = swap_config(name)
+    poses = pan_trajectory(len(GOLD[name]))
+    vol = vf_py.Volume(olib, cfg, False)
+    for i, g in enumerate(GOLD[name]):
+        d = vf_py.render_depth(olib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        assert sha(d) == g["depth_sha"]
+        st = vol.process(d, None, poses[i])
+        got = (st.blocks_allocated, st.allocation_dropped, st.visible_blocks, st.swapped_in, st.swapped_out,
+               st.bytes_in, st.bytes_out)
+        want = tuple(g[k] for k in ("blocks_allocated", "allocation_dropped", "visible_blocks", "swapped_in",
+                                    "swapped_out", "bytes_in", "bytes_out"))
+        assert got == want, f"frame {i}: stats {got} vs {want}"
+        e = vol.entries()
+        e["pad"] = 0
+        assert sha(e) == g["entries_sha"], f"frame {i}: entries"
+        assert sha(vol.voxels().reshape(-1, 4)[:, :3]) == g["voxels_sha"], f"frame {i}: voxels"
+        assert sha(vol.swap_states()) == g["states_sha"], f"frame {i}: swap states"
+        assert vol.store_count() == g["store_count"] and _store_digest(vol) == g["store_sha"], f"frame {i}: store"
+    vol.close()
