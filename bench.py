@@ -160,23 +160,24 @@ def cpu_reference_run(cfg, n_frames: int, budget_s: float, threads: int = 0):
     Frames 1.. (tracked) are timed; frame 0 (no tracking) is untimed."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import vf_py
-    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, trajectory
+    from paper_1410_0925_b200.scene import scene_for, trajectory_for
 
     if not vf_py.ref_available():
         return None
+    spheres, planes, far = scene_for(cfg)
     lib = vf_py.ref_lib()
     lib.lib.vfr_set_threads(threads if threads > 0 else (os.cpu_count() or 1))
     cores = int(lib.lib.vfr_get_threads())
-    poses = trajectory(n_frames + 1)
+    poses = trajectory_for(cfg, n_frames + 1)
     vol = vf_py.Volume(lib, cfg, tracking=cfg.tracking)
     rgb = cfg.voxel_type == 2
-    depth0 = vf_py.render_depth(lib, cfg, poses[0], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
-    c0 = vf_py.render_rgb(lib, cfg, poses[0], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) if rgb else None
+    depth0 = vf_py.render_depth(lib, cfg, poses[0], spheres, planes, 0.05, far)
+    c0 = vf_py.render_rgb(lib, cfg, poses[0], spheres, planes, 0.05, far) if rgb else None
     vol.process(depth0, c0, None if cfg.tracking else poses[0])
     t_total, frames, voxels = 0.0, 0, 0
     for i in range(1, n_frames + 1):
-        d = vf_py.render_depth(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
-        c = vf_py.render_rgb(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) if rgb else None
+        d = vf_py.render_depth(lib, cfg, poses[i], spheres, planes, 0.05, far)
+        c = vf_py.render_rgb(lib, cfg, poses[i], spheres, planes, 0.05, far) if rgb else None
         t0 = time.perf_counter()
         st = vol.process(d, c, None if cfg.tracking else poses[i])
         t_total += time.perf_counter() - t0
@@ -219,7 +220,8 @@ def run_reference_arm(args, dist: Dist):
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(times), "warmup": 1, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} {w}x{h} {cfg.voxel_size * 1000:.0f}mm voxels, box room + spheres",
+        "config": {"workload": f"{cfg.name} {w}x{h} {cfg.voxel_size * 1000:.0f}mm voxels, {cfg.scene} scene"
+                               + (f", swapping B={cfg.swap_buffer_blocks}" if cfg.use_swapping else ""),
                    "l2": "n/a (CPU)"},
         "voxel_updates_per_s": float(np.mean(vps)),
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": res["cores"], "kind": "reference",
@@ -235,7 +237,7 @@ def run_reference_arm(args, dist: Dist):
 def run_ours(args, dist: Dist):
     from paper_1410_0925_b200 import DeviceBuffer, Intrinsics, make_pipeline, render_synthetic, settings_from_config
     from paper_1410_0925_b200 import _abi
-    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, trajectory
+    from paper_1410_0925_b200.scene import CONFIGS, scene_for, trajectory_for
 
     L = _abi.load()
     cfg = CONFIGS[args.config]
@@ -244,13 +246,14 @@ def run_ours(args, dist: Dist):
     intr = Intrinsics(fx, fy, cx, cy, w, h)
     rgb = cfg.voxel_type == 2
     n_frames = args.warmup + args.steps
-    poses = trajectory(n_frames)
+    poses = trajectory_for(cfg, n_frames)
+    spheres, planes, far = scene_for(cfg)
     # inputs rendered once on the GPU, resident in HBM
     d_frames = [DeviceBuffer(w * h * 4) for _ in range(n_frames)]
     c_frames = [DeviceBuffer(w * h * 3) for _ in range(n_frames)] if rgb else None
     for i in range(n_frames):
-        render_synthetic(poses[i], intr, BOX_ROOM_SPHERES, BOX_ROOM_PLANES, d_frames[i].ptr,
-                         c_frames[i].ptr if rgb else None, device=device)
+        render_synthetic(poses[i], intr, spheres, planes, d_frames[i].ptr, c_frames[i].ptr if rgb else None,
+                         far=far, device=device)
     settings, calib = settings_from_config(cfg)
     flush = args.l2_flush_mib << 20
     sharded = dist.world > 1 and args.mode == "shard"
@@ -267,10 +270,13 @@ def run_ours(args, dist: Dist):
             attach_nccl(p, dist.rank, dist.world, dist.pg)
         return p
 
+    swaps = []
+
     def run_device(collect_stages=False):
         p = new_pipeline()
         hctx = p.handle
         ms_frames, vis_blocks, modified = [], [], []
+        swaps.clear()
         stage = np.zeros(8)
         for i in range(n_frames):
             timed = i >= args.warmup
@@ -293,6 +299,8 @@ def run_ours(args, dist: Dist):
                 st = _abi.VfFrameStats()
                 _abi.check("vf_read_stats", L.vf_read_stats(hctx, C.byref(st)))
                 vis_blocks.append(st.visible_blocks)
+                swaps.append((st.swapped_in, st.swapped_out, st.swap_bytes_in + st.swap_bytes_out,
+                              st.allocation_dropped))
                 modified.append(L.vf_last_modified_voxels(hctx))
         if collect_stages:
             stage, nprof = p.stage_times()
@@ -305,6 +313,7 @@ def run_ours(args, dist: Dist):
     clocks = ClockSampler(device)
     clocks.start()
     ms_frames, vis, modified, _, launches = run_device()
+    swaps_t = list(swaps)
     clk = clocks.stop()
     t_local = float(ms_frames.sum()) / 1000.0
     t_max = dist.max(t_local)
@@ -364,7 +373,9 @@ def run_ours(args, dist: Dist):
     # B = N_vis (512 sizeof(V) + 4 + 16) + N_mod sizeof(V) + W H 4 (+ W H 3 rgb)
     integ_bytes = nvis * (512 * vsize + 4 + 16) + nmod * vsize + npix * 4 + (npix * 3 if rgb else 0)
     stages = {"tracking": stage_ms[0], "allocation": stage_ms[1], "integration": stage_ms[2],
-              "raycast": stage_ms[3]}
+              "raycast": stage_ms[4]}
+    if cfg.use_swapping:
+        stages["swapping"] = stage_ms[3]
     integ_ms = stage_ms[2]
     integ_gbs = integ_bytes / (integ_ms * 1e-3) / 1e9 if integ_ms > 0 else 0.0
     dominant = max(stages, key=stages.get)
@@ -379,7 +390,9 @@ def run_ours(args, dist: Dist):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TSDF/raycast) + f64 (allocation DDA, ICP)",
-        "data": "synthetic (GPU-rendered box room + spheres, 100-frame small-motion trajectory)",
+        "data": (f"synthetic (GPU-rendered corridor + pillars, {n_frames}-frame walk at 5 cm/frame)"
+                 if cfg.scene == "corridor" else
+                 "synthetic (GPU-rendered box room + spheres, 100-frame small-motion trajectory)"),
         "config": {
             "workload": f"{cfg.name}: {w}x{h} depth, {cfg.voxel_size * 1000:.0f} mm voxels, mu {cfg.mu * 1000:.0f} mm, "
                         f"{'VoxelSRgb' if rgb else 'VoxelS'}, hash {cfg.hash.bucket_count}x{cfg.hash.bucket_size}"
@@ -395,6 +408,13 @@ def run_ours(args, dist: Dist):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": npix * 4 + (npix * 3 if rgb else 0),
                 "d2h_bytes_per_step": readback},
         "gpu_launches": launches,
+        **({"swap": {"swapped_in_per_frame": float(np.mean([x[0] for x in swaps_t])),
+                     "swapped_out_per_frame": float(np.mean([x[1] for x in swaps_t])),
+                     "bytes_per_frame": float(np.mean([x[2] for x in swaps_t])),
+                     "allocation_dropped_total": int(sum(x[3] for x in swaps_t)),
+                     "buffer_blocks": cfg.swap_buffer_blocks,
+                     "host_store": "pinned host memory mapped into the device; transfers by k_swap_transfer"}}
+           if cfg.use_swapping else {}),
         "roofline": roofline,
         "clocks": clk,
     }

@@ -35,7 +35,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define VF_ABI_VERSION 1
+#define VF_ABI_VERSION 2
 
 enum vf_status {
   VF_OK = 0,
@@ -81,6 +81,13 @@ typedef struct vf_settings {
   int shard_index;
   int shard_shift;
   int shard_halo; /* 1: also fuse surfaces within one block of this shard's territory */
+  /* Host swapping (EngineSettings::use_swapping / swap_buffer_blocks,
+   * pipeline.hpp:20-23; swap.hpp).  The host block store is pinned host
+   * memory mapped into the device (swap_host_blocks slots; 0 = 4 x block_count);
+   * swap_buffer_blocks <= 4096. */
+  int use_swapping;
+  int swap_buffer_blocks;
+  int swap_host_blocks;
 } vf_settings;
 
 typedef struct vf_intrinsics { /* Intrinsics (core/intrinsics.hpp:10-32) */
@@ -110,6 +117,9 @@ typedef struct vf_frame_stats {
   int error_flags;
   double pose[12];
   double ms_tracking, ms_allocation, ms_integration, ms_swapping, ms_raycast, ms_total;
+  /* SwapMetrics (swap.hpp:28-40) */
+  int swapped_in, swapped_out;
+  uint64_t swap_bytes_in, swap_bytes_out;
 } vf_frame_stats;
 
 typedef struct vf_alloc_stats { /* AllocationStats (allocation.hpp:42-47) */
@@ -205,6 +215,23 @@ int vf_depth_pyramid(vf_ctx* ctx, const float* depth_m, float* out);
 int vf_render_synthetic(int device, int n_spheres, const double* spheres, int n_planes, const double* planes,
                         const double world_to_cam[12], const vf_intrinsics* intr, double near_clip,
                         double far_clip, float* d_depth, uint8_t* d_rgb);
+
+/* --- swap engine / host block store (swap.hpp:45-253, block_store.hpp:14-53) --- */
+/* Per-entry SwapState codes (swap.hpp:19-25: 0 inactive, 1 needs_swap_in,
+ * 2 in_transfer, 3 active, 4 needs_swap_out) into out[entry_count]. */
+int vf_swap_states(vf_ctx* ctx, uint8_t* out);
+/* BlockStore::stored_count / has + read: the stored block of entry `entry` in
+ * the VoxelCodec layout (voxel.hpp:93-189; 512 x 3 B VoxelS, 512 x 7 B
+ * VoxelSRgb).  Returns 1 and fills payload (may be NULL) if stored, else 0. */
+long vf_swap_stored_count(vf_ctx* ctx);
+int vf_swap_store_read(vf_ctx* ctx, int entry, uint8_t* payload);
+/* Write every stored block to a VXBS file (make_file_block_store /
+ * load_block_store_file format, block_store.hpp:14-53): 16-byte header then
+ * (u32 entry index, payload) records, ascending entry order. */
+int vf_swap_save_store(vf_ctx* ctx, const char* path);
+/* Load a VXBS file into the host store (load_block_store_file): records for
+ * entries that are swapped out in the current table become their host data. */
+int vf_swap_load_store(vf_ctx* ctx, const char* path);
 
 /* --- spatial sharding ---
  * Owner shard of a block position (the device rule, for hosts and tests). */

@@ -28,11 +28,14 @@ STATUS_NAMES = {
 }
 
 # Every symbol include/voxfuse_b200.h declares (checked by tests/test_abi.py).
+ABI_VERSION = 2  # VF_ABI_VERSION in include/voxfuse_b200.h
+
 EXPORTS = [
     "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
     "vf_process_frame", "vf_process_frame_device", "vf_synchronize", "vf_read_stats",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
     "vf_get_surface_points", "vf_stage_forward_project", "vf_render_image",
+    "vf_swap_states", "vf_swap_stored_count", "vf_swap_store_read", "vf_swap_save_store", "vf_swap_load_store",
     "vf_entry_count", "vf_voxel_bytes", "vf_export_entries", "vf_export_voxels", "vf_export_free_stacks",
     "vf_import_state", "vf_export_visible_list", "vf_export_ranges",
     "vf_stage_allocate", "vf_stage_integrate", "vf_stage_raycast", "vf_stage_icp", "vf_icp_trace",
@@ -73,6 +76,9 @@ class VfSettings(C.Structure):
         ("shard_index", C.c_int),
         ("shard_shift", C.c_int),
         ("shard_halo", C.c_int),
+        ("use_swapping", C.c_int),
+        ("swap_buffer_blocks", C.c_int),
+        ("swap_host_blocks", C.c_int),
     ]
 
 
@@ -106,6 +112,10 @@ class VfFrameStats(C.Structure):
         ("ms_swapping", C.c_double),
         ("ms_raycast", C.c_double),
         ("ms_total", C.c_double),
+        ("swapped_in", C.c_int),
+        ("swapped_out", C.c_int),
+        ("swap_bytes_in", C.c_uint64),
+        ("swap_bytes_out", C.c_uint64),
     ]
 
 
@@ -152,6 +162,11 @@ def load() -> C.CDLL:
         "vf_set_maps": (C.c_int, [vp, vp, vp, dp]),
         "vf_volume_digest": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
         "vf_get_surface_points": (C.c_long, [vp, vp, vp, C.c_long]),
+        "vf_swap_states": (C.c_int, [vp, vp]),
+        "vf_swap_stored_count": (C.c_long, [vp]),
+        "vf_swap_store_read": (C.c_int, [vp, C.c_int, vp]),
+        "vf_swap_save_store": (C.c_int, [vp, C.c_char_p]),
+        "vf_swap_load_store": (C.c_int, [vp, C.c_char_p]),
         "vf_stage_forward_project": (C.c_int, [vp]),
         "vf_render_image": (C.c_int, [vp, C.c_int, vp]),
         "vf_entry_count": (C.c_long, [vp]),

@@ -484,37 +484,6 @@ __global__ void __launch_bounds__(256) k_alloc_apply(const float* __restrict__ d
   ctr->dropped_excess_full = dex;
 }
 
-// detail::block_projects_into_view (allocation.hpp:101-130).  Corners are
-// int * 8 (+8) in int, times the FP32 voxel size, then widened (:110-112).
-__device__ __forceinline__ bool block_projects_into_view(int bx, int by, int bz, const PoseD& w2c, const IntrD& in,
-                                                         float vs, float near_clip, float far_clip, int margin) {
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  double zmin = inf, zmax = -inf, xmin = inf, xmax = -inf, ymin = inf, ymax = -inf;
-  bool any_behind = false;
-#pragma unroll
-  for (int corner = 0; corner < 8; ++corner) {
-    const D3 w = mk((double)((float)(bx * kBlockSide + ((corner & 1) ? kBlockSide : 0)) * vs),
-                    (double)((float)(by * kBlockSide + ((corner & 2) ? kBlockSide : 0)) * vs),
-                    (double)((float)(bz * kBlockSide + ((corner & 4) ? kBlockSide : 0)) * vs));
-    const D3 cam = apply(w2c, w);
-    zmin = cam.z < zmin ? cam.z : zmin;
-    zmax = zmax < cam.z ? cam.z : zmax;
-    if (cam.z <= 1e-6) {
-      any_behind = true;
-      continue;
-    }
-    const double u = in.fx * cam.x / cam.z + in.cx;
-    const double v = in.fy * cam.y / cam.z + in.cy;
-    xmin = u < xmin ? u : xmin;
-    xmax = xmax < u ? u : xmax;
-    ymin = v < ymin ? v : ymin;
-    ymax = ymax < v ? v : ymax;
-  }
-  if (zmax <= (double)near_clip || zmin >= (double)far_clip) return false;
-  if (any_behind) return true;
-  return xmax >= -margin && xmin <= in.width - 1 + margin && ymax >= -margin && ymin <= in.height - 1 + margin;
-}
-
 // K1c: build_visible_list (allocation.hpp:216-248) over the compact list of
 // allocated entries instead of all 2.2 M table slots.  The result is the same
 // set in a different order (order is irrelevant downstream).

@@ -34,6 +34,7 @@ struct DevState {
   PoseD init_pose;  // optional ICP initial pose (vf_stage_icp)
   FrameParams fp;
   AllocMeta meta;
+  SwapCounters swap;
 };
 
 PoseD pose_from(const double* p) {
@@ -123,6 +124,11 @@ struct vf_ctx {
   int surf_cap = 0, surf_tiles = 0;
   uint8_t* image = nullptr;  // get_image output (w*h*3) + depth-max word
   int* image_dmax = nullptr;
+  // swap engine (vf_swap.cu): device arrays + the pinned, mapped host store
+  bool swapping = false;
+  SwapDev sw{};
+  uint32_t* host_pool = nullptr;  // host pointer of sw.host_pool
+  int host_cap = 0;
 
   // host state
   DevState* hstate = nullptr;  // pinned
@@ -325,7 +331,23 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   stage_mark(c, 3);
   if (fork) {
     VF_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0));
-  } else {
+  }
+  if (c->swapping) {
+    // request_swap_ins/outs + execute_swap_in/out (pipeline_impl.hpp:104-113)
+    k_swap_request<<<c->num_sms * 4, 256, 0, st>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
+                                                   s.near_clip, s.far_clip, s.visibility_margin_px, s.swap_margin_px,
+                                                   c->sw, &c->dstate->ctr);
+    VF_LAUNCHED(c, "k_swap_request");
+    k_swap_select<<<1, 1024, 0, st>>>(c->entries, c->vba_slots, c->sw, s.swap_buffer_blocks,
+                                      (c->vsize == 8 ? 7 : 3) * kBlockVolume, &c->dstate->ctr);
+    VF_LAUNCHED(c, "k_swap_select");
+    k_swap_transfer<<<c->num_sms * 2, 256, 0, st>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
+                                                    s.max_weight);
+    VF_LAUNCHED(c, "k_swap_transfer");
+    launches += 3;
+  }
+  stage_mark(c, 4);
+  if (!fork) {
     k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
                                              s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
   }
@@ -349,7 +371,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     VF_LAUNCHED(c, "k_forward_project");
     ++launches;
   }
-  stage_mark(c, 4);
+  stage_mark(c, 5);
   c->launches_last = launches;
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
@@ -405,6 +427,10 @@ void fill_stats(vf_ctx* c, bool tracked, int frame_index, vf_frame_stats* st) {
   st->visible_blocks = h.ctr.visible_count;
   st->allocated_total = c->s.block_count - h.ctr.vba_top;
   st->error_flags = h.ctr.error_flags;
+  st->swapped_in = h.swap.swapped_in;
+  st->swapped_out = h.swap.swapped_out;
+  st->swap_bytes_in = h.swap.bytes_in;
+  st->swap_bytes_out = h.swap.bytes_out;
   pose_to(h.pose, st->pose);
 }
 
@@ -429,7 +455,7 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
   ++c->frame;
   if (c->profiling) {
     VF_CUDA(c, cudaStreamSynchronize(c->stream));
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 5; ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
       c->stage_ms[i] += ms;
@@ -462,10 +488,13 @@ void free_all(vf_ctx* c) {
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list, c->req_marked,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
                   c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
-                  c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax};
+                  c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax,
+                  c->sw.state, c->sw.host_slot, c->sw.host_free, c->sw.in_cand, c->sw.out_cand,
+                  c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
+  if (c->host_pool) cudaFreeHost(c->host_pool);
   if (c->hpose) cudaFreeHost(c->hpose);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -476,6 +505,8 @@ void free_all(vf_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
+
+int reset_swap(vf_ctx* c);
 
 int reset_volume(vf_ctx* c) {
   // HashVolume(HashConfig) (hash_volume.hpp:133-140): all entries unallocated,
@@ -503,10 +534,26 @@ int reset_volume(vf_ctx* c) {
   VF_CUDA(c, cudaMemcpy(c->dstate, &ds, sizeof(ds), cudaMemcpyHostToDevice));
   VF_CUDA(c, cudaMemset(c->points, 0, sizeof(float4) * c->npix));
   VF_CUDA(c, cudaMemset(c->normals, 0, sizeof(float4) * c->npix));
+  if (int rc = reset_swap(c)) return rc;
   VF_CUDA(c, cudaStreamSynchronize(c->stream));
   VF_CUDA(c, cudaGetLastError());
   c->frame = 0;
   c->maps_valid = false;
+  return VF_OK;
+}
+
+// Empty host store, every entry inactive (GlobalCache constructor, swap.hpp:48-52).
+int reset_swap(vf_ctx* c) {
+  if (!c->swapping) return VF_OK;
+  VF_CUDA(c, cudaMemset(c->sw.state, 0, (size_t)c->entry_count));
+  VF_CUDA(c, cudaMemset(c->sw.host_slot, 0xFF, sizeof(int) * (size_t)c->entry_count));
+  std::vector<int> iota((size_t)c->host_cap);
+  for (int i = 0; i < c->host_cap; ++i) iota[(size_t)i] = c->host_cap - 1 - i;  // pops hand out 0, 1, 2, ...
+  VF_CUDA(c, cudaMemcpy(c->sw.host_free, iota.data(), sizeof(int) * iota.size(), cudaMemcpyHostToDevice));
+  SwapCounters sc;
+  std::memset(&sc, 0, sizeof(sc));
+  sc.host_top = c->host_cap;
+  VF_CUDA(c, cudaMemcpy(&c->dstate->swap, &sc, sizeof(sc), cudaMemcpyHostToDevice));
   return VF_OK;
 }
 
@@ -561,6 +608,9 @@ void vf_default_settings(vf_settings* s) {
   s->shard_index = 0;
   s->shard_shift = 3;
   s->shard_halo = 1;
+  s->use_swapping = 0;  // pipeline.hpp:20-23
+  s->swap_buffer_blocks = 100;
+  s->swap_host_blocks = 0;
 }
 
 int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out) {
@@ -595,6 +645,17 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     return VF_ERR_CUDA;
   }
   c->vsize = s->voxel_type == VF_VOXEL_S_RGB ? 8 : 4;
+  if (s->use_swapping) {
+    const long entries = (long)s->bucket_count * s->bucket_size + s->excess_count;
+    if (s->swap_buffer_blocks < 1 || s->swap_buffer_blocks > kSwapSortCap || s->swap_host_blocks < 0 ||
+        entries >= (1L << 24)) {
+      free_all(c);
+      delete c;
+      return VF_ERR_INVALID;
+    }
+    c->swapping = true;
+    c->host_cap = s->swap_host_blocks > 0 ? s->swap_host_blocks : 4 * s->block_count;
+  }
   if (s->shard_count > 1) {
     if (s->shard_count > kMaxShards || s->shard_index < 0 || s->shard_index >= s->shard_count || s->shard_shift < 0 ||
         s->shard_shift > 8) {
@@ -705,7 +766,16 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->surf_points, sizeof(float) * 3 * (size_t)c->surf_cap)) ||
       (rc = dalloc(c, &c->surf_colors, sizeof(float) * 3 * (size_t)c->surf_cap)) ||
       (rc = dalloc(c, &c->surf_scan, sizeof(unsigned long long) * (1 + (size_t)c->surf_tiles))) ||
-      (rc = dalloc(c, &c->image, 3 * (size_t)c->npix)) || (rc = dalloc(c, &c->image_dmax, sizeof(int)))) {
+      (rc = dalloc(c, &c->image, 3 * (size_t)c->npix)) || (rc = dalloc(c, &c->image_dmax, sizeof(int))) ||
+      (c->swapping &&
+       ((rc = dalloc(c, &c->sw.state, (size_t)c->entry_count)) ||
+        (rc = dalloc(c, &c->sw.host_slot, sizeof(int) * (size_t)c->entry_count)) ||
+        (rc = dalloc(c, &c->sw.host_free, sizeof(int) * (size_t)c->host_cap)) ||
+        (rc = dalloc(c, &c->sw.in_cand, sizeof(int) * (size_t)c->entry_count)) ||
+        (rc = dalloc(c, &c->sw.out_cand, sizeof(int) * (size_t)c->entry_count)) ||
+        (rc = dalloc(c, &c->sw.stage_entry, sizeof(int) * 2 * kSwapSortCap)) ||
+        (rc = dalloc(c, &c->sw.stage_slot, sizeof(int) * 2 * kSwapSortCap)) ||
+        (rc = dalloc(c, &c->sw.stage_host, sizeof(int) * 2 * kSwapSortCap))))) {
     free_all(c);
     delete c;
     return rc;
@@ -715,6 +785,22 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     free_all(c);
     delete c;
     return VF_ERR_CUDA;
+  }
+  if (c->swapping) {
+    // host block store: pinned, mapped into the device address space (UVA)
+    const size_t bytes = (size_t)c->host_cap * kBlockVolume * (size_t)c->vsize;
+    void* dp = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&c->host_pool), bytes, cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess ||
+        cudaHostGetDevicePointer(&dp, c->host_pool, 0) != cudaSuccess) {
+      std::fprintf(stderr, "[voxfuse_b200] cannot allocate the %zu-byte pinned host block store\n", bytes);
+      c->host_pool = nullptr;
+      free_all(c);
+      delete c;
+      return VF_ERR_CUDA;
+    }
+    c->sw.host_pool = reinterpret_cast<uint32_t*>(dp);
+    c->sw.ctr = &c->dstate->swap;
   }
   if (cudaMallocHost(reinterpret_cast<void**>(&c->hstate), sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->hpose), sizeof(PoseD)) != cudaSuccess) {
@@ -853,6 +939,178 @@ int vf_render_image(vf_ctx* c, int mode, uint8_t* out) {
   return VF_OK;
 }
 
+// --- swap engine: host store access (block_store.hpp / block_store.cpp) ---
+namespace {
+constexpr uint32_t kVxbsMagic = 0x53425856u;  // 'VXBS' (block_store.hpp:41)
+constexpr uint16_t kVxbsVersion = 1;
+int codec_bytes(const vf_ctx* c) { return c->vsize == 8 ? 7 : 3; }
+// VoxelCodec::encode / decode (voxel.hpp:124-155) on device-layout words
+void encode_block(const vf_ctx* c, const uint32_t* words, uint8_t* out) {
+  const int cb = codec_bytes(c);
+  for (int v = 0; v < kBlockVolume; ++v) {
+    const uint32_t w0 = words[v * (c->vsize / 4)];
+    uint8_t* p = out + (size_t)v * cb;
+    p[0] = (uint8_t)(w0 & 0xFF);
+    p[1] = (uint8_t)((w0 >> 8) & 0xFF);
+    p[2] = (uint8_t)((w0 >> 16) & 0xFF);
+    if (c->vsize == 8) {
+      const uint32_t w1 = words[v * 2 + 1];
+      p[3] = (uint8_t)(w0 >> 24);
+      p[4] = (uint8_t)(w1 & 0xFF);
+      p[5] = (uint8_t)((w1 >> 8) & 0xFF);
+      p[6] = (uint8_t)((w1 >> 16) & 0xFF);
+    }
+  }
+}
+void decode_block(const vf_ctx* c, const uint8_t* in, uint32_t* words) {
+  const int cb = codec_bytes(c);
+  for (int v = 0; v < kBlockVolume; ++v) {
+    const uint8_t* p = in + (size_t)v * cb;
+    if (c->vsize == 8) {
+      words[v * 2] = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+      words[v * 2 + 1] = (uint32_t)p[4] | ((uint32_t)p[5] << 8) | ((uint32_t)p[6] << 16);
+    } else {
+      words[v] = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
+    }
+  }
+}
+void put_u16(uint8_t* p, uint16_t v) {
+  p[0] = (uint8_t)(v & 0xFF);
+  p[1] = (uint8_t)(v >> 8);
+}
+void put_u32(uint8_t* p, uint32_t v) {
+  for (int i = 0; i < 4; ++i) p[i] = (uint8_t)((v >> (8 * i)) & 0xFF);
+}
+uint32_t get_u32(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+}  // namespace
+
+int vf_swap_states(vf_ctx* c, uint8_t* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  if (!c->swapping) return VF_ERR_STATE;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(out, c->sw.state, (size_t)c->entry_count, cudaMemcpyDeviceToHost));
+  return VF_OK;
+}
+
+long vf_swap_stored_count(vf_ctx* c) {
+  if (!c) return VF_ERR_INVALID;
+  if (!c->swapping) return 0;
+  if (int rc = read_state(c)) return rc;
+  return (long)c->host_cap - c->hstate->swap.host_top;
+}
+
+int vf_swap_store_read(vf_ctx* c, int entry, uint8_t* payload) {
+  if (!c || entry < 0 || entry >= c->entry_count) return VF_ERR_INVALID;
+  if (!c->swapping) return 0;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  int hs = -1;
+  VF_CUDA(c, cudaMemcpy(&hs, c->sw.host_slot + entry, sizeof(int), cudaMemcpyDeviceToHost));
+  if (hs < 0) return 0;
+  if (payload) encode_block(c, c->host_pool + (size_t)hs * kBlockVolume * (c->vsize / 4), payload);
+  return 1;
+}
+
+int vf_swap_save_store(vf_ctx* c, const char* path) {
+  if (!c || !path) return VF_ERR_INVALID;
+  if (!c->swapping) return VF_ERR_STATE;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  std::vector<int> hs((size_t)c->entry_count);
+  VF_CUDA(c, cudaMemcpy(hs.data(), c->sw.host_slot, sizeof(int) * hs.size(), cudaMemcpyDeviceToHost));
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    c->err = std::string("cannot create block store file: ") + path;
+    return VF_ERR_INVALID;
+  }
+  const int payload = codec_bytes(c) * kBlockVolume;
+  uint8_t header[16] = {};
+  put_u32(header, kVxbsMagic);
+  put_u16(header + 4, kVxbsVersion);
+  put_u16(header + 6, (uint16_t)(c->vsize == 8 ? VF_VOXEL_S_RGB : VF_VOXEL_S));  // VoxelType tag (voxel.hpp:90)
+  put_u32(header + 8, (uint32_t)c->entry_count);
+  put_u32(header + 12, (uint32_t)payload);
+  bool ok = std::fwrite(header, 1, 16, f) == 16;
+  std::vector<uint8_t> rec((size_t)payload + 4);
+  for (int i = 0; ok && i < c->entry_count; ++i) {
+    if (hs[(size_t)i] < 0) continue;
+    put_u32(rec.data(), (uint32_t)i);
+    encode_block(c, c->host_pool + (size_t)hs[(size_t)i] * kBlockVolume * (c->vsize / 4), rec.data() + 4);
+    ok = std::fwrite(rec.data(), 1, rec.size(), f) == rec.size();
+  }
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) {
+    c->err = std::string("short write to block store file: ") + path;
+    return VF_ERR_INVALID;
+  }
+  return VF_OK;
+}
+
+int vf_swap_load_store(vf_ctx* c, const char* path) {
+  if (!c || !path) return VF_ERR_INVALID;
+  if (!c->swapping) return VF_ERR_STATE;
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) {
+    c->err = std::string("cannot open block store file: ") + path;
+    return VF_ERR_INVALID;
+  }
+  uint8_t header[16];
+  const int payload = codec_bytes(c) * kBlockVolume;
+  const uint16_t tag = (uint16_t)(c->vsize == 8 ? VF_VOXEL_S_RGB : VF_VOXEL_S);
+  if (std::fread(header, 1, 16, f) != 16 || get_u32(header) != kVxbsMagic ||
+      (uint16_t)(header[4] | (header[5] << 8)) != kVxbsVersion || (uint16_t)(header[6] | (header[7] << 8)) != tag ||
+      get_u32(header + 8) != (uint32_t)c->entry_count || get_u32(header + 12) != (uint32_t)payload) {
+    std::fclose(f);
+    c->err = std::string("not a compatible block store file: ") + path;
+    return VF_ERR_INVALID;
+  }
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (int rc = read_state(c)) {
+    std::fclose(f);
+    return rc;
+  }
+  std::vector<int> hs((size_t)c->entry_count), hfree((size_t)c->host_cap);
+  std::vector<HashEntry> ents((size_t)c->entry_count);
+  cudaMemcpy(hs.data(), c->sw.host_slot, sizeof(int) * hs.size(), cudaMemcpyDeviceToHost);
+  cudaMemcpy(hfree.data(), c->sw.host_free, sizeof(int) * hfree.size(), cudaMemcpyDeviceToHost);
+  cudaMemcpy(ents.data(), c->entries, sizeof(HashEntry) * ents.size(), cudaMemcpyDeviceToHost);
+  int top = c->hstate->swap.host_top;
+  std::vector<uint8_t> rec((size_t)payload + 4);
+  int rc = VF_OK;
+  for (;;) {
+    const size_t got = std::fread(rec.data(), 1, rec.size(), f);
+    if (got == 0) break;
+    if (got != rec.size()) {
+      rc = VF_ERR_INVALID;
+      c->err = "truncated block store record";
+      break;
+    }
+    const uint32_t idx = get_u32(rec.data());
+    if (idx >= (uint32_t)c->entry_count) {
+      rc = VF_ERR_INVALID;
+      c->err = "block store record index out of range";
+      break;
+    }
+    // only swapped-out entries can ever be paged back in (swap.hpp:145)
+    if (ents[idx].block_state != kEntrySwappedOut) continue;
+    int slot = hs[idx];
+    if (slot < 0) {
+      if (top == 0) {
+        rc = VF_ERR_OVERFLOW;
+        c->err = "host block store full";
+        break;
+      }
+      slot = hfree[(size_t)--top];
+      hs[idx] = slot;
+    }
+    decode_block(c, rec.data() + 4, c->host_pool + (size_t)slot * kBlockVolume * (c->vsize / 4));
+  }
+  std::fclose(f);
+  VF_CUDA(c, cudaMemcpy(c->sw.host_slot, hs.data(), sizeof(int) * hs.size(), cudaMemcpyHostToDevice));
+  VF_CUDA(c, cudaMemcpy(&c->dstate->swap.host_top, &top, sizeof(int), cudaMemcpyHostToDevice));
+  return rc;
+}
+
 long vf_entry_count(const vf_ctx* c) { return c ? c->entry_count : -1; }
 long vf_voxel_bytes(const vf_ctx* c) { return c ? (long)c->s.block_count * kBlockVolume * c->vsize : -1; }
 
@@ -898,6 +1156,7 @@ int vf_import_state(vf_ctx* c, const void* entries, const void* voxels, int vba_
   k_rebuild_alloc_list<<<c->num_sms * 4, 256, 0, c->stream>>>(c->entries, c->entry_count, c->alloc_list, c->alloc_cap,
                                                               &c->dstate->ctr);
   VF_CUDA(c, cudaGetLastError());
+  if (int rc = reset_swap(c)) return rc;  // imported tables come without host data
   VF_CUDA(c, cudaStreamSynchronize(c->stream));
   return VF_OK;
 }
@@ -1221,7 +1480,8 @@ long vf_last_modified_voxels(vf_ctx* c) {
 int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
   if (!c) return VF_ERR_INVALID;
   int icp = 1 + ((c->icp_cluster && c->icp_coarse_levels > 0 && c->icp_coarse_levels < c->s.hierarchy_levels) ? 1 : 0);
-  return 7 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 1 : 0) + icp : 0) + (c->nccl_comm ? 2 : 0);
+  return 7 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 1 : 0) + icp : 0) + (c->nccl_comm ? 2 : 0) +
+         (c->vsize == 8 ? 1 : 0) + (c->swapping ? 3 : 0);
 }
 
 }  // extern "C"

@@ -124,6 +124,35 @@ __global__ void k_colourize_depth(const float* depth, int n, const int* dmax_bit
 constexpr int kSurfaceStride = 4;  // pipeline_impl.hpp:219
 constexpr int kFpTileItems = 256;
 
+// swap engine (vf_swap.cu)
+constexpr int kSwapSortCap = 4096;  // max swap_buffer_blocks
+struct SwapCounters {
+  int host_top;  // free host-store slots
+  int n_in_cand, n_out_cand;
+  int staged_in, staged_out;
+  int swapped_in, swapped_out;  // SwapMetrics (swap.hpp:28-40) of the last frame
+  int pad;
+  unsigned long long bytes_in, bytes_out;
+};
+struct SwapDev {
+  uint8_t* state;     // SwapState per entry (swap.hpp:19-25)
+  int* host_slot;     // entry -> host-store slot, -1: no stored data (BlockStore::has)
+  int* host_free;     // free host slots (stack)
+  int* in_cand;       // this frame's needs_swap_in / needs_swap_out entries
+  int* out_cand;
+  int* stage_entry;   // staged transfers: swap-ins first, then swap-outs
+  int* stage_slot;
+  int* stage_host;
+  uint32_t* host_pool;  // pinned, device-mapped: slot * 512 device-layout voxels
+  SwapCounters* ctr;
+};
+__global__ void k_swap_request(const HashEntry* entries, const int* alloc_list, const FrameParams* fp, IntrD in,
+                               float vs, float near_clip, float far_clip, int margin, int swap_margin, SwapDev sw,
+                               Counters* ctr);
+__global__ void k_swap_select(HashEntry* entries, int* vba_slots, SwapDev sw, int buffer_blocks, int payload_bytes,
+                              Counters* ctr);
+__global__ void k_swap_transfer(uint32_t* voxels, int words_per_voxel, SwapDev sw, int max_weight);
+
 constexpr int kMaxShards = 16;
 struct ShardGroupArgs {
   int n;

@@ -99,6 +99,9 @@ class EngineSettings:
     shard_index: int = 0   # ... this context's shard ...
     shard_shift: int = 3   # ... owning super-blocks of 2^shift blocks per axis
     shard_halo: bool = True  # ... and fusing surfaces within one block of them
+    use_swapping: bool = False  # host swapping (pipeline.hpp:20-23, swap.hpp)
+    swap_buffer_blocks: int = 100
+    swap_host_blocks: int = 0  # host store slots (0: 4 x block_count)
 
     def to_c(self) -> VfSettings:
         s = VfSettings()
@@ -123,6 +126,7 @@ def settings_from_config(cfg) -> tuple[EngineSettings, Calibration]:
         rotation_only_levels=cfg.rotation_only_levels, max_iterations=cfg.max_iterations,
         min_valid_points=cfg.min_valid_points, icp_dist_threshold=cfg.icp_dist_threshold,
         convergence_eps=cfg.convergence_eps, max_condition=cfg.max_condition, tracking=cfg.tracking,
+        use_swapping=getattr(cfg, "use_swapping", False), swap_buffer_blocks=getattr(cfg, "swap_buffer_blocks", 100),
     )
     intr = Intrinsics(fx, fy, cx, cy, w, h)
     return s, Calibration(depth=intr, rgb=intr)
@@ -145,12 +149,17 @@ class FrameStats:
     allocated_total: int = 0
     tracking_valid_points: int = 0
     error_flags: int = 0
+    swapped_in: int = 0  # SwapMetrics (swap.hpp:28-40)
+    swapped_out: int = 0
+    bytes_in: int = 0
+    bytes_out: int = 0
 
     @classmethod
     def from_c(cls, s: VfFrameStats) -> "FrameStats":
         return cls(s.frame, bool(s.tracking_ok), s.tracking_iterations, s.tracking_cost, s.blocks_allocated,
                    s.allocation_dropped, s.visible_blocks, np.array(s.pose[:]), s.ms_total, s.allocation_requested,
-                   s.allocated_total, s.tracking_valid_points, s.error_flags)
+                   s.allocated_total, s.tracking_valid_points, s.error_flags, s.swapped_in, s.swapped_out,
+                   s.swap_bytes_in, s.swap_bytes_out)
 
 
 def _ptr(a):
@@ -261,6 +270,41 @@ class Pipeline:
         rp = _pose(render_pose)
         self._chk("vf_set_maps", self._L.vf_set_maps(self._h, _ptr(p), _ptr(n),
                                                      rp.ctypes.data_as(C.POINTER(C.c_double))))
+
+    # -- swap engine (swap.hpp) --
+    def swap_states(self) -> np.ndarray:
+        """Per-entry SwapState codes (swap.hpp:19-25)."""
+        out = np.zeros(self._settings.entry_count, np.uint8)
+        self._chk("vf_swap_states", self._L.vf_swap_states(self._h, _ptr(out)))
+        return out
+
+    def store_count(self) -> int:
+        """BlockStore::stored_count (block_store.hpp:34-38)."""
+        return int(self._chk("vf_swap_stored_count", self._L.vf_swap_stored_count(self._h)))
+
+    def store_read(self, entry: int):
+        """BlockStore::read of one entry (VoxelCodec bytes), or None when not stored."""
+        payload = np.zeros(512 * (7 if self._settings.voxel_type == VOXEL_TYPE_S_RGB else 3), np.uint8)
+        rc = self._chk("vf_swap_store_read", self._L.vf_swap_store_read(self._h, int(entry), _ptr(payload)))
+        return payload if rc == 1 else None
+
+    def store(self) -> dict:
+        """{entry index: payload} for every stored block."""
+        e = self.entries()
+        out = {}
+        for i in np.nonzero(e["block_state"] == -1)[0]:
+            p = self.store_read(int(i))
+            if p is not None:
+                out[int(i)] = p
+        return out
+
+    def save_store(self, path: str) -> None:
+        """Write the host store as a VXBS file (block_store.hpp:14-53)."""
+        self._chk("vf_swap_save_store", self._L.vf_swap_save_store(self._h, str(path).encode()))
+
+    def load_store(self, path: str) -> None:
+        """load_block_store_file into the host store (block_store.cpp:143-181)."""
+        self._chk("vf_swap_load_store", self._L.vf_swap_load_store(self._h, str(path).encode()))
 
     def surface_points(self):
         """TrackingState::surface_points / surface_colors (tracking_state.hpp:30-31):

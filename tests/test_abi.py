@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     L = _abi.load()
     missing = [n for n in declared() if not hasattr(L, n)]
     assert not missing, f"not exported: {missing}"
-    assert L.vf_abi_version() == 1
+    assert L.vf_abi_version() == _abi.ABI_VERSION
 
 
 def test_struct_layouts_match_the_c_abi():
