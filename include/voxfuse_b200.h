@@ -88,6 +88,7 @@ typedef struct vf_settings {
   int use_swapping;
   int swap_buffer_blocks;
   int swap_host_blocks;
+  float max_depth; /* disparity conversion clamp, metres (EngineSettings::max_depth, pipeline.hpp:37) */
 } vf_settings;
 
 typedef struct vf_intrinsics { /* Intrinsics (core/intrinsics.hpp:10-32) */
@@ -146,6 +147,17 @@ int vf_process_frame(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb, vf_f
  * device pointers).  stats may be NULL: then nothing is read back and the call
  * does not synchronise. */
 int vf_process_frame_device(vf_ctx* ctx, const float* d_depth, const uint8_t* d_rgb, vf_frame_stats* stats);
+/* IPipeline::process_raw_frame (pipeline.hpp:71, pipeline_impl.hpp:59-62):
+ * a raw 16-bit disparity frame, converted on the device by
+ * disparity_image_to_depth (view.hpp:18-28) with the calibration's a, b and
+ * depth fx and settings.max_depth.  big_endian != 0: the buffer holds the raw
+ * bytes of a 16-bit P5 raster (read_pgm16, src/pnm.cpp:63-73). */
+int vf_process_raw_frame(vf_ctx* ctx, const uint16_t* disparity, const uint8_t* rgb, int big_endian,
+                         vf_frame_stats* stats);
+int vf_process_raw_frame_device(vf_ctx* ctx, const uint16_t* d_disparity, const uint8_t* d_rgb, int big_endian,
+                                vf_frame_stats* stats);
+/* disparity_image_to_depth alone (stage entry point): width*height floats out. */
+int vf_disparity_to_depth(vf_ctx* ctx, const uint16_t* disparity, int big_endian, float* depth_out);
 int vf_synchronize(vf_ctx* ctx);
 int vf_read_stats(vf_ctx* ctx, vf_frame_stats* stats);
 

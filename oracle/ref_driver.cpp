@@ -443,6 +443,18 @@ long vfr_store_count(void* ctx) {
   auto f = [&](const auto& c) -> long { return c.store().stored_count(); };
   return b->voxel_type() == 2 ? with_cache<VoxelSRgb>(b, f) : with_cache<VoxelS>(b, f);
 }
+// disparity_image_to_depth through the reference's own Calibration (view.hpp:18-28)
+void vfr_disparity_to_depth(const std::uint16_t* disp, int w, int h, double a, double b, double fx,
+                            float max_depth, float* depth) {
+  Image2D<std::uint16_t> img(w, h);
+  std::memcpy(img.pixels().data(), disp, sizeof(std::uint16_t) * static_cast<std::size_t>(w) * h);
+  Calibration k;
+  k.depth.fx = fx;
+  k.disparity.a = a;
+  k.disparity.b = b;
+  const Image2D<float> d = disparity_image_to_depth(img, k, max_depth);
+  std::memcpy(depth, d.pixels().data(), sizeof(float) * static_cast<std::size_t>(w) * h);
+}
 std::uint64_t vfr_digest(void* ctx) { return static_cast<CtxBase*>(ctx)->digest(); }
 long vfr_allocated_blocks(void* ctx) { return static_cast<CtxBase*>(ctx)->allocated_blocks(); }
 

@@ -1191,6 +1191,22 @@ long vfo_store_count(const vfo_ctx* c) {
   return n;
 }
 
+/* disparity_to_depth (io/calibration.hpp:45-60) over an image
+ * (disparity_image_to_depth, engine/view.hpp:18-28) */
+void vfo_disparity_to_depth(const uint16_t* disp, long n, double a, double b, double fx, float max_depth,
+                            float* depth) {
+  const float fa = (float)a, fb = (float)b, ffx = (float)fx;
+  for (long i = 0; i < n; ++i) {
+    const float denom = fa - (float)disp[i];
+    if (denom <= 0.0f) {
+      depth[i] = 0.0f;
+      continue;
+    }
+    const float z = 8.0f * fb * ffx / denom;
+    depth[i] = (z > 0.0f && z <= max_depth) ? z : 0.0f;
+  }
+}
+
 /* Pipeline::colourize_depth (pipeline_impl.hpp:225-239) */
 void vfo_colourize_depth(const float* depth, int w, int h, uint8_t* out) {
   const size_t n = (size_t)w * h;

@@ -99,6 +99,9 @@ long vfo_surface_points(const vfo_ctx* c, float* points, float* colors);
 int vfo_stage_forward_project(vfo_ctx* c);
 int vfo_render_image(vfo_ctx* c, int color, uint8_t* out);
 void vfo_colourize_depth(const float* depth, int w, int h, uint8_t* out);
+/* disparity_image_to_depth (view.hpp:18-28, calibration.hpp:45-60) */
+void vfo_disparity_to_depth(const uint16_t* disp, long n, double a, double b, double fx, float max_depth,
+                            float* depth);
 /* swap engine (swap.hpp:14-253): per-entry SwapState codes (inactive 0,
  * needs_swap_in 1, in_transfer 2, active 3, needs_swap_out 4); host store
  * contents in the VoxelCodec layout (voxel.hpp:93-189, 3 / 7 bytes per voxel):

@@ -398,6 +398,22 @@ def colourize_depth(depth: np.ndarray) -> np.ndarray:
     return out
 
 
+def disparity_to_depth(lib: _Lib, disp: np.ndarray, a: float, b: float, fx: float, max_depth: float = 8.0):
+    """disparity_image_to_depth: oracle (vfo_) or reference (vfr_)."""
+    disp = np.ascontiguousarray(disp, dtype=np.uint16)
+    out = np.zeros(disp.shape, np.float32)
+    vp = C.c_void_p
+    if lib.prefix == "vfo_":
+        f = lib.lib.vfo_disparity_to_depth
+        f.argtypes = [vp, C.c_long, C.c_double, C.c_double, C.c_double, C.c_float, vp]
+        f(disp.ctypes.data_as(vp), disp.size, a, b, fx, max_depth, out.ctypes.data_as(vp))
+    else:
+        f = lib.lib.vfr_disparity_to_depth
+        f.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_float, vp]
+        f(disp.ctypes.data_as(vp), disp.shape[1], disp.shape[0], a, b, fx, max_depth, out.ctypes.data_as(vp))
+    return out
+
+
 def depth_pyramid(lib: _Lib, depth: np.ndarray, levels: int) -> list:
     h, w = depth.shape
     sizes = []

@@ -33,6 +33,7 @@ ABI_VERSION = 2  # VF_ABI_VERSION in include/voxfuse_b200.h
 EXPORTS = [
     "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
     "vf_process_frame", "vf_process_frame_device", "vf_synchronize", "vf_read_stats",
+    "vf_process_raw_frame", "vf_process_raw_frame_device", "vf_disparity_to_depth",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
     "vf_get_surface_points", "vf_stage_forward_project", "vf_render_image",
     "vf_swap_states", "vf_swap_stored_count", "vf_swap_store_read", "vf_swap_save_store", "vf_swap_load_store",
@@ -79,6 +80,7 @@ class VfSettings(C.Structure):
         ("use_swapping", C.c_int),
         ("swap_buffer_blocks", C.c_int),
         ("swap_host_blocks", C.c_int),
+        ("max_depth", C.c_float),
     ]
 
 
@@ -154,6 +156,9 @@ def load() -> C.CDLL:
         "vf_process_frame": (C.c_int, [vp, vp, vp, C.POINTER(VfFrameStats)]),
         "vf_process_frame_device": (C.c_int, [vp, vp, vp, C.POINTER(VfFrameStats)]),
         "vf_synchronize": (C.c_int, [vp]),
+        "vf_process_raw_frame": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(VfFrameStats)]),
+        "vf_process_raw_frame_device": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(VfFrameStats)]),
+        "vf_disparity_to_depth": (C.c_int, [vp, vp, C.c_int, vp]),
         "vf_read_stats": (C.c_int, [vp, C.POINTER(VfFrameStats)]),
         "vf_set_pose": (C.c_int, [vp, dp]),
         "vf_get_pose": (C.c_int, [vp, dp]),

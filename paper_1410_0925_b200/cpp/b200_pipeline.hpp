@@ -14,8 +14,9 @@
 // meaning; construction errors are reported with the reference's exception
 // type (std::invalid_argument, pipeline_impl.hpp:55-57), runtime CUDA errors
 // as std::runtime_error.  Scope: hash backend, VoxelS /
-// VoxelSRgb, ICP tracker; the dense backend, float voxels, the colour / Ren
-// trackers and swapping raise std::invalid_argument.
+// VoxelSRgb, ICP tracker, host swapping, raw disparity input; the dense
+// backend, float voxels and the colour / Ren trackers raise
+// std::invalid_argument.
 #pragma once
 
 #include <cstdint>
@@ -77,7 +78,6 @@ inline vf_settings to_vf_settings(const voxfuse::EngineSettings& s) {
     throw std::invalid_argument("voxfuse_b200: voxel types VoxelS and VoxelSRgb only");
   if (s.tracker.type != TrackerType::icp)
     throw std::invalid_argument("voxfuse_b200: only the ICP depth tracker is implemented");
-  if (s.use_swapping) throw std::invalid_argument("voxfuse_b200: host swapping is not implemented yet");
   vf_settings c;
   vf_default_settings(&c);
   c.voxel_type = s.voxel_type == VoxelType::s_rgb ? VF_VOXEL_S_RGB : VF_VOXEL_S;
@@ -102,6 +102,9 @@ inline vf_settings to_vf_settings(const voxfuse::EngineSettings& s) {
   c.max_condition = s.tracker.max_condition;
   c.tracking = 1;
   c.use_graphs = 1;
+  c.use_swapping = s.use_swapping ? 1 : 0;  // swap.hpp; host store in pinned, device-mapped memory
+  c.swap_buffer_blocks = s.swap_buffer_blocks;
+  c.max_depth = s.max_depth;
   return c;
 }
 
@@ -123,6 +126,11 @@ class B200Pipeline final : public voxfuse::IPipeline {
     detail::check(rc, "vf_create", nullptr);
   }
   ~B200Pipeline() override {
+    // swap_store_path (pipeline.hpp:23): the reference streams records into a
+    // VXBS file as blocks leave; the GPU store lives in pinned memory and is
+    // written to the same format when the pipeline is destroyed.
+    if (ctx_ && settings_.use_swapping && !settings_.swap_store_path.empty())
+      vf_swap_save_store(ctx_, settings_.swap_store_path.c_str());
     if (ctx_) vf_destroy(ctx_);
   }
   B200Pipeline(const B200Pipeline&) = delete;
@@ -141,6 +149,11 @@ class B200Pipeline final : public voxfuse::IPipeline {
     vf_frame_stats st;
     detail::check(vf_process_frame(ctx_, depth_m.pixels().data(), rgb_ptr, &st), "vf_process_frame", ctx_);
     if (rgb) last_rgb_ = *rgb;
+    return finish_frame(st);
+  }
+
+ private:
+  voxfuse::FrameStats finish_frame(const vf_frame_stats& st) {
     pose_ = detail::pose_from_array(st.pose);
     maps_stale_ = true;
     voxfuse::FrameStats fs;
@@ -152,15 +165,30 @@ class B200Pipeline final : public voxfuse::IPipeline {
     fs.allocation_dropped = st.allocation_dropped;
     fs.visible_blocks = st.visible_blocks;
     fs.pose = pose_;
+    fs.swap.swapped_in = st.swapped_in;
+    fs.swap.swapped_out = st.swapped_out;
+    fs.swap.bytes_in = st.swap_bytes_in;
+    fs.swap.bytes_out = st.swap_bytes_out;
     fs.ms_total = st.ms_total;  // GPU time of the frame (CUDA events)
     return fs;
   }
 
-  // IPipeline::process_raw_frame (pipeline_impl.hpp:48-51): disparity -> depth
-  // with the reference's own conversion, then the GPU frame.
+ public:
+  // IPipeline::process_raw_frame (pipeline_impl.hpp:59-62): the u16
+  // disparity goes up (half the bytes of a float depth map) and
+  // disparity_image_to_depth runs on the device.
   voxfuse::FrameStats process_raw_frame(const voxfuse::Image2D<voxfuse::Vec3u8>* rgb,
                                         const voxfuse::Image2D<std::uint16_t>& disparity) override {
-    return process_frame(rgb, voxfuse::disparity_image_to_depth(disparity, calib_, settings_.max_depth));
+    if (disparity.width() != calib_.depth.width || disparity.height() != calib_.depth.height)
+      throw std::invalid_argument("voxfuse_b200: disparity image size does not match the calibration");
+    const std::uint8_t* rgb_ptr = nullptr;
+    if (rgb && !rgb->empty() && settings_.voxel_type == voxfuse::VoxelType::s_rgb)
+      rgb_ptr = reinterpret_cast<const std::uint8_t*>(rgb->pixels().data());
+    vf_frame_stats st;
+    detail::check(vf_process_raw_frame(ctx_, disparity.pixels().data(), rgb_ptr, 0, &st), "vf_process_raw_frame",
+                  ctx_);
+    if (rgb) last_rgb_ = *rgb;
+    return finish_frame(st);
   }
 
   // IPipeline::get_image (pipeline_impl.hpp:125-137): rendered on the GPU

@@ -96,6 +96,8 @@ struct vf_ctx {
   int* visible_list = nullptr;
   DevState* dstate = nullptr;
   float* depth = nullptr;
+  uint16_t* disp = nullptr;  // raw disparity frame (process_raw_frame)
+  float* image_depth_scratch = nullptr;
   uint8_t* rgb = nullptr;
   float* pyr = nullptr;
   float2* ranges = nullptr;
@@ -439,9 +441,20 @@ int upload(vf_ctx* c, void* dst, const void* src, size_t n, bool src_device) {
   return VF_OK;
 }
 
-int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_inputs, vf_frame_stats* stats) {
-  if (!c || !depth) return VF_ERR_INVALID;
-  if (int rc = upload(c, c->depth, depth, sizeof(float) * (size_t)c->npix, device_inputs)) return rc;
+int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_inputs, vf_frame_stats* stats,
+                 const uint16_t* disparity = nullptr, bool big_endian = false) {
+  if (!c || (!depth && !disparity)) return VF_ERR_INVALID;
+  if (disparity) {
+    // process_raw_frame (pipeline_impl.hpp:59-62): 2 bytes per pixel cross the
+    // link, the conversion runs on the device
+    if (int rc = upload(c, c->disp, disparity, sizeof(uint16_t) * (size_t)c->npix, device_inputs)) return rc;
+    k_disparity_to_depth<<<(c->npix + 255) / 256, 256, 0, c->stream>>>(
+        c->disp, c->npix, big_endian ? 1 : 0, (float)c->calib.disparity_a, (float)c->calib.disparity_b,
+        (float)c->calib.depth.fx, c->s.max_depth, c->depth);
+    VF_CUDA(c, cudaGetLastError());
+  } else if (int rc = upload(c, c->depth, depth, sizeof(float) * (size_t)c->npix, device_inputs)) {
+    return rc;
+  }
   const bool with_rgb = rgb != nullptr && c->vsize == 8;
   if (with_rgb) {
     if (int rc = upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, device_inputs)) return rc;
@@ -490,7 +503,7 @@ void free_all(vf_ctx* c) {
                   c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
                   c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax,
                   c->sw.state, c->sw.host_slot, c->sw.host_free, c->sw.in_cand, c->sw.out_cand,
-                  c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host};
+                  c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host, c->disp, c->image_depth_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -611,6 +624,7 @@ void vf_default_settings(vf_settings* s) {
   s->use_swapping = 0;  // pipeline.hpp:20-23
   s->swap_buffer_blocks = 100;
   s->swap_host_blocks = 0;
+  s->max_depth = 8.0f;  // pipeline.hpp:37 (disparity conversion clamp)
 }
 
 int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out) {
@@ -754,6 +768,8 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->visible_list, sizeof(int) * (size_t)c->alloc_cap)) ||
       (rc = dalloc(c, &c->dstate, sizeof(DevState))) ||
       (rc = dalloc(c, &c->depth, sizeof(float) * (size_t)c->npix)) ||
+      (rc = dalloc(c, &c->disp, sizeof(uint16_t) * (size_t)c->npix)) ||
+      (rc = dalloc(c, &c->image_depth_scratch, sizeof(float) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height)) ||
       (rc = dalloc(c, &c->pyr, sizeof(float) * std::max<size_t>(c->pyr_floats, 1))) ||
       (rc = dalloc(c, &c->ranges, sizeof(float2) * (size_t)c->frag_w * c->frag_h)) ||
@@ -838,6 +854,30 @@ int vf_process_frame(vf_ctx* c, const float* depth_m, const uint8_t* rgb, vf_fra
 
 int vf_process_frame_device(vf_ctx* c, const float* d_depth, const uint8_t* d_rgb, vf_frame_stats* stats) {
   return frame_common(c, d_depth, d_rgb, true, stats);
+}
+
+int vf_process_raw_frame(vf_ctx* c, const uint16_t* disparity, const uint8_t* rgb, int big_endian,
+                         vf_frame_stats* stats) {
+  vf_frame_stats local;
+  return frame_common(c, nullptr, rgb, false, stats ? stats : &local, disparity, big_endian != 0);
+}
+
+int vf_process_raw_frame_device(vf_ctx* c, const uint16_t* d_disparity, const uint8_t* d_rgb, int big_endian,
+                                vf_frame_stats* stats) {
+  return frame_common(c, nullptr, d_rgb, true, stats, d_disparity, big_endian != 0);
+}
+
+int vf_disparity_to_depth(vf_ctx* c, const uint16_t* disparity, int big_endian, float* depth_out) {
+  if (!c || !disparity || !depth_out) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(c->disp, disparity, sizeof(uint16_t) * (size_t)c->npix, cudaMemcpyHostToDevice));
+  k_disparity_to_depth<<<(c->npix + 255) / 256, 256, 0, c->stream>>>(
+      c->disp, c->npix, big_endian ? 1 : 0, (float)c->calib.disparity_a, (float)c->calib.disparity_b,
+      (float)c->calib.depth.fx, c->s.max_depth, c->image_depth_scratch);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemcpy(depth_out, c->image_depth_scratch, sizeof(float) * (size_t)c->npix, cudaMemcpyDeviceToHost));
+  return VF_OK;
 }
 
 int vf_synchronize(vf_ctx* c) {

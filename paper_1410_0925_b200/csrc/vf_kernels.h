@@ -107,6 +107,8 @@ __global__ void k_icp_cluster(IcpArgs a);
 __global__ void k_synth(int n_spheres, const double* spheres, int n_planes, const double* planes, PoseD c2w,
                         IntrD in, double near_clip, double far_clip, float* depth, uint8_t* rgb);
 __global__ void k_fill_voxels(uint32_t* vox, size_t n_voxels, int words_per_voxel);
+__global__ void k_disparity_to_depth(const uint16_t* disp, int n, int big_endian, float a, float b, float fx,
+                                     float max_depth, float* depth);
 __global__ void k_rebuild_alloc_list(const HashEntry* entries, int n, int* alloc_list, int cap, Counters* ctr);
 __global__ void k_init_ranges(float2* ranges, int n);
 __global__ void k_reset_visible(Counters* ctr);

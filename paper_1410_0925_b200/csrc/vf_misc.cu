@@ -98,6 +98,24 @@ __global__ void __launch_bounds__(256) k_synth(int n_spheres, const double* __re
 }
 
 // VoxelS{} / VoxelSRgb{}: sdf 32767, weights 0 (voxel.hpp:29-46).
+// disparity_image_to_depth / disparity_to_depth (engine/view.hpp:18-28,
+// io/calibration.hpp:45-60); big_endian: the samples are the raw bytes of a
+// 16-bit P5 raster (read_pgm16, src/pnm.cpp:63-73), byte-swapped here.
+__global__ void k_disparity_to_depth(const uint16_t* __restrict__ disp, int n, int big_endian, float a, float b,
+                                     float fx, float max_depth, float* __restrict__ depth) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t d = __ldg(disp + i);
+  if (big_endian) d = ((d & 0xFFu) << 8) | (d >> 8);
+  const float denom = a - (float)d;
+  float z = 0.0f;
+  if (!(denom <= 0.0f)) {
+    const float v = 8.0f * b * fx / denom;
+    z = (v > 0.0f && v <= max_depth) ? v : 0.0f;
+  }
+  depth[i] = z;
+}
+
 __global__ void k_fill_voxels(uint32_t* __restrict__ vox, size_t n_voxels, int words_per_voxel) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_voxels; i += (size_t)gridDim.x * blockDim.x) {
     vox[i * words_per_voxel] = 0x00007FFFu;

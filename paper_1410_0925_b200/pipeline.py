@@ -102,6 +102,7 @@ class EngineSettings:
     use_swapping: bool = False  # host swapping (pipeline.hpp:20-23, swap.hpp)
     swap_buffer_blocks: int = 100
     swap_host_blocks: int = 0  # host store slots (0: 4 x block_count)
+    max_depth: float = 8.0  # disparity conversion clamp (pipeline.hpp:37)
 
     def to_c(self) -> VfSettings:
         s = VfSettings()
@@ -229,6 +230,24 @@ class Pipeline:
         st = VfFrameStats()
         self._chk("vf_process_frame", self._L.vf_process_frame(self._h, _ptr(d), _ptr(c), C.byref(st)))
         return FrameStats.from_c(st)
+
+    def process_raw_frame(self, rgb, disparity, big_endian: bool = False) -> FrameStats:
+        """IPipeline::process_raw_frame(rgb*, disparity) (pipeline_impl.hpp:59-62):
+        u16 disparity (or, big_endian, the raw bytes of a 16-bit P5 raster)."""
+        d = np.ascontiguousarray(disparity, dtype=np.uint16).reshape(self.height, self.width)
+        c = None if rgb is None else np.ascontiguousarray(rgb, dtype=np.uint8)
+        st = VfFrameStats()
+        self._chk("vf_process_raw_frame",
+                  self._L.vf_process_raw_frame(self._h, _ptr(d), _ptr(c), 1 if big_endian else 0, C.byref(st)))
+        return FrameStats.from_c(st)
+
+    def disparity_to_depth(self, disparity, big_endian: bool = False) -> np.ndarray:
+        """disparity_image_to_depth (view.hpp:18-28) on the device."""
+        d = np.ascontiguousarray(disparity, dtype=np.uint16).reshape(self.height, self.width)
+        out = np.zeros((self.height, self.width), np.float32)
+        self._chk("vf_disparity_to_depth",
+                  self._L.vf_disparity_to_depth(self._h, _ptr(d), 1 if big_endian else 0, _ptr(out)))
+        return out
 
     def process_frame_device(self, d_depth: int, d_rgb: int | None = None, read_stats: bool = False):
         """Inputs already in device memory (raw device pointers)."""

@@ -354,3 +354,35 @@ def test_forward_project_from_oracle_state(olib):
             assert len(sg) == int(np.count_nonzero(pts[::4, ::4, 3])) and not cg.any()
             assert np.array_equal(p.get_image(0), o.image(3))
         p.close()
+
+
+def test_process_raw_frame_bit_exact(olib):
+    """process_raw_frame (pipeline_impl.hpp:59-62): disparity converted on the
+    device equals the oracle's disparity_image_to_depth bit for bit, and the
+    frame fed from disparity equals the frame fed from that depth, both as
+    u16 samples and as the big-endian bytes of a P5 raster."""
+    from dataclasses import replace
+    cfg = CONFIGS["T320"].with_(tracking=False)
+    s, c = settings_from_config(cfg)
+    c = replace(c, disparity_a=1135.09, disparity_b=0.0819141)
+    a, b, fx = 1135.09, 0.0819141, cfg.intrinsics[0]
+    pose, depth, _ = frames(olib, cfg, 1)[0]
+    # disparity that round-trips to the rendered depth (depth_to_disparity, calibration.hpp:62-70)
+    with np.errstate(divide="ignore"):
+        dd = np.where(depth > 0, np.float32(a) - np.float32(8.0) * np.float32(b) * np.float32(fx) / depth, 65535)
+    disp = np.where((dd < 0) | (dd > 65535), 65535, dd + 0.5).astype(np.uint16)
+    want = vf_py.disparity_to_depth(olib, disp, a, b, fx, 8.0)
+    p = make_pipeline(s, c)
+    assert np.array_equal(p.disparity_to_depth(disp).view(np.uint32), want.view(np.uint32))
+    be = disp.byteswap()  # raw P5 bytes read as native u16
+    assert np.array_equal(p.disparity_to_depth(be, big_endian=True).view(np.uint32), want.view(np.uint32))
+    p.set_pose(pose)
+    p.process_raw_frame(None, be, big_endian=True)
+    q = make_pipeline(s, c)
+    q.set_pose(pose)
+    q.process_frame(None, want)
+    assert entries_equal(p.entries(), q.entries())
+    assert np.array_equal(p.voxels(), q.voxels())
+    assert np.array_equal(p.tracking_state()[0], q.tracking_state()[0])
+    p.close()
+    q.close()

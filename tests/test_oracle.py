@@ -185,3 +185,21 @@ def test_oracle_golden_swap(olib, name):
         assert sha(vol.swap_states()) == g["states_sha"], f"frame {i}: swap states"
         assert vol.store_count() == g["store_count"] and _store_digest(vol) == g["store_sha"], f"frame {i}: store"
     vol.close()
+
+
+def _disparity_cases(seed=0x14100925):
+    rng = np.random.default_rng(seed)
+    d = rng.integers(0, 65536, size=(120, 160), dtype=np.uint16)
+    d[0, :8] = [0, 1, 1134, 1135, 1136, 65535, 400, 900]  # pole a - d <= 0, saturated, in range
+    return d
+
+
+def test_disparity_to_depth_matches_reference(olib, rlib):
+    """disparity_image_to_depth (view.hpp:18-28): restatement vs the reference,
+    Kinect-style a / b, including the pole and the max_depth clamp."""
+    d = _disparity_cases()
+    for a, b, fx, mx in [(1135.09, 0.0819141, 573.71, 8.0), (1135.09, 0.0819141, 573.71, 3.0), (900.0, 0.2, 525.0, 8.0)]:
+        o = vf_py.disparity_to_depth(olib, d, a, b, fx, mx)
+        r = vf_py.disparity_to_depth(rlib, d, a, b, fx, mx)
+        assert np.array_equal(o.view(np.uint32), r.view(np.uint32))
+        assert (o > 0).any() and (o == 0).any()
