@@ -275,6 +275,15 @@ int launch_forward_project(vf_ctx* c) {
   return VF_OK;
 }
 
+// Integration CTAs per SM (VF_INT_GRID_MULT overrides, for tuning runs).
+int int_grid_mult() {
+  static const int m = [] {
+    const char* e = std::getenv("VF_INT_GRID_MULT");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  return m;
+}
+
 // The frame, as stream work.  With track=true the ICP runs first against the
 // maps of the previous frame; the updated pose stays on the device.
 int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
@@ -325,7 +334,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     VF_CUDA(c, cudaEventRecord(c->ev_join, c->side));
   }
   const bool color = c->vsize == 8;
-  launch_integrate(c->num_sms * 8, st, color, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+  launch_integrate(c->num_sms * int_grid_mult(), st, color, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
                    with_rgb ? c->rgb : nullptr, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
                    s.stop_integrating_at_max);
   VF_LAUNCHED(c, "k_integrate");
@@ -1262,7 +1271,7 @@ int vf_stage_integrate(vf_ctx* c, const float* depth_m, const uint8_t* rgb, cons
   if (with_rgb && upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, false)) return VF_ERR_CUDA;
   if (int rc = set_pose_dev(c, pose)) return rc;
   k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
-  launch_integrate(c->num_sms * 8, st, c->vsize == 8, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+  launch_integrate(c->num_sms * int_grid_mult(), st, c->vsize == 8, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
                    with_rgb ? c->rgb : nullptr, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
                    s.stop_integrating_at_max);
   VF_CUDA(c, cudaGetLastError());
