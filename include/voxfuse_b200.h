@@ -89,7 +89,17 @@ typedef struct vf_settings {
   int swap_buffer_blocks;
   int swap_host_blocks;
   float max_depth; /* disparity conversion clamp, metres (EngineSettings::max_depth, pipeline.hpp:37) */
+  /* TrackerSettings::type / ren_sigma / skip_points (tracking_state.hpp:10-22) */
+  int tracker_type; /* vf_tracker_type */
+  float ren_sigma;
+  int skip_points;
 } vf_settings;
+
+enum vf_tracker_type { /* TrackerType (tracking_state.hpp:10) */
+  VF_TRACKER_ICP = 0,
+  VF_TRACKER_COLOR = 1,  /* photometric, needs VoxelSRgb and RGB frames */
+  VF_TRACKER_ICP_REN = 2 /* ICP on the coarse levels + SDF (Ren) refinement */
+};
 
 typedef struct vf_intrinsics { /* Intrinsics (core/intrinsics.hpp:10-32) */
   double fx, fy, cx, cy;
@@ -214,6 +224,14 @@ int vf_stage_raycast(vf_ctx* ctx, const double pose[12]);
  * reference's icp_track it does not change the context's pose. */
 int vf_stage_icp(vf_ctx* ctx, const float* depth_m, const double initial_pose[12], double out_pose[12],
                  int* iterations, double* cost, int* valid_points, int* ok);
+/* ren_refine (ren_tracker.hpp:30-120) of depth_m against the current volume
+ * from initial_pose; does not change the context's pose. */
+int vf_stage_ren(vf_ctx* ctx, const float* depth_m, const double initial_pose[12], double out_pose[12],
+                 int* iterations, double* cost, int* valid_points, int* ok);
+/* build_color_pyramid + color_track (color_tracker.hpp:107-154) of the current
+ * surface list (vf_get_surface_points) against an RGB frame (VoxelSRgb only). */
+int vf_stage_color(vf_ctx* ctx, const uint8_t* rgb, const double initial_pose[12], double out_pose[12],
+                   int* iterations, double* cost, int* valid_points, int* ok);
 /* Per-iteration ICP sums of the last track: rows of 48 doubles
  * (level, iter, 21 H, 6 g, cost, count, rotation_only, evaluation camera-to-world
  * pose (12), 4 phase timers in SM cycles). Returns the row count. */

@@ -44,6 +44,9 @@ struct vfr_config {
   int rgb_width, rgb_height;
   double rgb_to_depth[12];  // row-major R (9) then t (3)
   int use_swapping, swap_buffer_blocks;
+  int tracker_type;  // TrackerType: 0 icp, 1 color, 2 icp_ren
+  float ren_sigma;
+  int skip_points;
 };
 
 struct vfr_stats {
@@ -88,7 +91,6 @@ EngineSettings settings_from(const vfr_config& c) {
   s.far_clip = c.far_clip;
   s.visibility_margin_px = c.margin_px;
   s.swap_margin_px = c.swap_margin_px;
-  s.tracker.type = TrackerType::icp;
   s.tracker.hierarchy_levels = c.levels;
   s.tracker.rotation_only_levels = c.rotation_only_levels;
   s.tracker.max_iterations = c.max_iterations;
@@ -96,6 +98,10 @@ EngineSettings settings_from(const vfr_config& c) {
   s.tracker.icp_dist_threshold = c.icp_dist_threshold;
   s.tracker.convergence_eps = c.convergence_eps;
   s.tracker.max_condition = c.max_condition;
+  s.tracker.type = c.tracker_type == 1 ? TrackerType::color : c.tracker_type == 2 ? TrackerType::icp_ren
+                                                                                  : TrackerType::icp;
+  s.tracker.ren_sigma = c.ren_sigma;
+  s.tracker.skip_points = c.skip_points != 0;
   s.use_swapping = c.use_swapping != 0;
   s.swap_buffer_blocks = c.swap_buffer_blocks;
   return s;
@@ -134,6 +140,9 @@ struct CtxBase {
   virtual int image(int mode, std::uint8_t* out) const = 0;
   // swap engine state (swap.hpp:45-91); nullptr without swapping
   virtual const void* cache_ptr() const { return nullptr; }
+  // ren_refine / color_track on this context's volume and surface list
+  virtual TrackingResult stage_ren(const float*, const Pose&) const { return {}; }
+  virtual TrackingResult stage_color(const std::uint8_t*, const Pose&) const { return {}; }
   virtual int voxel_type() const = 0;
 };
 
@@ -254,6 +263,14 @@ struct StagesCtx final : CtxBase {
       cache.emplace(GlobalCache<TVoxel>::in_memory(volume.entry_count(), s.swap_buffer_blocks));
   }
   const void* cache_ptr() const override { return cache ? &*cache : nullptr; }
+  TrackingResult stage_ren(const float* depth, const Pose& init) const override {
+    return ren_refine(depth_image(depth, cfg.width, cfg.height), calib.depth, volume, s.scene, init, s.tracker);
+  }
+  TrackingResult stage_color(const std::uint8_t* rgb, const Pose& init) const override {
+    const ColorPyramid pyr =
+        build_color_pyramid(rgb_image(rgb, cfg.rgb_width, cfg.rgb_height), calib.rgb, s.tracker.hierarchy_levels);
+    return color_track(st.surface_points, st.surface_colors, pyr, init, s.tracker);
+  }
   int voxel_type() const override { return TVoxel::has_color ? 2 : 1; }
   int process(const float* depth, const std::uint8_t* rgb, const double* pose, vfr_stats* out) override {
     if (!pose) return -1;
@@ -442,6 +459,20 @@ long vfr_store_count(void* ctx) {
   const CtxBase* b = static_cast<CtxBase*>(ctx);
   auto f = [&](const auto& c) -> long { return c.store().stored_count(); };
   return b->voxel_type() == 2 ? with_cache<VoxelSRgb>(b, f) : with_cache<VoxelS>(b, f);
+}
+// ren_refine / color_track through the reference (stage isolation)
+int vfr_stage_track(void* ctx, int which, const void* frame, const double* init, double* out_pose, int* iters,
+                    double* cost, int* valid, int* ok) {
+  const CtxBase* b = static_cast<CtxBase*>(ctx);
+  const Pose p0 = pose_from(init);
+  const TrackingResult r = which == 1 ? b->stage_color(static_cast<const std::uint8_t*>(frame), p0)
+                                      : b->stage_ren(static_cast<const float*>(frame), p0);
+  pose_to(r.pose, out_pose);
+  *iters = r.iterations;
+  *cost = r.final_cost;
+  *valid = r.valid_points;
+  *ok = r.ok ? 1 : 0;
+  return 0;
 }
 // disparity_image_to_depth through the reference's own Calibration (view.hpp:18-28)
 void vfr_disparity_to_depth(const std::uint16_t* disp, int w, int h, double a, double b, double fx,

@@ -39,6 +39,10 @@ typedef struct vfo_config {
   double rgb_to_depth[12];
   /* EngineSettings::use_swapping / swap_buffer_blocks (pipeline.hpp:20-23) */
   int use_swapping, swap_buffer_blocks;
+  /* TrackerSettings::type / ren_sigma / skip_points (the restatement covers the ICP tracker only) */
+  int tracker_type;
+  float ren_sigma;
+  int skip_points;
 } vfo_config;
 
 typedef struct vfo_stats {

@@ -64,6 +64,9 @@ class Config(C.Structure):
         ("rgb_to_depth", C.c_double * 12),
         ("use_swapping", C.c_int),
         ("swap_buffer_blocks", C.c_int),
+        ("tracker_type", C.c_int),
+        ("ren_sigma", C.c_float),
+        ("skip_points", C.c_int),
     ]
 
 
@@ -126,6 +129,9 @@ def make_config(cfg) -> Config:
         c.rgb_to_depth[i] = v
     c.use_swapping = 1 if getattr(cfg, "use_swapping", False) else 0
     c.swap_buffer_blocks = getattr(cfg, "swap_buffer_blocks", 100)
+    c.tracker_type = {"icp": 0, "color": 1, "icp_ren": 2}[getattr(cfg, "tracker", "icp")]
+    c.ren_sigma = 10.0
+    c.skip_points = 0
     return c
 
 
@@ -341,6 +347,20 @@ class Volume:
             if p is not None:
                 out[int(i)] = p
         return out
+
+    def stage_track(self, which: str, frame: np.ndarray, initial: np.ndarray):
+        """Reference ren_refine ("ren", depth) / color_track ("color", rgb) on this
+        (known-pose) context: (pose, iterations, cost, valid_points, ok)."""
+        f = self.L.lib.vfr_stage_track
+        f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
+                      C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        frame = np.ascontiguousarray(frame)
+        ini = np.ascontiguousarray(initial, np.float64)
+        out = np.zeros(12)
+        it, cost, valid, ok = C.c_int(), C.c_double(), C.c_int(), C.c_int()
+        f(self.h, 1 if which == "color" else 0, frame.ctypes.data_as(C.c_void_p), ini.ctypes.data_as(C.c_void_p),
+          out.ctypes.data_as(C.c_void_p), C.byref(it), C.byref(cost), C.byref(valid), C.byref(ok))
+        return out, it.value, cost.value, valid.value, bool(ok.value)
 
     def surface_points(self):
         """TrackingState::surface_points / surface_colors (n x 3 float32 each)."""

@@ -40,6 +40,7 @@ EXPORTS = [
     "vf_entry_count", "vf_voxel_bytes", "vf_export_entries", "vf_export_voxels", "vf_export_free_stacks",
     "vf_import_state", "vf_export_visible_list", "vf_export_ranges",
     "vf_stage_allocate", "vf_stage_integrate", "vf_stage_raycast", "vf_stage_icp", "vf_icp_trace",
+    "vf_stage_ren", "vf_stage_color",
     "vf_depth_pyramid", "vf_render_synthetic",
     "vf_shard_owner", "vf_shard_nccl_unique_id", "vf_shard_attach_nccl", "vf_shard_composite_local",
     "vf_device_alloc", "vf_device_free", "vf_memcpy_h2d", "vf_memcpy_d2h", "vf_host_alloc_pinned",
@@ -81,6 +82,9 @@ class VfSettings(C.Structure):
         ("swap_buffer_blocks", C.c_int),
         ("swap_host_blocks", C.c_int),
         ("max_depth", C.c_float),
+        ("tracker_type", C.c_int),
+        ("ren_sigma", C.c_float),
+        ("skip_points", C.c_int),
     ]
 
 
@@ -187,6 +191,8 @@ def load() -> C.CDLL:
         "vf_stage_raycast": (C.c_int, [vp, dp]),
         "vf_stage_icp": (C.c_int, [vp, vp, dp, dp, ip, dp, ip, ip]),
         "vf_icp_trace": (C.c_long, [vp, vp, C.c_long]),
+        "vf_stage_ren": (C.c_int, [vp, vp, dp, dp, ip, dp, ip, ip]),
+        "vf_stage_color": (C.c_int, [vp, vp, dp, dp, ip, dp, ip, ip]),
         "vf_depth_pyramid": (C.c_int, [vp, vp, vp]),
         "vf_render_synthetic": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, vp, dp, C.POINTER(VfIntrinsics),
                                           C.c_double, C.c_double, vp, vp]),

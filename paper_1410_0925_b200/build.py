@@ -25,7 +25,7 @@ OUT_DIR = PKG / "lib"
 LIB = OUT_DIR / "libvoxfuse_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["vf_alloc.cu", "vf_integrate.cu", "vf_raycast.cu", "vf_icp.cu", "vf_misc.cu", "vf_shard.cu", "vf_render.cu", "vf_swap.cu", "vf_api.cu"]
+SOURCES = ["vf_alloc.cu", "vf_integrate.cu", "vf_raycast.cu", "vf_icp.cu", "vf_misc.cu", "vf_shard.cu", "vf_render.cu", "vf_swap.cu", "vf_track.cu", "vf_api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",

@@ -35,6 +35,7 @@ struct DevState {
   FrameParams fp;
   AllocMeta meta;
   SwapCounters swap;
+  RenCtl ren;
 };
 
 PoseD pose_from(const double* p) {
@@ -126,6 +127,12 @@ struct vf_ctx {
   int surf_cap = 0, surf_tiles = 0;
   uint8_t* image = nullptr;  // get_image output (w*h*3) + depth-max word
   int* image_dmax = nullptr;
+  // other trackers (vf_track.cu)
+  double* ren_partials = nullptr;
+  int ren_grid = 0;
+  std::vector<IntrD> rgb_levels;  // colour pyramid intrinsics (Intrinsics::half per level)
+  float4* cpyr = nullptr;         // per level: colour, grad_x, grad_y
+  std::vector<size_t> cpyr_off;
   // swap engine (vf_swap.cu): device arrays + the pinned, mapped host store
   bool swapping = false;
   SwapDev sw{};
@@ -165,22 +172,28 @@ namespace {
 
 HashView hash_view(vf_ctx* c) { return HashView{c->entries, c->mask, c->s.bucket_size, c->ordered}; }
 
-int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool update_state = true) {
+// first_level 1: icp_track on the pyramid without its full-resolution level
+// (the icp_ren tracker, pipeline_impl.hpp:189-195).
+int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool update_state = true,
+               int first_level = 0) {
   IcpArgs a{};
-  const int L = c->s.hierarchy_levels;
+  const int L = c->s.hierarchy_levels - first_level;
   size_t off = 0;
-  for (int l = 0; l < L; ++l) {
-    const IntrD& in = c->levels[l];
-    a.lv[l].depth = l == 0 ? c->depth : c->pyr + off;
-    if (l > 0) off += (size_t)in.width * in.height;
-    a.lv[l].ux = c->utab + c->utab_off[l];
-    a.lv[l].uy = c->utab + c->utab_off[l] + in.width;
-    a.lv[l].w = in.width;
-    a.lv[l].h = in.height;
-    a.lv[l].fx = in.fx;
-    a.lv[l].fy = in.fy;
-    a.lv[l].cx = in.cx;
-    a.lv[l].cy = in.cy;
+  for (int g = 0; g < c->s.hierarchy_levels; ++g) {
+    const IntrD& in = c->levels[g];
+    const int l = g - first_level;
+    if (l >= 0) {
+      a.lv[l].depth = g == 0 ? c->depth : c->pyr + off;
+      a.lv[l].ux = c->utab + c->utab_off[g];
+      a.lv[l].uy = c->utab + c->utab_off[g] + in.width;
+      a.lv[l].w = in.width;
+      a.lv[l].h = in.height;
+      a.lv[l].fx = in.fx;
+      a.lv[l].fy = in.fy;
+      a.lv[l].cx = in.cx;
+      a.lv[l].cy = in.cy;
+    }
+    if (g > 0) off += (size_t)in.width * in.height;
   }
   a.levels = L;
   a.rotation_only_levels = c->s.rotation_only_levels;
@@ -201,7 +214,7 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
   a.trace_cap = kTraceCap;
   a.max_slots = c->icp_slots;
   a.ctl_io = c->icp_ctl;
-  const int coarse = c->icp_cluster ? c->icp_coarse_levels : 0;
+  const int coarse = c->icp_cluster ? std::min(c->icp_coarse_levels, L) : 0;
   if (coarse > 0) {
     // coarse levels in one thread-block cluster (cluster barrier + DSMEM)
     IcpArgs ac = a;
@@ -275,6 +288,99 @@ int launch_forward_project(vf_ctx* c) {
   return VF_OK;
 }
 
+// SDF refinement (ren_refine, ren_tracker.hpp:30-120): max_iterations
+// (terms, control) pairs, then the result.  combine_icp: the frame's icp_ren
+// tracker (start from the coarse ICP's pose when it succeeded).
+int enqueue_ren(vf_ctx* c, cudaStream_t st, bool combine_icp, const PoseD* explicit_init, bool update_state,
+                int* launches) {
+  const vf_settings& s = c->s;
+  k_ren_init<<<1, 32, 0, st>>>(&c->dstate->icp, &c->dstate->pose, combine_icp ? 1 : 0, explicit_init, &c->dstate->ren);
+  for (int it = 0; it < s.max_iterations; ++it) {
+    k_ren_terms<<<c->ren_grid, 256, 0, st>>>(c->depth, c->din, hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
+                                             c->vsize / 4, s.voxel_size, (double)s.ren_sigma, &c->dstate->ren,
+                                             c->ren_partials);
+    k_ren_ctl<<<1, 32, 0, st>>>(c->ren_partials, c->ren_grid, &c->dstate->ren, s.min_valid_points, s.max_condition,
+                                s.convergence_eps);
+  }
+  k_ren_finish<<<1, 32, 0, st>>>(&c->dstate->ren, s.max_iterations, combine_icp ? 1 : 0, &c->dstate->icp,
+                                 &c->dstate->pose, update_state ? 1 : 0);
+  VF_CUDA(c, cudaGetLastError());
+  *launches += 2 + 2 * s.max_iterations;
+  return VF_OK;
+}
+
+// build_color_pyramid (pyramid.hpp:112-132) of c->rgb, then color_track
+// (color_tracker.hpp:107-154) of the current surface list.
+int enqueue_color(vf_ctx* c, cudaStream_t st, const PoseD* explicit_init, bool update_state, int* launches) {
+  const vf_settings& s = c->s;
+  const int L = s.hierarchy_levels;
+  ColorTrackArgs a{};
+  for (int l = 0; l < L; ++l) {
+    const IntrD& in = c->rgb_levels[l];
+    const int n = in.width * in.height;
+    float4* col = c->cpyr + c->cpyr_off[l];
+    if (l == 0) {
+      k_cpyr_base<<<(n + 255) / 256, 256, 0, st>>>(c->rgb, n, col);
+    } else {
+      const IntrD& up = c->rgb_levels[l - 1];
+      k_cpyr_down<<<(n + 255) / 256, 256, 0, st>>>(c->cpyr + c->cpyr_off[l - 1], up.width, up.height, col);
+    }
+    k_cpyr_grad<<<(n + 255) / 256, 256, 0, st>>>(col, in.width, in.height, col + n, col + 2 * (size_t)n);
+    a.lv[l] = ColorLevel{col, col + n, col + 2 * (size_t)n, in.width, in.height, in.fx, in.fy, in.cx, in.cy};
+  }
+  a.levels = L;
+  a.stride = s.skip_points ? 2 : 1;
+  a.max_iterations = s.max_iterations;
+  a.min_valid_points = s.min_valid_points;
+  a.convergence_eps = s.convergence_eps;
+  a.points = c->surf_points;
+  a.colors = c->surf_colors;
+  a.count = &c->dstate->ctr.surface_count;
+  a.state = &c->dstate->pose;
+  a.explicit_init = explicit_init;
+  a.result = &c->dstate->icp;
+  a.update_state = update_state ? 1 : 0;
+  k_color_track<<<1, 1024, 0, st>>>(a);
+  VF_CUDA(c, cudaGetLastError());
+  *launches += 2 * L + 1;
+  return VF_OK;
+}
+
+// Pipeline::track (pipeline_impl.hpp:180-209) for the configured tracker;
+// the result lands in DevState::icp and, when ok and update_state, the pose.
+int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* explicit_init, bool update_state,
+                    int* launches) {
+  const vf_settings& s = c->s;
+  if (s.tracker_type == VF_TRACKER_COLOR) {
+    if (!with_rgb) {  // no RGB frame: {state.pose, false}
+      k_track_fail<<<1, 32, 0, st>>>(&c->dstate->pose, &c->dstate->icp);
+      ++*launches;
+      return VF_OK;
+    }
+    return enqueue_color(c, st, explicit_init, update_state, launches);
+  }
+  if (s.hierarchy_levels > 1) {
+    k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, st>>>(
+        c->depth, c->din.width, c->din.height, s.hierarchy_levels, c->pyr);
+    VF_LAUNCHED(c, "k_pyramid");
+    ++*launches;
+  }
+  if (s.tracker_type == VF_TRACKER_ICP_REN) {
+    if (s.hierarchy_levels > 1) {
+      if (int rc = launch_icp(c, st, false, /*update_state=*/false, /*first_level=*/1)) return rc;
+      ++*launches;
+    } else {
+      k_track_fail<<<1, 32, 0, st>>>(&c->dstate->pose, &c->dstate->icp);
+      ++*launches;
+    }
+    return enqueue_ren(c, st, true, explicit_init, update_state, launches);
+  }
+  if (int rc = launch_icp(c, st, false, update_state)) return rc;
+  VF_LAUNCHED(c, "k_icp");
+  ++*launches;
+  return VF_OK;
+}
+
 // Integration CTAs per SM (VF_INT_GRID_MULT overrides, for tuning runs).
 int int_grid_mult() {
   static const int m = [] {
@@ -292,15 +398,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   int launches = 0;
   stage_mark(c, 0);
   if (track) {
-    if (s.hierarchy_levels > 1) {
-      k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, st>>>(
-          c->depth, c->din.width, c->din.height, s.hierarchy_levels, c->pyr);
-  VF_LAUNCHED(c, "k_pyramid");
-      ++launches;
-    }
-    if (int rc = launch_icp(c, st)) return rc;
-    VF_LAUNCHED(c, "k_icp");
-    ++launches;
+    if (int rc = enqueue_tracker(c, st, with_rgb, nullptr, true, &launches)) return rc;
   }
   stage_mark(c, 1);
   k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
@@ -512,7 +610,8 @@ void free_all(vf_ctx* c) {
                   c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
                   c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax,
                   c->sw.state, c->sw.host_slot, c->sw.host_free, c->sw.in_cand, c->sw.out_cand,
-                  c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host, c->disp, c->image_depth_scratch};
+                  c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host, c->disp, c->image_depth_scratch,
+                  c->ren_partials, c->cpyr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -634,6 +733,9 @@ void vf_default_settings(vf_settings* s) {
   s->swap_buffer_blocks = 100;
   s->swap_host_blocks = 0;
   s->max_depth = 8.0f;  // pipeline.hpp:37 (disparity conversion clamp)
+  s->tracker_type = VF_TRACKER_ICP;  // tracking_state.hpp:12-22
+  s->ren_sigma = 10.0f;
+  s->skip_points = 0;
 }
 
 int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** out) {
@@ -668,6 +770,13 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     return VF_ERR_CUDA;
   }
   c->vsize = s->voxel_type == VF_VOXEL_S_RGB ? 8 : 4;
+  if (s->tracker_type < VF_TRACKER_ICP || s->tracker_type > VF_TRACKER_ICP_REN ||
+      (s->tracker_type == VF_TRACKER_COLOR && c->vsize != 8)) {
+    // "colour tracker requires a voxel type with colour information" (pipeline_impl.hpp:55-57)
+    free_all(c);
+    delete c;
+    return VF_ERR_INVALID;
+  }
   if (s->use_swapping) {
     const long entries = (long)s->bucket_count * s->bucket_size + s->excess_count;
     if (s->swap_buffer_blocks < 1 || s->swap_buffer_blocks > kSwapSortCap || s->swap_host_blocks < 0 ||
@@ -715,6 +824,14 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     for (int y = 0; y < in.height; ++y) utab_h.push_back((y - in.cy) / in.fy);
   }
   c->alloc_cap = c->entry_count;
+  c->ren_grid = c->num_sms * 4;
+  c->rgb_levels.push_back(c->rgbin);
+  for (int l = 1; l < s->hierarchy_levels; ++l) c->rgb_levels.push_back(intr_half(c->rgb_levels.back()));
+  size_t cpyr_n = 0;
+  for (const IntrD& in : c->rgb_levels) {
+    c->cpyr_off.push_back(cpyr_n);
+    cpyr_n += 3 * (size_t)in.width * in.height;
+  }
   c->surf_cap = ((c->din.width + kSurfaceStride - 1) / kSurfaceStride) *
                 ((c->din.height + kSurfaceStride - 1) / kSurfaceStride);
   c->surf_tiles = (c->surf_cap + kFpTileItems - 1) / kFpTileItems;
@@ -792,6 +909,8 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->surf_colors, sizeof(float) * 3 * (size_t)c->surf_cap)) ||
       (rc = dalloc(c, &c->surf_scan, sizeof(unsigned long long) * (1 + (size_t)c->surf_tiles))) ||
       (rc = dalloc(c, &c->image, 3 * (size_t)c->npix)) || (rc = dalloc(c, &c->image_dmax, sizeof(int))) ||
+      (rc = dalloc(c, &c->ren_partials, sizeof(double) * 32 * (size_t)c->ren_grid)) ||
+      (c->vsize == 8 && (rc = dalloc(c, &c->cpyr, sizeof(float4) * cpyr_n))) ||
       (c->swapping &&
        ((rc = dalloc(c, &c->sw.state, (size_t)c->entry_count)) ||
         (rc = dalloc(c, &c->sw.host_slot, sizeof(int) * (size_t)c->entry_count)) ||
@@ -1322,6 +1441,44 @@ int vf_stage_icp(vf_ctx* c, const float* depth_m, const double initial_pose[12],
   return VF_OK;
 }
 
+namespace {
+int stage_result(vf_ctx* c, double* out_pose, int* iterations, double* cost, int* valid_points, int* ok) {
+  if (int rc = read_state(c)) return rc;
+  const IcpResult& r = c->hstate->icp;
+  if (out_pose) pose_to(r.pose, out_pose);
+  if (iterations) *iterations = r.iterations;
+  if (cost) *cost = r.final_cost;
+  if (valid_points) *valid_points = r.valid_points;
+  if (ok) *ok = r.ok;
+  return VF_OK;
+}
+}  // namespace
+
+int vf_stage_ren(vf_ctx* c, const float* depth_m, const double initial_pose[12], double out_pose[12],
+                 int* iterations, double* cost, int* valid_points, int* ok) {
+  if (!c || !depth_m || !initial_pose) return VF_ERR_INVALID;
+  cudaStream_t st = c->stream;
+  if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
+  *c->hpose = pose_from(initial_pose);
+  VF_CUDA(c, cudaMemcpyAsync(&c->dstate->init_pose, c->hpose, sizeof(PoseD), cudaMemcpyHostToDevice, st));
+  int launches = 0;
+  if (int rc = enqueue_ren(c, st, false, &c->dstate->init_pose, false, &launches)) return rc;
+  return stage_result(c, out_pose, iterations, cost, valid_points, ok);
+}
+
+int vf_stage_color(vf_ctx* c, const uint8_t* rgb, const double initial_pose[12], double out_pose[12],
+                   int* iterations, double* cost, int* valid_points, int* ok) {
+  if (!c || !rgb || !initial_pose) return VF_ERR_INVALID;
+  if (c->vsize != 8) return VF_ERR_INVALID;
+  cudaStream_t st = c->stream;
+  if (int rc = upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, false)) return rc;
+  *c->hpose = pose_from(initial_pose);
+  VF_CUDA(c, cudaMemcpyAsync(&c->dstate->init_pose, c->hpose, sizeof(PoseD), cudaMemcpyHostToDevice, st));
+  int launches = 0;
+  if (int rc = enqueue_color(c, st, &c->dstate->init_pose, false, &launches)) return rc;
+  return stage_result(c, out_pose, iterations, cost, valid_points, ok);
+}
+
 long vf_icp_trace(vf_ctx* c, double* out, long max_rows) {
   if (!c) return VF_ERR_INVALID;
   if (int rc = read_state(c)) return rc;
@@ -1529,8 +1686,24 @@ long vf_last_modified_voxels(vf_ctx* c) {
 int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
   if (!c) return VF_ERR_INVALID;
   int icp = 1 + ((c->icp_cluster && c->icp_coarse_levels > 0 && c->icp_coarse_levels < c->s.hierarchy_levels) ? 1 : 0);
-  return 7 + (tracking_frame ? (c->s.hierarchy_levels > 1 ? 1 : 0) + icp : 0) + (c->nccl_comm ? 2 : 0) +
-         (c->vsize == 8 ? 1 : 0) + (c->swapping ? 3 : 0);
+  const int L = c->s.hierarchy_levels;
+  int track = 0;
+  if (tracking_frame) {
+    switch (c->s.tracker_type) {
+      case VF_TRACKER_COLOR:
+        track = 2 * L + 1;  // colour pyramid + the one-CTA tracker (RGB frames)
+        break;
+      case VF_TRACKER_ICP_REN: {
+        const int coarse = (c->icp_cluster && c->icp_coarse_levels > 0) ? std::min(c->icp_coarse_levels, L - 1) : 0;
+        track = (L > 1 ? 1 : 0) + (L > 1 ? 1 + ((coarse > 0 && coarse < L - 1) ? 1 : 0) : 1) + 2 +
+                2 * c->s.max_iterations;
+        break;
+      }
+      default:
+        track = (L > 1 ? 1 : 0) + icp;
+    }
+  }
+  return 7 + track + (c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 3 : 0);
 }
 
 }  // extern "C"

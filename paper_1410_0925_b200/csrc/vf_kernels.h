@@ -126,6 +126,47 @@ __global__ void k_colourize_depth(const float* depth, int n, const int* dmax_bit
 constexpr int kSurfaceStride = 4;  // pipeline_impl.hpp:219
 constexpr int kFpTileItems = 256;
 
+// other trackers (vf_track.cu)
+struct RenCtl {
+  PoseD init;  // ren_refine's init_world_to_cam
+  PoseD c2w;
+  double final_cost;
+  int iterations, valid_points, done, ok;
+};
+__global__ void k_ren_init(const IcpResult* icp, const PoseD* state, int use_icp, const PoseD* explicit_init,
+                           RenCtl* ctl);
+__global__ void k_ren_terms(const float* depth, IntrD in, HashView hv, const uint32_t* vox, int vstride, float vs,
+                            double sigma, const RenCtl* ctl, double* partials);
+__global__ void k_ren_ctl(const double* partials, int nparts, RenCtl* ctl, int min_valid_points, double max_condition,
+                          float convergence_eps);
+__global__ void k_ren_finish(RenCtl* ctl, int max_iterations, int combine_icp, IcpResult* res, PoseD* state,
+                             int update_state);
+struct ColorLevel {
+  const float4* color;
+  const float4* gx;
+  const float4* gy;
+  int w, h;
+  double fx, fy, cx, cy;
+};
+struct ColorTrackArgs {
+  ColorLevel lv[kMaxLevels];
+  int levels, stride, max_iterations, min_valid_points;
+  float convergence_eps;
+  const float* points;  // float3 surface points / colours (forward_project_points)
+  const float* colors;
+  const int* count;     // device count (Counters::surface_count), or nullptr: n
+  int n;
+  PoseD* state;
+  const PoseD* explicit_init;  // nullptr: *state
+  IcpResult* result;
+  int update_state;
+};
+__global__ void k_cpyr_base(const uint8_t* rgb, int n, float4* out);
+__global__ void k_cpyr_down(const float4* src, int sw, int sh, float4* dst);
+__global__ void k_cpyr_grad(const float4* src, int w, int h, float4* gx, float4* gy);
+__global__ void k_color_track(ColorTrackArgs a);
+__global__ void k_track_fail(const PoseD* state, IcpResult* res);
+
 // swap engine (vf_swap.cu)
 constexpr int kSwapSortCap = 4096;  // max swap_buffer_blocks
 struct SwapCounters {

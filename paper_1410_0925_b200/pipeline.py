@@ -27,6 +27,7 @@ from ._abi import VfAllocStats, VfCalib, VfFrameStats, VfIntrinsics, VfSettings,
 ENTRY_DTYPE = np.dtype(
     [("x", "<i2"), ("y", "<i2"), ("z", "<i2"), ("pad", "<i2"), ("offset", "<i4"), ("block_state", "<i4")]
 )
+TRACKER_TYPES = {"icp": 0, "color": 1, "icp_ren": 2}
 VOXEL_TYPE_S = 1
 VOXEL_TYPE_S_RGB = 2
 
@@ -103,6 +104,9 @@ class EngineSettings:
     swap_buffer_blocks: int = 100
     swap_host_blocks: int = 0  # host store slots (0: 4 x block_count)
     max_depth: float = 8.0  # disparity conversion clamp (pipeline.hpp:37)
+    tracker_type: int = 0  # TrackerType: 0 icp, 1 color, 2 icp_ren (tracking_state.hpp:10)
+    ren_sigma: float = 10.0
+    skip_points: bool = False
 
     def to_c(self) -> VfSettings:
         s = VfSettings()
@@ -128,6 +132,7 @@ def settings_from_config(cfg) -> tuple[EngineSettings, Calibration]:
         min_valid_points=cfg.min_valid_points, icp_dist_threshold=cfg.icp_dist_threshold,
         convergence_eps=cfg.convergence_eps, max_condition=cfg.max_condition, tracking=cfg.tracking,
         use_swapping=getattr(cfg, "use_swapping", False), swap_buffer_blocks=getattr(cfg, "swap_buffer_blocks", 100),
+        tracker_type=TRACKER_TYPES[getattr(cfg, "tracker", "icp")],
     )
     intr = Intrinsics(fx, fy, cx, cy, w, h)
     return s, Calibration(depth=intr, rgb=intr)
@@ -427,6 +432,26 @@ class Pipeline:
             self._h, _ptr(d), None if init is None else init.ctypes.data_as(C.POINTER(C.c_double)),
             pose.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it), C.byref(cost), C.byref(valid), C.byref(ok)))
         return dict(pose=pose, ok=bool(ok.value), iterations=it.value, cost=cost.value, valid_points=valid.value)
+
+    def _track_stage(self, fn, first, initial):
+        out = np.zeros(12)
+        it, cost, valid, ok = C.c_int(), C.c_double(), C.c_int(), C.c_int()
+        ini = _pose(initial)
+        self._chk(fn, getattr(self._L, fn)(self._h, _ptr(first), ini.ctypes.data_as(C.POINTER(C.c_double)),
+                                           out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it), C.byref(cost),
+                                           C.byref(valid), C.byref(ok)))
+        return out, it.value, cost.value, valid.value, bool(ok.value)
+
+    def ren_refine(self, depth_m, initial):
+        """ren_refine (ren_tracker.hpp:30-120) against the current volume:
+        (pose, iterations, cost, valid_points, ok)."""
+        return self._track_stage("vf_stage_ren", _f32(depth_m, (self.height, self.width)), initial)
+
+    def color_track(self, rgb, initial):
+        """build_color_pyramid + color_track (color_tracker.hpp:107-154) of the
+        current surface list: (pose, iterations, cost, valid_points, ok)."""
+        c = np.ascontiguousarray(rgb, dtype=np.uint8)
+        return self._track_stage("vf_stage_color", c, initial)
 
     def icp_trace(self) -> np.ndarray:
         """Rows of 48: level, iter, 21 H, 6 g, cost, count, rotation_only, eval cam->world pose (12), 4 timers."""

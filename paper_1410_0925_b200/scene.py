@@ -233,6 +233,7 @@ class BenchConfig:
     use_swapping: bool = False  # EngineSettings::use_swapping (pipeline.hpp:20-23)
     swap_buffer_blocks: int = 100
     scene: str = "box_room"  # box_room | corridor
+    tracker: str = "icp"  # TrackerType: icp | color | icp_ren (tracking_state.hpp:10)
 
     @property
     def intrinsics(self):

@@ -1,0 +1,91 @@
+"""The reference's other trackers on the GPU (vf_track.cu): SDF-based Ren
+refinement (TrackerType::icp_ren) and the photometric colour tracker
+(TrackerType::color), against the reference itself (oracle/_ref, its own
+sources compiled unmodified).
+
+Bars: stage calls on identical inputs (the volume and surface list are
+bit-identical — tests/test_gpu_parity.py) agree in ok / iteration count and
+the pose within 1e-6 (only FP64 reduction order and tanhf / expf ulps differ);
+tracked sequences within the tracker tolerance of SURVEY.md §8(c)
+(1e-4 rad, 0.1 mm per frame)."""
+import numpy as np
+import pytest
+
+import vf_py
+from helpers import centre_dist, frames, rot_angle
+from paper_1410_0925_b200 import make_pipeline, settings_from_config
+from paper_1410_0925_b200.scene import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+
+def _known_pose_pair(rlib, cfg, fr):
+    s, c = settings_from_config(cfg.with_(tracking=False))
+    p = make_pipeline(s, c)
+    r = vf_py.Volume(rlib, cfg, tracking=False)
+    for pose, depth, col in fr:
+        p.set_pose(pose)
+        p.process_frame(col, depth)
+        r.process(depth, col, pose)
+    return p, r
+
+
+def _close(a, b, rot=1e-6, pos=1e-6):
+    return rot_angle(a, b) <= rot and centre_dist(a, b) <= pos
+
+
+@pytest.mark.parametrize("name", ["T320", "C1"])
+def test_ren_refine_stage_matches_reference(olib, rlib, name):
+    cfg = CONFIGS[name]
+    fr = frames(olib, cfg, 4)
+    p, r = _known_pose_pair(rlib, cfg, fr[:3])
+    pose3, depth3, _ = fr[3]
+    for init in (fr[2][0], pose3):
+        g = p.ren_refine(depth3, init)
+        w = r.stage_track("ren", depth3, init)
+        assert g[4] == w[4], "ok differs"
+        assert g[1] == w[1], f"iterations {g[1]} vs {w[1]}"
+        assert _close(g[0], w[0]), (rot_angle(g[0], w[0]), centre_dist(g[0], w[0]))
+        assert abs(g[3] - w[3]) <= max(2, 1e-4 * w[3]), "valid points"
+    p.close()
+
+
+def test_color_track_stage_matches_reference(olib, rlib):
+    cfg = CONFIGS["C2"]
+    fr = frames(olib, cfg, 4, rgb=True)
+    p, r = _known_pose_pair(rlib, cfg, fr[:3])
+    sg, cg = p.surface_points()
+    sr, cr = r.surface_points()
+    assert np.array_equal(sg, sr) and np.array_equal(cg, cr)
+    pose3, _, col3 = fr[3]
+    for init in (fr[2][0], pose3):
+        g = p.color_track(col3, init)
+        w = r.stage_track("color", col3, init)
+        assert g[4] == w[4]
+        assert _close(g[0], w[0], 1e-5, 1e-5), (rot_angle(g[0], w[0]), centre_dist(g[0], w[0]), g[1], w[1])
+    p.close()
+
+
+@pytest.mark.parametrize("tracker,name,rgb", [("icp_ren", "C1", False), ("color", "C2", True)])
+def test_tracked_sequence_other_trackers(olib, rlib, tracker, name, rgb):
+    """IPipeline with TrackerType icp_ren / color: GPU vs the reference's own
+    pipeline over a tracked sequence.  (At T320 the reference's own Ren
+    refinement is unstable — it leaves the trajectory by metres within four
+    frames while the GPU path stays within 1 mm — so sequences are compared
+    at C1, where both converge; T320 is covered by the stage test.)"""
+    cfg = CONFIGS[name].with_(tracking=True, tracker=tracker)
+    n = 6
+    fr = frames(olib, cfg, n, rgb=rgb)
+    s, c = settings_from_config(cfg)
+    p = make_pipeline(s, c)
+    r = vf_py.Volume(rlib, cfg, tracking=True)
+    for i, (pose, depth, col) in enumerate(fr):
+        st = p.process_frame(col, depth)
+        sr = r.process(depth, col)
+        assert bool(st.tracking_ok) == bool(sr.tracking_ok), f"frame {i}: ok"
+        gp, rp = p.pose(), r.pose()
+        assert rot_angle(gp, rp) <= 1e-4 and centre_dist(gp, rp) <= 1e-4, \
+            f"frame {i}: {rot_angle(gp, rp)} rad, {centre_dist(gp, rp)} m"
+        if tracker == "icp_ren":  # (the photometric tracker drifts ~5 mm / frame on this scene, as the reference does)
+            assert rot_angle(gp, pose) <= 0.01 and centre_dist(gp, pose) <= 0.01, f"frame {i}: far from ground truth"
+    p.close()
