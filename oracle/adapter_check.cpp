@@ -33,6 +33,10 @@ struct vfa_config {  // same layout as vfr_config (oracle/ref_driver.cpp)
   double rgb_fx, rgb_fy, rgb_cx, rgb_cy;
   int rgb_width, rgb_height;
   double rgb_to_depth[12];
+  int use_swapping, swap_buffer_blocks;
+  int tracker_type;
+  float ren_sigma;
+  int skip_points;
 };
 
 // Runs n frames through IPipeline.  engine: 0 = reference make_pipeline,
@@ -63,6 +67,11 @@ int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, c
     s.tracker.icp_dist_threshold = c->icp_dist_threshold;
     s.tracker.convergence_eps = c->convergence_eps;
     s.tracker.max_condition = c->max_condition;
+    s.tracker.type = c->tracker_type == 1 ? TrackerType::color : c->tracker_type == 2 ? TrackerType::icp_ren
+                                                                                      : TrackerType::icp;
+    s.tracker.ren_sigma = c->ren_sigma;
+    s.use_swapping = c->use_swapping != 0;
+    s.swap_buffer_blocks = c->swap_buffer_blocks;
     Calibration k;
     k.depth.fx = c->fx;
     k.depth.fy = c->fy;

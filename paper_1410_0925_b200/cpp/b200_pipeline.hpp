@@ -14,8 +14,8 @@
 // meaning; construction errors are reported with the reference's exception
 // type (std::invalid_argument, pipeline_impl.hpp:55-57), runtime CUDA errors
 // as std::runtime_error.  Scope: hash backend, VoxelS /
-// VoxelSRgb, ICP tracker, host swapping, raw disparity input; the dense
-// backend, float voxels and the colour / Ren trackers raise
+// VoxelSRgb, the ICP / colour / ICP+Ren trackers, host swapping, raw
+// disparity input; the dense backend and float voxels raise
 // std::invalid_argument.
 #pragma once
 
@@ -76,8 +76,8 @@ inline vf_settings to_vf_settings(const voxfuse::EngineSettings& s) {
     throw std::invalid_argument("voxfuse_b200: only the voxel-block hash backend is implemented");
   if (s.voxel_type != VoxelType::s && s.voxel_type != VoxelType::s_rgb)
     throw std::invalid_argument("voxfuse_b200: voxel types VoxelS and VoxelSRgb only");
-  if (s.tracker.type != TrackerType::icp)
-    throw std::invalid_argument("voxfuse_b200: only the ICP depth tracker is implemented");
+  if (s.tracker.type == TrackerType::color && s.voxel_type != VoxelType::s_rgb)
+    throw std::invalid_argument("colour tracker requires a voxel type with colour information");
   vf_settings c;
   vf_default_settings(&c);
   c.voxel_type = s.voxel_type == VoxelType::s_rgb ? VF_VOXEL_S_RGB : VF_VOXEL_S;
@@ -105,6 +105,11 @@ inline vf_settings to_vf_settings(const voxfuse::EngineSettings& s) {
   c.use_swapping = s.use_swapping ? 1 : 0;  // swap.hpp; host store in pinned, device-mapped memory
   c.swap_buffer_blocks = s.swap_buffer_blocks;
   c.max_depth = s.max_depth;
+  c.tracker_type = s.tracker.type == TrackerType::color     ? VF_TRACKER_COLOR
+                   : s.tracker.type == TrackerType::icp_ren ? VF_TRACKER_ICP_REN
+                                                            : VF_TRACKER_ICP;
+  c.ren_sigma = s.tracker.ren_sigma;
+  c.skip_points = s.tracker.skip_points ? 1 : 0;
   return c;
 }
 
