@@ -381,6 +381,16 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
   return VF_OK;
 }
 
+// render_maps (raycast.hpp:415-435) over the current range image.
+int launch_raycast(vf_ctx* c, cudaStream_t st) {
+  const vf_settings& s = c->s;
+  const uint32_t* vox = reinterpret_cast<const uint32_t*>(c->voxels);
+  k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->ranges, &c->dstate->fp,
+                                                             c->din, s.voxel_size, s.mu, c->points, c->normals);
+  VF_CUDA(c, cudaGetLastError());
+  return VF_OK;
+}
+
 // Integration CTAs per SM (VF_INT_GRID_MULT overrides, for tuning runs).
 int int_grid_mult() {
   static const int m = [] {
@@ -461,9 +471,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
                                              s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
   }
   VF_LAUNCHED(c, "k_ranges");
-  k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
-                                                             c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
-                                                             s.voxel_size, s.mu, c->points, c->normals);
+  if (int rc = launch_raycast(c, st)) return rc;
   VF_LAUNCHED(c, "k_raycast");
   launches += 2;
   if (c->nccl_comm) {  // nearest-depth composite across the GPUs (vf_shard.cu)
@@ -1407,9 +1415,7 @@ int vf_stage_raycast(vf_ctx* c, const double pose[12]) {
   k_init_ranges<<<(c->frag_w * c->frag_h + 255) / 256, 256, 0, st>>>(c->ranges, c->frag_w * c->frag_h);
   k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
                                            s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
-  k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
-                                                         c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
-                                                         s.voxel_size, s.mu, c->points, c->normals);
+  if (int rc = launch_raycast(c, st)) return rc;
   VF_CUDA(c, cudaGetLastError());
   VF_CUDA(c, cudaStreamSynchronize(st));
   c->maps_valid = true;
