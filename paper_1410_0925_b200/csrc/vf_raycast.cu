@@ -93,11 +93,11 @@ __device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { retu
 // 16-byte lookups are conflict-free.  The way is the parity of the block
 // coordinates, so the 2x2x2 blocks a trilinear stencil can straddle never
 // evict each other.
+template <int kStride>  // 32-bit words per voxel: 1 (VoxelS) or 2 (VoxelSRgb)
 struct Sampler {
   HashView hv;
   const uint32_t* vox;  // first 4 bytes of each voxel: sdf (lo 16), w_depth (byte 2)
-  int stride;           // 32-bit words per voxel: 1 (VoxelS) or 2 (VoxelSRgb)
-  int4* cache;          // this thread's column of the shared cache
+  int4* cache;          // this thread's column of the shared cache: (block, first word of the block or -1)
 
   __device__ __forceinline__ void init() {
 #pragma unroll
@@ -107,12 +107,13 @@ struct Sampler {
     const int w = (x & 1) | ((y & 1) << 1) | ((z & 1) << 2);
     const int4 c = cache[w * kRayThreads];
     if (c.x == x && c.y == y && c.z == z) return c.w;
-    const int s = probe(hv, x, y, z);
+    const int slot = probe(hv, x, y, z);
+    const int s = slot < 0 ? -1 : slot * (kBlockVolume * kStride);
     cache[w * kRayThreads] = make_int4(x, y, z, s);
     return s;
   }
-  __device__ __forceinline__ uint32_t raw(int slot, int lx, int ly, int lz) const {
-    return __ldg(vox + ((size_t)slot * kBlockVolume + (lx + ly * kBlockSide + lz * kBlockSide * kBlockSide)) * stride);
+  __device__ __forceinline__ uint32_t raw(int base, int lx, int ly, int lz) const {
+    return __ldg(vox + (unsigned)(base + (lx + ly * kBlockSide + lz * kBlockSide * kBlockSide) * kStride));
   }
 
   // HashSdfSampler::read (raycast.hpp:73-76)
@@ -123,7 +124,7 @@ struct Sampler {
       return false;
     }
     const uint32_t r = raw(s, vx & 7, vy & 7, vz & 7);
-    value = sdf_to_float((int16_t)(r & 0xFFFFu));
+    value = sdf_bits_to_float(r);
     return ((r >> 16) & 0xFFu) > 0;
   }
 
@@ -150,7 +151,7 @@ struct Sampler {
     for (int corner = 0; corner < 8; ++corner) {
       const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
       if (((r[corner] >> 16) & 0xFFu) == 0) return __int_as_float(0x7fffffff);
-      const float v = sdf_to_float((int16_t)(r[corner] & 0xFFFFu));
+      const float v = sdf_bits_to_float(r[corner]);
       const float w = (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz);
       value += w * v;
     }
@@ -179,7 +180,8 @@ struct Sampler {
 
 // cast_ray (raycast.hpp:171-263) from the ray's start point and unit
 // direction in voxel units.  Returns the hit in metres.
-__device__ __forceinline__ bool march(Sampler& smp, F3 start, F3 dir, float total, float mu_vox, float vs, F3& hw) {
+template <typename TSampler>
+__device__ __forceinline__ bool march(TSampler& smp, F3 start, F3 dir, float total, float mu_vox, float vs, F3& hw) {
   const float fine_step = (8.0f < mu_vox) ? 8.0f : mu_vox;
   int state = 0;  // 0 coarse, 1 fine, 2 surface
   float t = 0.0f, t_front = -1.0f, sdf_front = 1.0f;
@@ -249,14 +251,14 @@ __device__ __forceinline__ bool march(Sampler& smp, F3 start, F3 dir, float tota
 
 // K3b: render_maps (raycast.hpp:415-435).  128-thread CTAs cover half a
 // 16x16 fragment (16 x 8 pixels), so every CTA reads one range.
-__global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS) k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride,
-                                                    const float2* __restrict__ ranges,
-                                                    const FrameParams* __restrict__ fp, IntrD in, float vs, float mu,
-                                                    float4* __restrict__ points, float4* __restrict__ normals) {
+template <int kStride>
+__device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t* __restrict__ vox,
+                                             const float2* __restrict__ ranges, const FrameParams* __restrict__ fp,
+                                             const IntrD& in, float vs, float mu, float4* __restrict__ points,
+                                             float4* __restrict__ normals, int4* s_cache) {
   const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
   const int x = fxi * kFragmentSize + (threadIdx.x & 15);
   const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (threadIdx.x >> 4);
-  __shared__ int4 s_cache[kCacheWays * kRayThreads];
   if (x >= in.width || y >= in.height) return;
   const size_t pix = (size_t)y * in.width + x;
   const float2 range = __ldg(ranges + fyi * gridDim.x + fxi);
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS) k_raycast(Hash
   float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
   if (total > 0) {
     dir = F3{dir.x / total, dir.y / total, dir.z / total};
-    Sampler smp{hv, vox, vstride, s_cache + threadIdx.x};
+    Sampler<kStride> smp{hv, vox, s_cache + threadIdx.x};
     smp.init();
     F3 hw;
     if (march(smp, start, dir, total, mu / vs, vs, hw)) {
@@ -290,6 +292,17 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS) k_raycast(Hash
   }
   points[pix] = out_p;
   normals[pix] = out_n;
+}
+
+__global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
+    k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
+              const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
+              float4* __restrict__ normals) {
+  __shared__ int4 s_cache[kCacheWays * kRayThreads];
+  if (vstride == 1)
+    raycast_body<1>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
+  else
+    raycast_body<2>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
 }
 
 }  // namespace vf
