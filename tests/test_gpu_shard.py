@@ -106,3 +106,41 @@ def test_nccl_composite_plumbing_single_rank(olib):
     a, b = ref.tracking_state(), p.tracking_state()
     assert np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
     assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+
+
+def test_sharded_corridor_with_swapping(olib):
+    """Config 5 on the config-4 scene: the corridor walk sharded over 4 virtual
+    shards, each with its own swap engine and host store.  Known poses: the
+    composited maps match the unsharded swapping volume (swapping changes
+    nothing in the agreement — tools/shard_corridor_diag.py).  Tracked: the
+    replicated ICP follows the walk with every shard paging blocks out."""
+    from dataclasses import replace
+    from paper_1410_0925_b200.scene import corridor_trajectory, scene_for
+    cfg = CONFIGS["C4"]
+    spheres, planes, far = scene_for(cfg)
+    poses = corridor_trajectory(40)
+    depths = [vf_py.render_depth(olib, cfg, p, spheres, planes, 0.05, far) for p in poses]
+    for track in (False, True):
+        s, c = settings_from_config(cfg.with_(tracking=track))
+        s = replace(s, swap_host_blocks=1 << 17)  # 256 MiB of pinned host store per context
+        ref = make_pipeline(s, c) if not track else None
+        grp = LocalShardGroup(s, c, 4, shift=3)
+        outs = 0
+        for i, (pose, d) in enumerate(zip(poses, depths)):
+            if not track:
+                ref.set_pose(pose)
+                grp.set_pose(pose)
+                ref.process_frame(None, d)
+            sts = grp.process_frame(None, d)
+            assert all(st.tracking_ok for st in sts) and all(st.allocation_dropped == 0 for st in sts), i
+            outs += sum(st.swapped_out for st in sts)
+        assert outs > 1000
+        if track:
+            p0 = grp.shards[0].pose()
+            assert all(np.array_equal(g.pose(), p0) for g in grp.shards[1:])
+            assert rot_angle(p0, poses[-1]) < 0.01 and centre_dist(p0, poses[-1]) < 0.02
+        else:
+            hit, pts, nrm = _maps_agreement(ref, grp.shards[0], cfg.voxel_size)
+            assert hit >= 0.99 and pts >= 0.99 and nrm >= 0.97, (hit, pts, nrm)
+            ref.close()
+        grp.close()
