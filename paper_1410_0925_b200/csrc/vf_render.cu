@@ -25,15 +25,32 @@ __device__ __noinline__ F3 sample_color(const HashView hv, const uint32_t* __res
   const float qx = p.x - 0.5f, qy = p.y - 0.5f, qz = p.z - 0.5f;
   const int x0 = __float2int_rz(floorf(qx)), y0 = __float2int_rz(floorf(qy)), z0 = __float2int_rz(floorf(qz));
   const float fx = qx - (float)x0, fy = qy - (float)y0, fz = qz - (float)z0;
+  // the eight corners' slots: one probe when the stencil sits inside one
+  // block, else one per corner; all probes and loads are issued before use
+  int slot[8];
+  if ((x0 & 7) < 7 && (y0 & 7) < 7 && (z0 & 7) < 7) {
+    const int s0 = find_slot(hv, x0 >> 3, y0 >> 3, z0 >> 3);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) slot[c] = s0;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      slot[c] = find_slot(hv, (x0 + (c & 1)) >> 3, (y0 + ((c >> 1) & 1)) >> 3, (z0 + ((c >> 2) & 1)) >> 3);
+  }
+  uint2 vv[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int vx = x0 + (c & 1), vy = y0 + ((c >> 1) & 1), vz = z0 + ((c >> 2) & 1);
+    vv[c] = slot[c] < 0 ? make_uint2(0u, 0u)
+                        : __ldg(reinterpret_cast<const uint2*>(vox) +
+                                ((size_t)slot[c] * kBlockVolume + ((vx & 7) + (vy & 7) * kBlockSide + (vz & 7) * 64)));
+  }
   float sx = 0.0f, sy = 0.0f, sz = 0.0f, wsum = 0.0f;
-#pragma unroll 1
+#pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
     const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-    const int vx = x0 + dx, vy = y0 + dy, vz = z0 + dz;
-    const int s = find_slot(hv, vx >> 3, vy >> 3, vz >> 3);
-    if (s < 0) continue;
-    const uint2 v = __ldg(reinterpret_cast<const uint2*>(vox) +
-                          ((size_t)s * kBlockVolume + ((vx & 7) + (vy & 7) * kBlockSide + (vz & 7) * 64)));
+    if (slot[corner] < 0) continue;
+    const uint2 v = vv[corner];
     if (((v.y >> 16) & 0xFFu) == 0) continue;  // w_color == 0
     const float w = (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz);
     sx += (float)(v.x >> 24) * w;
