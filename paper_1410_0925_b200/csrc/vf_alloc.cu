@@ -29,42 +29,58 @@ constexpr unsigned long long kStepMask = (1ull << kStepBits) - 1ull;
 // false to stop the walk early.
 template <typename Visit>
 __device__ __forceinline__ void dda_cells(const D3 p0, const D3 p1, Visit&& visit) {
-  const double a0[3] = {p0.x, p0.y, p0.z};
-  const double a1[3] = {p1.x, p1.y, p1.z};
-  int cell[3], end[3], step[3];
-  double t_max[3], t_delta[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    cell[a] = __double2int_rz(floor(a0[a]));
-    end[a] = __double2int_rz(floor(a1[a]));
-  }
-  if (!visit(cell[0], cell[1], cell[2], 0)) return;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double d = a1[a] - a0[a];
+  // per-axis state in named registers (an array indexed by the step axis
+  // would live in local memory)
+  int cx = __double2int_rz(floor(p0.x)), cy = __double2int_rz(floor(p0.y)), cz = __double2int_rz(floor(p0.z));
+  const int ex = __double2int_rz(floor(p1.x)), ey = __double2int_rz(floor(p1.y)), ez = __double2int_rz(floor(p1.z));
+  if (!visit(cx, cy, cz, 0)) return;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  auto setup = [&](double a0, double a1, int cell, int& step, double& t_max, double& t_delta) {
+    const double d = a1 - a0;
     if (d > 0) {
-      step[a] = 1;
-      t_max[a] = (cell[a] + 1 - a0[a]) / d;
-      t_delta[a] = 1.0 / d;
+      step = 1;
+      t_max = (cell + 1 - a0) / d;
+      t_delta = 1.0 / d;
     } else if (d < 0) {
-      step[a] = -1;
-      t_max[a] = (cell[a] - a0[a]) / d;
-      t_delta[a] = -1.0 / d;
+      step = -1;
+      t_max = (cell - a0) / d;
+      t_delta = -1.0 / d;
     } else {
-      step[a] = 0;
-      t_max[a] = __longlong_as_double(0x7ff0000000000000ll);
-      t_delta[a] = __longlong_as_double(0x7ff0000000000000ll);
+      step = 0;
+      t_max = inf;
+      t_delta = inf;
     }
-  }
-  const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
-  for (int i = 0; i < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++i) {
+  };
+  int sx, sy, sz;
+  double tmx, tmy, tmz, tdx, tdy, tdz;
+  setup(p0.x, p1.x, cx, sx, tmx, tdx);
+  setup(p0.y, p1.y, cy, sy, tmy, tdy);
+  setup(p0.z, p1.z, cz, sz, tmz, tdz);
+  const int max_steps = abs(ex - cx) + abs(ey - cy) + abs(ez - cz) + 3;
+  for (int i = 0; i < max_steps && (cx != ex || cy != ey || cz != ez); ++i) {
+    // ties pick the lower axis (strict <, allocation.hpp:89-90)
     int axis = 0;
-    if (t_max[1] < t_max[axis]) axis = 1;
-    if (t_max[2] < t_max[axis]) axis = 2;
-    if (t_max[axis] > 1.0) break;
-    cell[axis] += step[axis];
-    t_max[axis] += t_delta[axis];
-    if (!visit(cell[0], cell[1], cell[2], i + 1)) return;
+    double tm = tmx;
+    if (tmy < tm) {
+      axis = 1;
+      tm = tmy;
+    }
+    if (tmz < tm) {
+      axis = 2;
+      tm = tmz;
+    }
+    if (tm > 1.0) break;
+    if (axis == 0) {
+      cx += sx;
+      tmx += tdx;
+    } else if (axis == 1) {
+      cy += sy;
+      tmy += tdy;
+    } else {
+      cz += sz;
+      tmz += tdz;
+    }
+    if (!visit(cx, cy, cz, i + 1)) return;
   }
 }
 
@@ -142,20 +158,23 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
     if (!mine) return;
   }
   const unsigned long long key_base = (unsigned long long)(pixel + 1) << kStepBits;
-  dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
-    if (find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0) {
-      if ((unsigned long long)step > kStepMask) {
-        atomicOr(&ctr->error_flags, kErrDdaSteps);
-        return true;
-      }
-      const uint32_t bucket = hash_block(cx, cy, cz, hv.mask);
-      const unsigned long long old = atomicMax(req_key + bucket, key_base | (unsigned long long)step);
-      if (old == 0ull) {
-        atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
-        const int pos = atomicAdd(&ctr->n_marked, 1);
-        if (pos < kSortCap) req_marked[pos] = (int)bucket;
-      }
+  // a missing block: bid for its bucket (the winning key reproduces the
+  // reference's single-worker last writer)
+  auto request = [&](int cx, int cy, int cz, int step) {
+    if ((unsigned long long)step > kStepMask) {
+      atomicOr(&ctr->error_flags, kErrDdaSteps);
+      return;
     }
+    const uint32_t bucket = hash_block(cx, cy, cz, hv.mask);
+    const unsigned long long old = atomicMax(req_key + bucket, key_base | (unsigned long long)step);
+    if (old == 0ull) {
+      atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
+      const int pos = atomicAdd(&ctr->n_marked, 1);
+      if (pos < kSortCap) req_marked[pos] = (int)bucket;
+    }
+  };
+  dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
+    if (find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0) request(cx, cy, cz, step);
     return true;
   });
 }
