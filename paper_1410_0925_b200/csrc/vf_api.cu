@@ -174,8 +174,16 @@ HashView hash_view(vf_ctx* c) { return HashView{c->entries, c->mask, c->s.bucket
 
 // first_level 1: icp_track on the pyramid without its full-resolution level
 // (the icp_ren tracker, pipeline_impl.hpp:189-195).
+bool frame_trace() {
+  static const bool on = std::getenv("VF_ICP_TRACE") != nullptr;
+  return on;
+}
+
+// trace: record the per-iteration sums and phase timers (vf_icp_trace) —
+// always for stage calls, in frames only with VF_ICP_TRACE set (the extra
+// stores sit on the critical path of CTA 0 between grid barriers).
 int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool update_state = true,
-               int first_level = 0) {
+               int first_level = 0, bool trace = true) {
   IcpArgs a{};
   const int L = c->s.hierarchy_levels - first_level;
   size_t off = 0;
@@ -210,7 +218,7 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
   a.update_state = update_state ? 1 : 0;
   a.result = &c->dstate->icp;
   a.partials = c->partials;
-  a.trace = c->trace;
+  a.trace = trace ? c->trace : nullptr;
   a.trace_cap = kTraceCap;
   a.max_slots = c->icp_slots;
   a.ctl_io = c->icp_ctl;
@@ -367,7 +375,7 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
   }
   if (s.tracker_type == VF_TRACKER_ICP_REN) {
     if (s.hierarchy_levels > 1) {
-      if (int rc = launch_icp(c, st, false, /*update_state=*/false, /*first_level=*/1)) return rc;
+      if (int rc = launch_icp(c, st, false, /*update_state=*/false, /*first_level=*/1, frame_trace())) return rc;
       ++*launches;
     } else {
       k_track_fail<<<1, 32, 0, st>>>(&c->dstate->pose, &c->dstate->icp);
@@ -375,7 +383,7 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
     }
     return enqueue_ren(c, st, true, explicit_init, update_state, launches);
   }
-  if (int rc = launch_icp(c, st, false, update_state)) return rc;
+  if (int rc = launch_icp(c, st, false, update_state, 0, frame_trace())) return rc;
   VF_LAUNCHED(c, "k_icp");
   ++*launches;
   return VF_OK;

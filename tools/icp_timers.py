@@ -1,4 +1,6 @@
-"""ICP per-iteration phase timers (SM cycles) inside a normal tracked frame."""
+"""ICP per-iteration phase timers (SM cycles) inside a normal tracked frame (run with VF_ICP_TRACE=1)."""
+import os
+os.environ.setdefault("VF_ICP_TRACE", "1")
 import sys
 sys.path.insert(0, '.'); sys.path.insert(0, 'oracle'); sys.path.insert(0, 'tests')
 import numpy as np
