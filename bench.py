@@ -18,8 +18,14 @@ once, outside the timed region.
 * cpu_baseline: the reference's own code (oracle/_ref, shim-built) on the
   host cores, bounded sample, rank 0 at N=1 only.
 * --impl reference: that CPU reference as the arm of record.
-Under torchrun (N>1) every rank runs an independent replica on its own GPU
-(scaling "weak"); the sharded large-scene configuration is not built yet.
+Under torchrun (N>1), by default every rank runs its own copy of the camera
+sequence on its own GPU — the frames of one sequence are sequential (each is tracked
+against the previous frame's raycast), so sequences are the units sharded
+across ranks, with no data-path collective ("scaling": "weak").  --mode shard
+runs config 5 instead: one volume spatially sharded by block hash across the
+GPUs, every rank on the same frames, maps composited per pixel with NCCL
+inside the frame graph; that adds capacity, not frames/s, and is reported as
+"strong".
 """
 from __future__ import annotations
 
@@ -52,8 +58,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--l2-flush-mib", type=int, default=256)
-    ap.add_argument("--mode", default="shard", choices=["shard", "replica"],
-                    help="N>1: shard one volume across the GPUs (config 5) or run independent replicas")
+    ap.add_argument("--mode", default="replica", choices=["shard", "replica"],
+                    help="N>1: independent sequences per GPU (default) or one volume sharded across the GPUs "
+                         "(config 5, NCCL map composite)")
     return ap.parse_args()
 
 
@@ -241,7 +248,8 @@ def run_ours(args, dist: Dist):
 
     L = _abi.load()
     cfg = CONFIGS[args.config]
-    device = dist.local_rank
+    # VF_BENCH_ONE_DEVICE=1 puts every rank on GPU 0 (exercises the N>1 plumbing on a one-GPU box)
+    device = 0 if os.environ.get("VF_BENCH_ONE_DEVICE") else dist.local_rank
     fx, fy, cx, cy, w, h = cfg.intrinsics
     intr = Intrinsics(fx, fy, cx, cy, w, h)
     rgb = cfg.voxel_type == 2
@@ -389,7 +397,8 @@ def run_ours(args, dist: Dist):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TSDF/raycast) + f64 (allocation DDA, ICP)",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": "f32 (TSDF/raycast) + f64 (allocation DDA, ICP)",
         "data": (f"synthetic (GPU-rendered corridor + pillars, {n_frames}-frame walk at 5 cm/frame)"
                  if cfg.scene == "corridor" else
                  "synthetic (GPU-rendered box room + spheres, 100-frame small-motion trajectory)"),
@@ -399,7 +408,7 @@ def run_ours(args, dist: Dist):
                         f"+{cfg.hash.excess_count} / {cfg.hash.block_count} blocks, "
                         f"{'ICP tracking on' if cfg.tracking else 'known poses'}",
             "parallelism": (f"volume sharded by block hash over {dist.world} GPUs (NCCL map composite)" if sharded
-                            else f"replicas x{dist.world}" if dist.world > 1 else "single GPU"),
+                            else f"one sequence per GPU x{dist.world}" if dist.world > 1 else "single GPU"),
             "l2": f"flushed between frames ({args.l2_flush_mib} MiB write, outside the timed intervals)",
             "graphs": True,
         },
