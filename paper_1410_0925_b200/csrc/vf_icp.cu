@@ -210,6 +210,12 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
     __syncthreads();
     for (int iter = 0; iter < a.max_iterations; ++iter) {
       long long t0 = timer ? clock64() : 0;
+#ifdef VF_ICP_FINE_TIMERS
+      long long tf[6] = {0, 0, 0, 0, 0, 0};  // staging, transforms, taps, terms, warp reduce, CTA sum
+#define VF_TF(i) if (timer && k0 == 0) tf[i] = clock64()
+#else
+#define VF_TF(i)
+#endif
       const PoseD c2w = ctl.c2w;
       const PoseD render = ctl.render;
       const D3 rc = rotation_only ? mk(c2w.t[0], c2w.t[1], c2w.t[2]) : mk(0, 0, 0);
@@ -240,6 +246,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
             uy[k] = s_uy[y];
           }
         }
+        VF_TF(0);
         D3 pw[2];
         bool ok[2];
         int ix[2], iy[2];
@@ -260,6 +267,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           fx[k] = u - ix[k];
           fy[k] = v - iy[k];
         }
+        VF_TF(1);
         float4 tp[2][4], tn[2][4];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -277,6 +285,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
+          if (k == 0) VF_TF(2);
           if (!ok[k]) continue;
           D3 mp, mn;
           if (!bilinear_taps(tp[k], fx[k], fy[k], a.dist_thr, mp)) continue;
@@ -308,6 +317,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           acc[27] = fma(r, r, acc[27]);
           acc[28] += 1.0;
         }
+        VF_TF(3);
       }
       // CTA reduction: transpose butterfly inside each warp, then one warp
       // combines the warp sums.
@@ -316,6 +326,9 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v32[i] = i < kAcc ? acc[i] : 0.0;
         const double mine = warp_reduce32(v32);
+#ifdef VF_ICP_FINE_TIMERS
+        if (timer) tf[4] = clock64();
+#endif
         s_red[warp][lane] = mine;  // lane l holds value index l
       }
       __syncthreads();
@@ -457,6 +470,11 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           row[45] = (double)(t2 - t1);  // grid barrier
           row[46] = (double)(t3 - t2);  // partial sums
           row[47] = (double)(t4 - t3);  // controller
+#ifdef VF_ICP_FINE_TIMERS
+          // sub-phases of the pixel term pass (first pixel pair of thread 0)
+          for (int i = 0; i < 5; ++i) row[32 + i] = (double)(tf[i] - (i == 0 ? t0 : tf[i - 1]));
+          row[37] = (double)(t1 - tf[4]);
+#endif
         }
       }
       __syncthreads();
