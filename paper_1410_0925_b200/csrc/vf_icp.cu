@@ -222,15 +222,15 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
       double acc[kAcc];
 #pragma unroll
       for (int i = 0; i < kAcc; ++i) acc[i] = 0;
-      // Two pixels per step, each pipeline stage issued for both before it is
+      // kInflight pixels per step, each pipeline stage issued for all before it is
       // consumed, so their memory round trips (depth + tables, then the
       // eight map taps) overlap.
       const int total_slots = (npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride;
-      for (int k0 = 0; k0 < total_slots; k0 += 2) {
-        float d[2];
-        double ux[2], uy[2];
+      for (int k0 = 0; k0 < total_slots; k0 += kInflight) {
+        float d[kInflight];
+        double ux[kInflight], uy[kInflight];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kInflight; ++k) {
           const int slot = k0 + k;
           const int pix = blockIdx.x * blockDim.x + tid + slot * gstride;
           if (slot < nslots) {  // staged in shared memory
@@ -247,12 +247,12 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           }
         }
         VF_TF(0);
-        D3 pw[2];
-        bool ok[2];
-        int ix[2], iy[2];
-        double fx[2], fy[2];
+        D3 pw[kInflight];
+        bool ok[kInflight];
+        int ix[kInflight], iy[kInflight];
+        double fx[kInflight], fy[kInflight];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kInflight; ++k) {
           // unproject (intrinsics.hpp:39-43); (x - cx) / fx is tabulated per level
           const D3 pc = mk(ux[k] * d[k], uy[k] * d[k], (double)d[k]);
           pw[k] = apply(c2w, pc);
@@ -268,9 +268,9 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           fy[k] = v - iy[k];
         }
         VF_TF(1);
-        float4 tp[2][4], tn[2][4];
+        float4 tp[kInflight][4], tn[kInflight][4];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kInflight; ++k) {
           const size_t i00 = (size_t)iy[k] * a.map.width + ix[k];
           if (ok[k]) {
             tp[k][0] = __ldg(a.points + i00);
@@ -284,7 +284,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
           }
         }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kInflight; ++k) {
           if (k == 0) VF_TF(2);
           if (!ok[k]) continue;
           D3 mp, mn;

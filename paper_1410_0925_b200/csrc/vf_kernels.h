@@ -12,7 +12,11 @@ namespace vf {
 #ifndef VF_ICP_MIN_BLOCKS
 #define VF_ICP_MIN_BLOCKS 1
 #endif
+#ifndef VF_ICP_INFLIGHT
+#define VF_ICP_INFLIGHT 2
+#endif
 constexpr int kIcpThreads = VF_ICP_THREADS;
+constexpr int kInflight = VF_ICP_INFLIGHT;  // ICP pixels in flight per thread
 constexpr int kMaxIcpGrid = 512;  // partial-sum loop bound (grid <= 512 CTAs)
 constexpr int kMaxLevels = 6;
 
