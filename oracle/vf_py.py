@@ -106,7 +106,7 @@ def make_config(cfg) -> Config:
     c.voxel_size = cfg.voxel_size
     c.mu = cfg.mu
     c.max_weight = cfg.max_weight
-    c.stop_integrating_at_max = 0
+    c.stop_integrating_at_max = 1 if getattr(cfg, "stop_integrating_at_max", False) else 0
     c.bucket_count = cfg.hash.bucket_count
     c.bucket_size = cfg.hash.bucket_size
     c.excess_count = cfg.hash.excess_count

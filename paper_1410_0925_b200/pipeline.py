@@ -125,6 +125,7 @@ def settings_from_config(cfg) -> tuple[EngineSettings, Calibration]:
     fx, fy, cx, cy, w, h = cfg.intrinsics
     s = EngineSettings(
         voxel_type=cfg.voxel_type, voxel_size=cfg.voxel_size, mu=cfg.mu, max_weight=cfg.max_weight,
+        stop_integrating_at_max=getattr(cfg, "stop_integrating_at_max", False),
         bucket_count=cfg.hash.bucket_count, bucket_size=cfg.hash.bucket_size, excess_count=cfg.hash.excess_count,
         block_count=cfg.hash.block_count, near_clip=cfg.near_clip, far_clip=cfg.far_clip,
         visibility_margin_px=cfg.margin_px, swap_margin_px=cfg.swap_margin_px, hierarchy_levels=cfg.levels,

@@ -219,6 +219,7 @@ class BenchConfig:
     frames: int = 100
     hash: HashConfig = field(default_factory=HashConfig)
     max_weight: int = 100
+    stop_integrating_at_max: bool = False  # SceneParams (scene_params.hpp:10)
     near_clip: float = 0.1
     far_clip: float = 8.0
     margin_px: int = 8

@@ -1,8 +1,9 @@
 """Edge cases of the frame path against the oracle (bit-exact where the
 reference is defined): frames without valid depth, invalid / extreme depth
 samples, image sizes that are not multiples of the 16-pixel fragment or of
-the pyramid's 2x2 reduction, and the largest configuration (C3, 1280x960,
-2 mm, 2^20 blocks) at full size.
+the pyramid's 2x2 reduction, the largest configuration (C3, 1280x960,
+2 mm, 2^20 blocks) at full size, and non-default SceneParams / HashConfig
+(stop_integrating_at_max, one- and four-slot buckets).
 
 Not covered on purpose: NaN / inf depth.  mark_blocks converts
 floor(NaN or inf) to int (allocation.hpp:62-63), undefined behaviour in the
@@ -117,4 +118,29 @@ def test_largest_configuration_frame0_bit_exact(olib):
     assert (st.blocks_allocated, st.visible_blocks) == (so.blocks_allocated, so.visible_blocks)
     assert st.blocks_allocated > 100_000
     _same_state(p, o)
+    p.close()
+
+
+@pytest.mark.parametrize("variant", ["stop_at_max", "bucket1", "bucket4", "rgb_stop_at_max"])
+def test_scene_and_hash_parameters(olib, variant):
+    """Non-default SceneParams / HashConfig: stop_integrating_at_max with a
+    small max_weight (integrate_voxel's early out, integration.hpp:105-107),
+    one- and four-slot buckets (hash_volume.hpp:49-58): known poses,
+    bit-exact over a short sequence."""
+    cfg = CONFIGS["T320"].with_(tracking=False)
+    if variant in ("stop_at_max", "rgb_stop_at_max"):
+        cfg = cfg.with_(max_weight=3, stop_integrating_at_max=True, voxel_type=2 if variant.startswith("rgb") else 1)
+    elif variant == "bucket1":
+        cfg = cfg.with_(hash=HashConfig(bucket_count=1 << 17, bucket_size=1, excess_count=1 << 15, block_count=1 << 15))
+    else:
+        cfg = cfg.with_(hash=HashConfig(bucket_count=1 << 15, bucket_size=4, excess_count=1 << 13, block_count=1 << 15))
+    rgb = cfg.voxel_type == 2
+    vsize = 8 if rgb else 4
+    p, o = _pair(olib, cfg, False)
+    for pose, d, col in frames(olib, cfg, 6, rgb=rgb):
+        p.set_pose(pose)
+        st = p.process_frame(col, d)
+        so = o.process(d, col, pose)
+        assert (st.blocks_allocated, st.visible_blocks) == (so.blocks_allocated, so.visible_blocks)
+        _same_state(p, o, vsize)
     p.close()
