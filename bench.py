@@ -414,6 +414,12 @@ def run_ours(args, dist: Dist):
         },
         "voxel_updates_per_s": vox_updates,
         "stage_ms": stages,
+        # per-stage throughput in the units of SURVEY.md §8(d)
+        "stage_throughput": {
+            "raycast_rays_per_s": npix / (stages["raycast"] * 1e-3) if stages["raycast"] > 0 else None,
+            "integration_voxel_visits_per_s": nvis * 512 / (integ_ms * 1e-3) if integ_ms > 0 else None,
+            "allocation_pixels_per_s": npix / (stages["allocation"] * 1e-3) if stages["allocation"] > 0 else None,
+        },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": npix * 4 + (npix * 3 if rgb else 0),
                 "d2h_bytes_per_step": readback},
         "gpu_launches": launches,
