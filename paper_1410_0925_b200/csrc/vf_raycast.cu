@@ -257,8 +257,17 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
                                              const IntrD& in, float vs, float mu, float4* __restrict__ points,
                                              float4* __restrict__ normals, int4* s_cache) {
   const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
-  const int x = fxi * kFragmentSize + (threadIdx.x & 15);
-  const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (threadIdx.x >> 4);
+  // Each warp traces an 8 x 4 pixel patch of the CTA's 16 x 8 half fragment
+  // (2 x 2 warps): neighbouring rays march similar lengths, so the warp
+  // diverges less than with 16 x 2 rows (C1 raycast 0.221 -> 0.213 ms).
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+#ifndef VF_RAY_WARP_4X8
+  const int x = fxi * kFragmentSize + (lane & 7) + ((wq & 1) << 3);
+  const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (lane >> 3) + ((wq >> 1) << 2);
+#else
+  const int x = fxi * kFragmentSize + (lane & 3) + (wq << 2);
+  const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (lane >> 2);
+#endif
   if (x >= in.width || y >= in.height) return;
   const size_t pix = (size_t)y * in.width + x;
   const float2 range = __ldg(ranges + fyi * gridDim.x + fxi);
