@@ -132,12 +132,16 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
     }
   }
   __syncthreads();
-  const int npix = in.width * in.height;
-  const int pixel = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pixel >= npix) return;
+  // CTA = 32 x 8 pixel tile, warp = 8 x 4 patch: neighbouring rays walk the
+  // same blocks (probe locality) and similar numbers of cells (divergence)
+  const int tiles_x = (in.width + 31) >> 5;
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int x = (int)(blockIdx.x % tiles_x) * 32 + ((wq & 3) << 3) + (lane & 7);
+  const int y = (int)(blockIdx.x / tiles_x) * 8 + ((wq >> 2) << 2) + (lane >> 3);
+  if (x >= in.width || y >= in.height) return;
+  const int pixel = y * in.width + x;
   const float d = __ldg(depth + pixel);
   if (d <= 0.0f) return;
-  const int y = pixel / in.width, x = pixel - y * in.width;
   D3 p0, p1;
   pixel_segment(x, y, d, in, s_c2w, voxel_size, mu, p0, p1);
   if (shard.count > 1) {

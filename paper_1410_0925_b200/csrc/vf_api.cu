@@ -399,6 +399,9 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
   return VF_OK;
 }
 
+// k_mark's grid: one thread per pixel, 32 x 8 pixel tiles.
+int mark_grid(const vf_ctx* c) { return ((c->din.width + 31) / 32) * ((c->din.height + 7) / 8); }
+
 // Integration CTAs per SM (VF_INT_GRID_MULT overrides, for tuning runs).
 int int_grid_mult() {
   static const int m = [] {
@@ -419,7 +422,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     if (int rc = enqueue_tracker(c, st, with_rgb, nullptr, true, &launches)) return rc;
   }
   stage_mark(c, 1);
-  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
+  k_mark<<<mark_grid(c), 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
                                                 &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
                                                 c->req_bits, c->req_marked, &c->dstate->ctr);
   VF_LAUNCHED(c, "k_mark");
@@ -1373,7 +1376,7 @@ int vf_stage_allocate(vf_ctx* c, const float* depth_m, const double pose[12], vf
   cudaStream_t st = c->stream;
   if (int rc = upload(c, c->depth, depth_m, sizeof(float) * c->npix, false)) return rc;
   if (int rc = set_pose_dev(c, pose)) return rc;
-  k_mark<<<(c->npix + 255) / 256, 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
+  k_mark<<<mark_grid(c), 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
                                                 &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
                                                 c->req_bits, c->req_marked, &c->dstate->ctr);
   k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
