@@ -1,0 +1,75 @@
+"""C ABI contract on the GPU: status codes for invalid settings and calls in
+the wrong state (the reference throws std::invalid_argument at construction,
+pipeline_impl.hpp:55-57; the hot path never throws — here nothing crosses
+the ABI but a status)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1410_0925_b200 import _abi, make_pipeline, settings_from_config
+from paper_1410_0925_b200._abi import VoxfuseError
+from paper_1410_0925_b200.scene import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+VF_ERR_INVALID, VF_ERR_STATE = -1, -4
+
+
+def _create(**overrides):
+    from dataclasses import replace
+    s, c = settings_from_config(CONFIGS["T160"])
+    return make_pipeline(replace(s, **overrides), c)
+
+
+@pytest.mark.parametrize("overrides", [
+    {"bucket_count": 1000},                      # not a power of two
+    {"voxel_size": 0.0},
+    {"hierarchy_levels": 7},
+    {"tracker_type": 1},                         # colour tracker with VoxelS
+    {"tracker_type": 5},
+    {"use_swapping": True, "swap_buffer_blocks": 5000},
+    {"shard_count": 2, "shard_index": 2},
+])
+def test_invalid_settings_rejected(overrides):
+    with pytest.raises(VoxfuseError) as e:
+        _create(**overrides)
+    assert e.value.status == VF_ERR_INVALID
+
+
+def test_calls_in_the_wrong_state():
+    p = _create()
+    L = _abi.load()
+    out = np.zeros((p.height, p.width, 3), np.uint8)
+    # nothing rendered yet
+    assert L.vf_render_image(p.handle, 0, out.ctypes.data_as(C.c_void_p)) == VF_ERR_STATE
+    assert L.vf_render_image(p.handle, 1, out.ctypes.data_as(C.c_void_p)) == VF_ERR_STATE
+    pts = np.zeros((p.height, p.width, 4), np.float32)
+    assert L.vf_get_maps(p.handle, pts.ctypes.data_as(C.c_void_p), None) == VF_ERR_STATE
+    # swapping off: no store
+    assert L.vf_swap_states(p.handle, out.ctypes.data_as(C.c_void_p)) == VF_ERR_STATE
+    assert L.vf_swap_stored_count(p.handle) == 0
+    # null inputs and unknown modes
+    assert L.vf_process_frame(p.handle, None, None, None) == VF_ERR_INVALID
+    assert L.vf_render_image(p.handle, 9, out.ctypes.data_as(C.c_void_p)) == VF_ERR_INVALID
+    d = np.full((p.height, p.width), 1.5, np.float32)
+    p.process_frame(None, d)
+    # a too-small buffer for the surface list is refused, not overrun
+    assert L.vf_get_surface_points(p.handle, None, None, 0) == 0  # VoxelS: no colour list
+    p.close()
+
+
+def test_surface_list_capacity_checked():
+    s, c = settings_from_config(CONFIGS["C2"])
+    p = make_pipeline(s, c)
+    import vf_py
+    from helpers import frames
+    (pose, depth, col), = frames(vf_py.oracle_lib(), CONFIGS["C2"], 1, rgb=True)
+    p.set_pose(pose)
+    p.process_frame(col, depth)
+    L = _abi.load()
+    n = L.vf_get_surface_points(p.handle, None, None, 0)
+    assert n > 1000
+    buf = np.zeros((n - 1, 3), np.float32)
+    assert L.vf_get_surface_points(p.handle, buf.ctypes.data_as(C.c_void_p), None, n - 1) == VF_ERR_INVALID
+    p.close()
