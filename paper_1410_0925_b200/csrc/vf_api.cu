@@ -71,6 +71,7 @@ struct vf_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // parallel graph branch (k_ranges)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;  // swap-out transfers beside the raycast
   std::string err;
 
   int vsize = 4;
@@ -471,10 +472,20 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     k_swap_select<<<1, 1024, 0, st>>>(c->entries, c->vba_slots, c->sw, s.swap_buffer_blocks,
                                       (c->vsize == 8 ? 7 : 3) * kBlockVolume, &c->dstate->ctr);
     VF_LAUNCHED(c, "k_swap_select");
+    // swap-ins before the raycast (it may read them); swap-outs on the side
+    // stream, overlapping the raycast, joined at the end of the frame
     k_swap_transfer<<<c->num_sms * 2, 256, 0, st>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
-                                                    s.max_weight);
+                                                    s.max_weight, 0);
     VF_LAUNCHED(c, "k_swap_transfer");
-    launches += 3;
+    if (fork) {
+      VF_CUDA(c, cudaEventRecord(c->ev_fork2, st));
+      VF_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork2, 0));
+    }
+    k_swap_transfer<<<c->num_sms * 2, 256, 0, fork ? c->side : st>>>(reinterpret_cast<uint32_t*>(c->voxels),
+                                                                     c->vsize / 4, c->sw, s.max_weight, 1);
+    VF_LAUNCHED(c, "k_swap_transfer");
+    if (fork) VF_CUDA(c, cudaEventRecord(c->ev_join2, c->side));
+    launches += 4;
   }
   stage_mark(c, 4);
   if (!fork) {
@@ -499,6 +510,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     VF_LAUNCHED(c, "k_forward_project");
     ++launches;
   }
+  if (c->swapping && fork) VF_CUDA(c, cudaStreamWaitEvent(st, c->ev_join2, 0));
   stage_mark(c, 5);
   c->launches_last = launches;
   VF_CUDA(c, cudaGetLastError());
@@ -642,6 +654,8 @@ void free_all(vf_ctx* c) {
   if (c->ev_frame1) cudaEventDestroy(c->ev_frame1);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
+  if (c->ev_join2) cudaEventDestroy(c->ev_join2);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -784,7 +798,9 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return VF_ERR_CUDA;
   }
@@ -1720,7 +1736,7 @@ int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
         track = (L > 1 ? 1 : 0) + icp;
     }
   }
-  return 7 + track + (c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 3 : 0);
+  return 7 + track + (c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 4 : 0);
 }
 
 }  // extern "C"

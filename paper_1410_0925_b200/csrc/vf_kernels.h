@@ -198,7 +198,7 @@ __global__ void k_swap_request(const HashEntry* entries, const int* alloc_list, 
                                Counters* ctr);
 __global__ void k_swap_select(HashEntry* entries, int* vba_slots, SwapDev sw, int buffer_blocks, int payload_bytes,
                               Counters* ctr);
-__global__ void k_swap_transfer(uint32_t* voxels, int words_per_voxel, SwapDev sw, int max_weight);
+__global__ void k_swap_transfer(uint32_t* voxels, int words_per_voxel, SwapDev sw, int max_weight, int which);
 
 constexpr int kMaxShards = 16;
 struct ShardGroupArgs {

@@ -273,43 +273,66 @@ __device__ __forceinline__ void fuse(uint32_t h0, uint32_t h1, uint32_t& a0, uin
 
 }  // namespace
 
-// Moves the staged blocks: one warp per block, 16 B per lane per step.
-__global__ void __launch_bounds__(256) k_swap_transfer(uint32_t* __restrict__ voxels, int words_per_voxel,
-                                                       SwapDev sw, int max_weight) {
+// Moves the staged blocks, one warp per block.  which = 0: the swap-ins
+// (host slot read over the link, fused into the fresh device block); they
+// run before the raycast, which may read them.  which = 1: the swap-outs
+// (device block streamed to its host slot, then reset); their entries were
+// unlinked by k_swap_select, so nothing else in the frame reads these blocks
+// and the copy overlaps the raycast on a side stream.
+template <int kWords>
+__device__ __forceinline__ void transfer_block(uint4* dev, uint4* host, bool in, int max_weight) {
+  constexpr int kPerLane = kBlockVolume * kWords / 4 / 32;  // uint4 per lane: 4 (VoxelS) or 8 (VoxelSRgb)
   const int lane = threadIdx.x & 31;
+  uint4 v[kPerLane];
+  if (in) {
+    uint4 h[kPerLane];
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {  // all loads in flight before any use
+      h[k] = __ldcv(host + lane + 32 * k);
+      v[k] = dev[lane + 32 * k];
+    }
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      uint4 a = v[k];
+      if (kWords == 1) {
+        uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;
+        fuse<false>(h[k].x, 0, a.x, d0, max_weight);
+        fuse<false>(h[k].y, 0, a.y, d1, max_weight);
+        fuse<false>(h[k].z, 0, a.z, d2, max_weight);
+        fuse<false>(h[k].w, 0, a.w, d3, max_weight);
+      } else {
+        fuse<true>(h[k].x, h[k].y, a.x, a.y, max_weight);
+        fuse<true>(h[k].z, h[k].w, a.z, a.w, max_weight);
+      }
+      dev[lane + 32 * k] = a;
+    }
+  } else {
+    // TVoxel{} (voxel.hpp:29-30, :44-47)
+    const uint4 def = kWords == 1 ? make_uint4(0x7FFFu, 0x7FFFu, 0x7FFFu, 0x7FFFu) : make_uint4(0x7FFFu, 0u, 0x7FFFu, 0u);
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) v[k] = dev[lane + 32 * k];
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      __stcs(host + lane + 32 * k, v[k]);
+      dev[lane + 32 * k] = def;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_swap_transfer(uint32_t* __restrict__ voxels, int words_per_voxel,
+                                                       SwapDev sw, int max_weight, int which) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int k_in = sw.ctr->staged_in, k_out = sw.ctr->staged_out;
   const int block_words = kBlockVolume * words_per_voxel;
-  for (int r = gw; r < k_in + k_out; r += nw) {
+  const int r0 = which == 0 ? 0 : k_in, r1 = which == 0 ? k_in : k_in + k_out;
+  for (int r = r0 + gw; r < r1; r += nw) {
     uint4* dev = reinterpret_cast<uint4*>(voxels + (size_t)sw.stage_slot[r] * block_words);
     uint4* host = reinterpret_cast<uint4*>(sw.host_pool + (size_t)sw.stage_host[r] * block_words);
-    const int n4 = block_words / 4;
-    if (r < k_in) {
-      // secondary integration: host block fused into the freshly popped one
-      for (int q = lane; q < n4; q += 32) {
-        const uint4 h = __ldcv(host + q);
-        uint4 a = dev[q];
-        if (words_per_voxel == 1) {
-          uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-          fuse<false>(h.x, 0, a.x, d0, max_weight);
-          fuse<false>(h.y, 0, a.y, d1, max_weight);
-          fuse<false>(h.z, 0, a.z, d2, max_weight);
-          fuse<false>(h.w, 0, a.w, d3, max_weight);
-        } else {
-          fuse<true>(h.x, h.y, a.x, a.y, max_weight);
-          fuse<true>(h.z, h.w, a.z, a.w, max_weight);
-        }
-        dev[q] = a;
-      }
-    } else {
-      const uint32_t d = words_per_voxel == 1 ? 0x00007FFFu : 0u;  // TVoxel{} (voxel.hpp:29-30, :44-47)
-      const uint4 def = words_per_voxel == 1 ? make_uint4(d, d, d, d) : make_uint4(0x7FFFu, 0u, 0x7FFFu, 0u);
-      for (int q = lane; q < n4; q += 32) {
-        __stcs(host + q, dev[q]);
-        dev[q] = def;
-      }
-    }
+    if (words_per_voxel == 1)
+      transfer_block<1>(dev, host, which == 0, max_weight);
+    else
+      transfer_block<2>(dev, host, which == 0, max_weight);
   }
 }
 
