@@ -71,7 +71,7 @@ struct vf_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // parallel graph branch (k_ranges)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;  // swap-out transfers beside the raycast
+  cudaEvent_t ev_join2 = nullptr;  // swap-out transfers beside the raycast
   std::string err;
 
   int vsize = 4;
@@ -442,15 +442,39 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   VF_LAUNCHED(c, "k_visible");
   launches += 5;
   stage_mark(c, 2);
-  // k_ranges needs only the visible list and the pose: it runs on a side
-  // stream concurrently with integration (a parallel branch of the graph).
+  // The side stream (a parallel branch of the frame graph) takes the work
+  // that does not touch the blocks being integrated: the range image (it
+  // reads only entry positions) and the whole swap engine — swap-out
+  // candidates are outside the enlarged frustum and swap-in candidates are
+  // swapped out, so neither is on the visible list (visible ⊂ swap-visible,
+  // allocation.hpp:226-233); the VBA stack and the voxels they move are
+  // disjoint from integration's.  Swap-ins join before the raycast (it may
+  // read them); swap-outs join at the end of the frame.
   const bool fork = !c->profiling;
+  cudaStream_t branch = fork ? c->side : st;
+  auto enqueue_swap = [&](cudaStream_t sst) -> int {
+    // request_swap_ins/outs + execute_swap_in/out (pipeline_impl.hpp:104-113)
+    k_swap_request<<<c->num_sms * 4, 256, 0, sst>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
+                                                    s.near_clip, s.far_clip, s.visibility_margin_px, s.swap_margin_px,
+                                                    c->sw, &c->dstate->ctr);
+    VF_LAUNCHED(c, "k_swap_request");
+    k_swap_select<<<1, 1024, 0, sst>>>(c->entries, c->vba_slots, c->sw, s.swap_buffer_blocks,
+                                       (c->vsize == 8 ? 7 : 3) * kBlockVolume, &c->dstate->ctr);
+    VF_LAUNCHED(c, "k_swap_select");
+    k_swap_transfer<<<c->num_sms * 2, 256, 0, sst>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
+                                                     s.max_weight, 0);
+    VF_LAUNCHED(c, "k_swap_transfer");
+    launches += 3;
+    return VF_OK;
+  };
   if (fork) {
     VF_CUDA(c, cudaEventRecord(c->ev_fork, st));
     VF_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     k_ranges<<<c->num_sms * 2, 256, 0, c->side>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp,
                                                   c->din, s.voxel_size, s.near_clip, s.far_clip, c->ranges,
                                                   c->frag_w);
+    if (c->swapping)
+      if (int rc = enqueue_swap(c->side)) return rc;
     VF_CUDA(c, cudaEventRecord(c->ev_join, c->side));
   }
   const bool color = c->vsize == 8;
@@ -462,30 +486,16 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   stage_mark(c, 3);
   if (fork) {
     VF_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+  } else if (c->swapping) {
+    if (int rc = enqueue_swap(st)) return rc;
   }
   if (c->swapping) {
-    // request_swap_ins/outs + execute_swap_in/out (pipeline_impl.hpp:104-113)
-    k_swap_request<<<c->num_sms * 4, 256, 0, st>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
-                                                   s.near_clip, s.far_clip, s.visibility_margin_px, s.swap_margin_px,
-                                                   c->sw, &c->dstate->ctr);
-    VF_LAUNCHED(c, "k_swap_request");
-    k_swap_select<<<1, 1024, 0, st>>>(c->entries, c->vba_slots, c->sw, s.swap_buffer_blocks,
-                                      (c->vsize == 8 ? 7 : 3) * kBlockVolume, &c->dstate->ctr);
-    VF_LAUNCHED(c, "k_swap_select");
-    // swap-ins before the raycast (it may read them); swap-outs on the side
-    // stream, overlapping the raycast, joined at the end of the frame
-    k_swap_transfer<<<c->num_sms * 2, 256, 0, st>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
-                                                    s.max_weight, 0);
-    VF_LAUNCHED(c, "k_swap_transfer");
-    if (fork) {
-      VF_CUDA(c, cudaEventRecord(c->ev_fork2, st));
-      VF_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork2, 0));
-    }
-    k_swap_transfer<<<c->num_sms * 2, 256, 0, fork ? c->side : st>>>(reinterpret_cast<uint32_t*>(c->voxels),
-                                                                     c->vsize / 4, c->sw, s.max_weight, 1);
+    // swap-outs: after the selection, beside the raycast
+    k_swap_transfer<<<c->num_sms * 2, 256, 0, branch>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
+                                                        s.max_weight, 1);
     VF_LAUNCHED(c, "k_swap_transfer");
     if (fork) VF_CUDA(c, cudaEventRecord(c->ev_join2, c->side));
-    launches += 4;
+    ++launches;
   }
   stage_mark(c, 4);
   if (!fork) {
@@ -654,7 +664,6 @@ void free_all(vf_ctx* c) {
   if (c->ev_frame1) cudaEventDestroy(c->ev_frame1);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
   if (c->ev_join2) cudaEventDestroy(c->ev_join2);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -799,7 +808,6 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return VF_ERR_CUDA;
