@@ -258,6 +258,12 @@ CONFIGS = {
         "T160", 160, 120, 0.02, mu=0.06, frames=6,
         hash=HashConfig(bucket_count=1 << 14, excess_count=1 << 12, block_count=1 << 13),
     ),
+    # C2 as a kernel bench at C3 scale (the integration
+    # roofline is judged at C3 or at a C2 bench with >= 100k visible blocks)
+    "C2L": BenchConfig(
+        "C2L", 1280, 960, 0.002, voxel_type=2, tracking=False,
+        hash=HashConfig(bucket_count=1 << 21, excess_count=1 << 18, block_count=1 << 20),
+    ),
     # configs[3]: ~50 m corridor walk (1000 frames at 5 cm) with host swapping;
     # B = 512 transfers per frame keeps eviction ahead of the ~400 blocks a
     # frame allocates at this speed (the reference default B = 100 would
