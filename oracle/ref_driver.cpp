@@ -14,6 +14,7 @@
 //     render_synthetic_depth / render_synthetic_rgb (proj/src/synthetic.cpp).
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <optional>
 #include <vector>
@@ -21,6 +22,8 @@
 #include "voxfuse/core/parallel.hpp"
 #include "voxfuse/engine/pipeline.hpp"
 #include "voxfuse/engine/pipeline_impl.hpp"
+#include "voxfuse/io/calibration.hpp"
+#include "voxfuse/io/pnm.hpp"
 #include "voxfuse/io/synthetic.hpp"
 
 using namespace voxfuse;
@@ -473,6 +476,53 @@ int vfr_stage_track(void* ctx, int which, const void* frame, const double* init,
   *valid = r.valid_points;
   *ok = r.ok ? 1 : 0;
   return 0;
+}
+// Recorded-sequence I/O through the reference (pnm.cpp, calibration.cpp, sequence.cpp).
+// out: rgb (w, h, fx, fy, cx, cy), depth (same), rgb_to_depth (R row-major, t), a, b.
+int vfr_parse_calibration(const char* text, double* out, int* err_line) {
+  try {
+    const Calibration c = parse_calibration_text(text);
+    const Intrinsics* cams[2] = {&c.rgb, &c.depth};
+    for (int k = 0; k < 2; ++k) {
+      const Intrinsics& i = *cams[k];
+      double* o = out + 6 * k;
+      o[0] = i.width, o[1] = i.height, o[2] = i.fx, o[3] = i.fy, o[4] = i.cx, o[5] = i.cy;
+    }
+    pose_to(c.rgb_to_depth, out + 12);
+    out[24] = c.disparity.a;
+    out[25] = c.disparity.b;
+    return 0;
+  } catch (const CalibrationError& e) {
+    if (err_line) *err_line = e.line();
+    return -1;
+  }
+}
+int vfr_read_pgm16(const char* path, std::uint16_t* out, long cap, int* w, int* h) {
+  try {
+    std::ifstream in(path, std::ios::binary);
+    const Image2D<std::uint16_t> img = read_pgm16(in);
+    *w = img.width();
+    *h = img.height();
+    if ((long)img.size() > cap) return -2;
+    std::memcpy(out, img.pixels().data(), sizeof(std::uint16_t) * img.size());
+    return 0;
+  } catch (const PnmError&) {
+    return -1;
+  }
+}
+int vfr_read_ppm(const char* path, std::uint8_t* out, long cap, int* w, int* h) {
+  try {
+    std::ifstream in(path, std::ios::binary);
+    const Image2D<Vec3u8> img = read_ppm(in);
+    *w = img.width();
+    *h = img.height();
+    if ((long)img.size() * 3 > cap) return -2;
+    for (std::size_t i = 0; i < img.size(); ++i)
+      for (int ch = 0; ch < 3; ++ch) out[3 * i + ch] = img.pixels()[i](ch);
+    return 0;
+  } catch (const PnmError&) {
+    return -1;
+  }
 }
 // disparity_image_to_depth through the reference's own Calibration (view.hpp:18-28)
 void vfr_disparity_to_depth(const std::uint16_t* disp, int w, int h, double a, double b, double fx,
