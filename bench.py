@@ -182,6 +182,7 @@ def cpu_reference_run(cfg, n_frames: int, budget_s: float, threads: int = 0):
     c0 = vf_py.render_rgb(lib, cfg, poses[0], spheres, planes, 0.05, far) if rgb else None
     vol.process(depth0, c0, None if cfg.tracking else poses[0])
     t_total, frames, voxels = 0.0, 0, 0
+    stage = np.zeros(5)  # FrameStats::ms_* (pipeline.hpp:56-57)
     for i in range(1, n_frames + 1):
         d = vf_py.render_depth(lib, cfg, poses[i], spheres, planes, 0.05, far)
         c = vf_py.render_rgb(lib, cfg, poses[i], spheres, planes, 0.05, far) if rgb else None
@@ -190,11 +191,14 @@ def cpu_reference_run(cfg, n_frames: int, budget_s: float, threads: int = 0):
         t_total += time.perf_counter() - t0
         frames += 1
         voxels += st.visible_blocks * 512
+        stage += [st.ms_tracking, st.ms_allocation, st.ms_integration, st.ms_swapping, st.ms_raycast]
         if t_total >= budget_s:
             break
     vol.close()
+    names = ("tracking", "allocation", "integration", "swapping", "raycast")
     return {"fps": frames / t_total, "frames": frames, "seconds": t_total, "cores": cores,
-            "voxel_updates_per_s": voxels / t_total}
+            "voxel_updates_per_s": voxels / t_total,
+            "stage_ms": {k: float(v) / max(frames, 1) for k, v in zip(names, stage)}}
 
 
 def run_reference_arm(args, dist: Dist):
@@ -233,6 +237,7 @@ def run_reference_arm(args, dist: Dist):
         "voxel_updates_per_s": float(np.mean(vps)),
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": res["cores"], "kind": "reference",
                          "sample": sample},
+        "stage_ms": res["stage_ms"],
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -437,6 +442,7 @@ def run_ours(args, dist: Dist):
         ref = cpu_reference_run(cfg, min(n_frames - 1, 30), args.cpu_seconds)
         if ref:
             line["cpu_baseline"] = {"value": ref["fps"], "unit": UNIT, "cores": ref["cores"], "kind": "reference",
+                                    "stage_ms": ref["stage_ms"],
                                     "sample": f"{cfg.name} frames 1..{ref['frames']} ({ref['seconds']:.1f} s), "
                                               "reference pipeline (oracle/_ref) via process_frame"}
     if dist.rank == 0:
