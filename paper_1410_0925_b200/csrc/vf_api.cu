@@ -311,7 +311,7 @@ int enqueue_ren(vf_ctx* c, cudaStream_t st, bool combine_icp, const PoseD* expli
     k_ren_ctl<<<1, 32, 0, st>>>(c->ren_partials, c->ren_grid, &c->dstate->ren, s.min_valid_points, s.max_condition,
                                 s.convergence_eps);
   }
-  k_ren_finish<<<1, 32, 0, st>>>(&c->dstate->ren, s.max_iterations, combine_icp ? 1 : 0, &c->dstate->icp,
+  k_ren_finish<<<1, 32, 0, st>>>(&c->dstate->ren, combine_icp ? 1 : 0, &c->dstate->icp,
                                  &c->dstate->pose, update_state ? 1 : 0);
   VF_CUDA(c, cudaGetLastError());
   *launches += 2 + 2 * s.max_iterations;

@@ -143,8 +143,7 @@ __global__ void k_ren_terms(const float* depth, IntrD in, HashView hv, const uin
                             double sigma, const RenCtl* ctl, double* partials);
 __global__ void k_ren_ctl(const double* partials, int nparts, RenCtl* ctl, int min_valid_points, double max_condition,
                           float convergence_eps);
-__global__ void k_ren_finish(RenCtl* ctl, int max_iterations, int combine_icp, IcpResult* res, PoseD* state,
-                             int update_state);
+__global__ void k_ren_finish(RenCtl* ctl, int combine_icp, IcpResult* res, PoseD* state, int update_state);
 struct ColorLevel {
   const float4* color;
   const float4* gx;

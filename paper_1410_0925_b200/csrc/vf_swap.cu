@@ -34,34 +34,6 @@ namespace {
 
 constexpr uint8_t kSwInactive = 0, kSwNeedsIn = 1, kSwActive = 3, kSwNeedsOut = 4;
 
-// block-wide exclusive scan of one int per thread (blockDim.x == 1024)
-__device__ __forceinline__ int block_excl_scan(int v, int* s_tmp, int* total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) s_tmp[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    const int w = lane < (int)(blockDim.x >> 5) ? s_tmp[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += t;
-    }
-    s_tmp[lane] = wi - w;
-    if (lane == 31) *total = wi;
-  }
-  __syncthreads();
-  const int r = s_tmp[wid] + incl - v;
-  __syncthreads();
-  return r;
-}
-
 // The k smallest values of list[0..m) (distinct non-negative ints < 2^24),
 // ascending, into out[0..k) (k <= kSwapSortCap).  Small lists are sorted
 // whole; large ones first find the k-th smallest value with a two-pass

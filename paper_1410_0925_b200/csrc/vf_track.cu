@@ -216,7 +216,7 @@ __global__ void k_ren_ctl(const double* __restrict__ partials, int nparts, RenCt
 // ren_refine's result (ren_tracker.hpp:112-116) and, for icp_ren, Pipeline::track's
 // combination with the coarse ICP (pipeline_impl.hpp:189-201); writes the
 // frame's TrackingResult and, when ok and update_state, the pose.
-__global__ void k_ren_finish(RenCtl* __restrict__ ctl, int max_iterations, int combine_icp, IcpResult* __restrict__ res,
+__global__ void k_ren_finish(RenCtl* __restrict__ ctl, int combine_icp, IcpResult* __restrict__ res,
                              PoseD* __restrict__ state, int update_state) {
   if (threadIdx.x != 0) return;
   const bool ok = ctl->done ? ctl->ok != 0 : true;  // max_iterations reached: ok
@@ -240,7 +240,6 @@ __global__ void k_ren_finish(RenCtl* __restrict__ ctl, int max_iterations, int c
   *res = out;
   ctl->done = 1;
   if (update_state && out.ok) *state = out.pose;
-  (void)max_iterations;
 }
 
 // ---------------------------------------------------------------------------
