@@ -89,3 +89,27 @@ def test_tracked_sequence_other_trackers(olib, rlib, tracker, name, rgb):
         if tracker == "icp_ren":  # (the photometric tracker drifts ~5 mm / frame on this scene, as the reference does)
             assert rot_angle(gp, pose) <= 0.01 and centre_dist(gp, pose) <= 0.01, f"frame {i}: far from ground truth"
     p.close()
+
+
+def test_colour_tracker_with_swapping(olib, rlib):
+    """Feature combination: VoxelSRgb volume, the colour tracker, host
+    swapping with a small buffer, through the reference's own pipeline and
+    the GPU, on the pan away and back."""
+    from helpers import swap_config
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, pan_trajectory
+    cfg = swap_config("T160_swap_roundtrip").with_(voxel_type=2, tracking=True, tracker="color")
+    poses = pan_trajectory(12, max_yaw=0.3)
+    s, c = settings_from_config(cfg)
+    p = make_pipeline(s, c)
+    r = vf_py.Volume(rlib, cfg, tracking=True)
+    outs = 0
+    for i, pose in enumerate(poses):
+        d = vf_py.render_depth(olib, cfg, pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        col = vf_py.render_rgb(olib, cfg, pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        st = p.process_frame(col, d)
+        sr = r.process(d, col)
+        assert bool(st.tracking_ok) == bool(sr.tracking_ok), i
+        assert rot_angle(p.pose(), r.pose()) <= 1e-4 and centre_dist(p.pose(), r.pose()) <= 1e-4, i
+        outs += st.swapped_out
+    assert outs > 0
+    p.close()
