@@ -22,7 +22,6 @@ namespace vf {
 namespace {
 
 constexpr int kStepBits = 12;
-constexpr int kSortCap = 4096;  // requests sorted in shared memory (steady state)
 constexpr unsigned long long kStepMask = (1ull << kStepBits) - 1ull;
 
 // detail::dda_cells (allocation.hpp:60-96) in FP64.  Visit(cell, step) returns
@@ -119,7 +118,7 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
                                               IntrD rgb_in, PoseD depth_to_rgb, FrameParams* __restrict__ fp,
                                               HashView hv, float voxel_size, float mu, ShardSpec shard,
                                               unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
-                                              int* __restrict__ req_marked, Counters* __restrict__ ctr) {
+                                              Counters* __restrict__ ctr) {
   __shared__ PoseD s_c2w;
   if (threadIdx.x == 0) {
     const PoseD w2c = *pose;
@@ -171,11 +170,7 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
     }
     const uint32_t bucket = hash_block(cx, cy, cz, hv.mask);
     const unsigned long long old = atomicMax(req_key + bucket, key_base | (unsigned long long)step);
-    if (old == 0ull) {
-      atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
-      const int pos = atomicAdd(&ctr->n_marked, 1);
-      if (pos < kSortCap) req_marked[pos] = (int)bucket;
-    }
+    if (old == 0ull) atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
   };
   dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
     if (find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0) request(cx, cy, cz, step);
@@ -204,168 +199,136 @@ __device__ __forceinline__ void decode_request(unsigned long long key, const flo
   });
 }
 
-// K1b-scan (one CTA): ascending compaction of the request bitmap, the
-// bucket-full test that decides whether a request needs an excess entry, the
-// prefix sums that fix every request's free-stack pop, and the fast/slow
-// decision.  Also resets the per-frame counters consumed later in the frame.
-__global__ void __launch_bounds__(1024) k_alloc_scan(uint32_t* __restrict__ req_bits, int n_words, HashView hv,
-                                                     const int* __restrict__ req_marked, int* __restrict__ req_list,
-                                                     int* __restrict__ req_excess_rank, int max_requests,
-                                                     AllocMeta* __restrict__ meta, Counters* __restrict__ ctr,
-                                                     float2* __restrict__ ranges, int n_frag) {
-  __shared__ int s_scan[64];
-  __shared__ int s_total;
-  __shared__ int s_sort[kSortCap];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int f = tid; f < n_frag; f += nt) ranges[f] = make_float2(3.402823466e+38f, 0.0f);
-  const int n_marked = *(volatile int*)&ctr->n_marked;
-  if (n_marked <= kSortCap) {
-    // Steady state: the few requested buckets were appended by k_mark; sort
-    // them ascending (bitonic, in shared memory) and clear their bits.
-    int P = 2;
-    while (P < n_marked) P <<= 1;
-    for (int i = tid; i < P; i += nt) s_sort[i] = i < n_marked ? __ldcg(req_marked + i) : 0x7fffffff;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = tid; i < P; i += nt) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const int x = s_sort[i], y = s_sort[ixj];
-            if ((x > y) == ((i & k) == 0)) {
-              s_sort[i] = y;
-              s_sort[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int i = tid; i < n_marked; i += nt) {
-      const int b = s_sort[i];
-      if (i < max_requests) req_list[i] = b;
-      req_bits[b >> 5] = 0u;  // every set bit of this frame is in the list
-    }
-    if (tid == 0) s_total = n_marked;
-    __syncthreads();
-  } else {
-  // Words are read as uint4 with all of a thread's loads in flight at once
-  // (n_words is a multiple of 4 whenever bucket_count >= 128; smaller tables
-  // take the scalar path).
-  const bool vec = (n_words & 3) == 0;
-  const int units = vec ? n_words >> 2 : n_words;
-  const int chunk = (units + nt - 1) / nt;
-  const int u0 = min(tid * chunk, units), u1 = min(u0 + chunk, units);
-  int cnt = 0;
-  if (vec) {
-    const uint4* bits4 = reinterpret_cast<const uint4*>(req_bits);
-#pragma unroll 8
-    for (int u = u0; u < u1; ++u) {
-      const uint4 b = __ldcg(bits4 + u);
-      cnt += __popc(b.x) + __popc(b.y) + __popc(b.z) + __popc(b.w);
-    }
-  } else {
-    for (int u = u0; u < u1; ++u) cnt += __popc(__ldcg(req_bits + u));
-  }
-  // block exclusive scan: warp shuffles, then one warp over the warp totals
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((tid & 31) >= o) incl += v;
-  }
-  if ((tid & 31) == 31) s_scan[tid >> 5] = incl;
+// K1b-compact: perform_allocations' ascending walk over the requests
+// (allocation.hpp:179-206) as an ordered compaction of the request bitmap,
+// plus insert_block's bucket-full test (hash_volume.hpp:225-236) deciding
+// which requests take an excess entry, and the prefix sums that fix every
+// request's free-stack pops (k_alloc_apply), over all CTAs: one thread per
+// bitmap word (256-word
+// tiles in ascending order, dynamic tile tickets), a block scan of the
+// packed (requests, excess) counts, then a decoupled look-back over the tiles
+// for both prefixes at once.  The last tile publishes the frame's counters.
+// scan[0] is the ticket, scan[1 + t] tile t's (status | requests | excess);
+// the frame zeroes them before the launch.
+__device__ __forceinline__ unsigned long long compact_flag(unsigned long long st, unsigned req, unsigned ex) {
+  return (st << 62) | ((unsigned long long)req << 31) | (unsigned long long)ex;
+}
+__global__ void __launch_bounds__(kCompactThreads) k_alloc_compact(uint32_t* __restrict__ req_bits, int n_words,
+                                                                   HashView hv, int* __restrict__ req_list,
+                                                                   int* __restrict__ req_excess_rank,
+                                                                   unsigned long long* scan, AllocMeta* __restrict__ meta,
+                                                                   Counters* __restrict__ ctr,
+                                                                   float2* __restrict__ ranges, int n_frag) {
+  __shared__ int s_tile;
+  __shared__ int s_warp[kCompactThreads / 32];
+  __shared__ unsigned s_base_req, s_base_ex;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = (int)atomicAdd(scan, 1ull);
+  for (int f = blockIdx.x * blockDim.x + tid; f < n_frag; f += gridDim.x * blockDim.x)
+    ranges[f] = make_float2(3.402823466e+38f, 0.0f);  // RangeImage: invalid = (FLT_MAX, 0)
   __syncthreads();
-  if (tid < 32) {
-    int w = tid < (nt >> 5) ? s_scan[tid] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, w, o);
-      if (tid >= o) w += v;
-    }
-    s_scan[32 + tid] = w;  // inclusive warp-total prefix
-  }
-  __syncthreads();
-  int base = incl - cnt + ((tid >> 5) ? s_scan[32 + (tid >> 5) - 1] : 0);
-  if (tid == nt - 1) s_total = base + cnt;
-  __syncthreads();
-  if (cnt) {
-    const int w0 = vec ? u0 * 4 : u0, w1 = vec ? u1 * 4 : u1;
-    for (int w = w0; w < w1; ++w) {
-      uint32_t bits = __ldcg(req_bits + w);
-      if (!bits) continue;
-      req_bits[w] = 0u;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1u;
-        if (base < max_requests) req_list[base] = w * 32 + b;
-        ++base;
-      }
-    }
-  }
-  }
-  __syncthreads();
-  const int n = min(s_total, max_requests);
-  // bucket-full test -> excess ranks, in list order
-  const int c2 = (n + nt - 1) / nt;
-  const int r0 = min(tid * c2, n), r1 = min(r0 + c2, n);
-  int ex = 0;
-  for (int k = r0; k < r1; ++k) {
-    const int h = req_list[k] * hv.bucket_size;
+  const int tile = s_tile;
+  const int n_tiles = (n_words + kCompactThreads - 1) / kCompactThreads;
+  const int w = tile * kCompactThreads + tid;
+  const uint32_t bits = w < n_words ? __ldcg(req_bits + w) : 0u;
+  // insert_block's bucket-full test: does the request need an excess entry?
+  uint32_t needs_ex = 0u;
+  for (uint32_t m = bits; m; m &= m - 1u) {
+    const int b = __ffs(m) - 1;
+    const int h = (w * 32 + b) * hv.bucket_size;
     bool has_free = false;
-    for (int j = 0; j < hv.bucket_size; ++j)
-      if (load_entry_cg(hv.entries + h + j).block_state == kEntryUnallocated) {
-        has_free = true;
-        break;
-      }
-    req_excess_rank[k] = has_free ? -1 : 0;
-    ex += has_free ? 0 : 1;
+    for (int j = 0; j < hv.bucket_size && !has_free; ++j)
+      has_free = load_entry_cg(hv.entries + h + j).block_state == kEntryUnallocated;
+    if (!has_free) needs_ex |= 1u << b;
   }
-  __syncthreads();
-  int eincl = ex;
+  // block exclusive scan of (requests << 16 | excess): both stay below 2^16 per tile
+  const int v = (__popc(bits) << 16) | __popc(needs_ex);
+  int incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, eincl, o);
-    if ((tid & 31) >= o) eincl += v;
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
-  if ((tid & 31) == 31) s_scan[tid >> 5] = eincl;
+  if (lane == 31) s_warp[wid] = incl;
   __syncthreads();
-  if (tid < 32) {
-    int w = tid < (nt >> 5) ? s_scan[tid] : 0;
+  if (wid == 0) {
+    const int wv = lane < kCompactThreads / 32 ? s_warp[lane] : 0;
+    int wi = wv;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, w, o);
-      if (tid >= o) w += v;
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
     }
-    s_scan[32 + tid] = w;
+    if (lane < kCompactThreads / 32) s_warp[lane] = wi - wv;
+    const int agg = __shfl_sync(0xffffffffu, wi, kCompactThreads / 32 - 1);
+    const unsigned agg_req = (unsigned)agg >> 16, agg_ex = (unsigned)agg & 0xFFFFu;
+    unsigned long long* flags = scan + 1;
+    if (lane == 0) atomicExch(flags + tile, compact_flag(tile == 0 ? 2ull : 1ull, agg_req, agg_ex));
+    // decoupled look-back (tile order = ascending bucket order)
+    unsigned pre_req = 0, pre_ex = 0;
+    int j = tile - 1;
+    while (j >= 0) {
+      const int k = j - lane;
+      unsigned long long f = 0;
+      if (k >= 0) {
+        do {
+          asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(f) : "l"(flags + k) : "memory");
+        } while ((f >> 62) == 0);
+      }
+      const unsigned st = k >= 0 ? (unsigned)(f >> 62) : 2u;
+      const unsigned pmask = __ballot_sync(0xffffffffu, st == 2u);
+      const int stop = pmask ? __ffs(pmask) - 1 : 31;
+      const bool take = k >= 0 && lane <= stop;
+      unsigned r = take ? (unsigned)((f >> 31) & 0x7FFFFFFFull) : 0u, e = take ? (unsigned)(f & 0x7FFFFFFFull) : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+      }
+      pre_req += r;
+      pre_ex += e;
+      if (pmask) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      if (tile > 0) atomicExch(flags + tile, compact_flag(2ull, pre_req + agg_req, pre_ex + agg_ex));
+      s_base_req = pre_req;
+      s_base_ex = pre_ex;
+      if (tile == n_tiles - 1) {  // the frame's totals: allocation meta and per-frame counter resets
+        const int n = (int)(pre_req + agg_req), n_ex = (int)(pre_ex + agg_ex);
+        const Counters c = *ctr;
+        AllocMeta m;
+        m.n = n;
+        m.n_excess = n_ex;
+        m.vba_base = c.vba_top;
+        m.excess_base = c.excess_top;
+        m.slow = (n > c.vba_top || n_ex > c.excess_top) ? 1 : 0;
+        if (!m.slow) {
+          ctr->vba_top = c.vba_top - n;
+          ctr->excess_top = c.excess_top - n_ex;
+          ctr->allocated = n;
+          ctr->dropped_vba_full = 0;
+          ctr->dropped_excess_full = 0;
+        }
+        ctr->requested = n;
+        ctr->n_requests = n;
+        ctr->visible_count = 0;
+        ctr->modified_voxels = 0;
+        *meta = m;
+      }
+    }
   }
   __syncthreads();
-  int ebase = eincl - ex + ((tid >> 5) ? s_scan[32 + (tid >> 5) - 1] : 0);
-  for (int k = r0; k < r1; ++k)
-    if (req_excess_rank[k] == 0) req_excess_rank[k] = ebase++;
-  if (tid == nt - 1) {
-    const int n_ex = ebase;
-    Counters c = *ctr;
-    AllocMeta m;
-    m.n = n;
-    m.n_excess = n_ex;
-    m.vba_base = c.vba_top;
-    m.excess_base = c.excess_top;
-    m.slow = (n > c.vba_top || n_ex > c.excess_top) ? 1 : 0;
-    if (s_total > max_requests) ctr->error_flags |= kErrRequestList;
-    if (!m.slow) {
-      ctr->vba_top = c.vba_top - n;
-      ctr->excess_top = c.excess_top - n_ex;
-      ctr->allocated = n;
-      ctr->dropped_vba_full = 0;
-      ctr->dropped_excess_full = 0;
+  if (bits) {
+    const int excl = s_warp[wid] + incl - v;
+    int r = (int)s_base_req + (excl >> 16), e = (int)s_base_ex + (excl & 0xFFFF);
+    for (uint32_t m = bits; m; m &= m - 1u) {
+      const int b = __ffs(m) - 1;
+      req_list[r] = w * 32 + b;
+      req_excess_rank[r] = (needs_ex >> b) & 1u ? e++ : -1;
+      ++r;
     }
-    ctr->requested = n;
-    ctr->n_requests = n;
-    ctr->visible_count = 0;
-    ctr->modified_voxels = 0;
-    ctr->n_marked = 0;
-    *meta = m;
+    req_bits[w] = 0u;
   }
 }
 

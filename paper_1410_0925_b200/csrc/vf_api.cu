@@ -91,8 +91,8 @@ struct vf_ctx {
   unsigned long long* req_key = nullptr;
   uint32_t* req_bits = nullptr;
   int* req_list = nullptr;
-  int* req_marked = nullptr;
   int* req_excess_rank = nullptr;
+  unsigned long long* compact_scan = nullptr;  // k_alloc_compact's ticket + look-back flags
   int* alloc_list = nullptr;
   int alloc_cap = 0;
   int* visible_list = nullptr;
@@ -403,6 +403,18 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
 // k_mark's grid: one thread per pixel, 32 x 8 pixel tiles.
 int mark_grid(const vf_ctx* c) { return ((c->din.width + 31) / 32) * ((c->din.height + 7) / 8); }
 
+// perform_allocations' ordered compaction of the request bitmap (k_alloc_compact).
+int launch_alloc_scan(vf_ctx* c, cudaStream_t st) {
+  const int n_words = c->s.bucket_count / 32;
+  const int tiles = (n_words + kCompactThreads - 1) / kCompactThreads;
+  VF_CUDA(c, cudaMemsetAsync(c->compact_scan, 0, sizeof(unsigned long long) * (1 + (size_t)tiles), st));
+  k_alloc_compact<<<tiles, kCompactThreads, 0, st>>>(c->req_bits, n_words, hash_view(c), c->req_list,
+                                                     c->req_excess_rank, c->compact_scan, &c->dstate->meta,
+                                                     &c->dstate->ctr, c->ranges, c->frag_w * c->frag_h);
+  VF_CUDA(c, cudaGetLastError());
+  return VF_OK;
+}
+
 // Integration CTAs per SM (VF_INT_GRID_MULT overrides, for tuning runs).
 int int_grid_mult() {
   static const int m = [] {
@@ -425,12 +437,10 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   stage_mark(c, 1);
   k_mark<<<mark_grid(c), 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
                                                 &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
-                                                c->req_bits, c->req_marked, &c->dstate->ctr);
+                                                c->req_bits, &c->dstate->ctr);
   VF_LAUNCHED(c, "k_mark");
-  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
-                                   c->req_excess_rank, s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
-                                   c->frag_w * c->frag_h);
-  VF_LAUNCHED(c, "k_alloc_scan");
+  if (int rc = launch_alloc_scan(c, st)) return rc;
+  VF_LAUNCHED(c, "k_alloc_compact");
   k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
                                                 c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
                                                 c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots,
@@ -646,13 +656,13 @@ void free_all(vf_ctx* c) {
   for (auto& row : c->graph)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
-  void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list, c->req_marked,
+  void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
                   c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
                   c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax,
                   c->sw.state, c->sw.host_slot, c->sw.host_free, c->sw.in_cand, c->sw.out_cand,
                   c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host, c->disp, c->image_depth_scratch,
-                  c->ren_partials, c->cpyr};
+                  c->ren_partials, c->cpyr, c->compact_scan};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
@@ -931,8 +941,9 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->req_key, sizeof(unsigned long long) * (size_t)s->bucket_count)) ||
       (rc = dalloc(c, &c->req_bits, sizeof(uint32_t) * (size_t)(s->bucket_count / 32))) ||
       (rc = dalloc(c, &c->req_list, sizeof(int) * (size_t)s->bucket_count)) ||
-      (rc = dalloc(c, &c->req_marked, sizeof(int) * (size_t)kMarkedCap)) ||
       (rc = dalloc(c, &c->req_excess_rank, sizeof(int) * (size_t)s->bucket_count)) ||
+      (rc = dalloc(c, &c->compact_scan,
+                   sizeof(unsigned long long) * (2 + (size_t)s->bucket_count / 32 / kCompactThreads))) ||
       (rc = dalloc(c, &c->alloc_list, sizeof(int) * (size_t)c->alloc_cap)) ||
       (rc = dalloc(c, &c->visible_list, sizeof(int) * (size_t)c->alloc_cap)) ||
       (rc = dalloc(c, &c->dstate, sizeof(DevState))) ||
@@ -1402,10 +1413,8 @@ int vf_stage_allocate(vf_ctx* c, const float* depth_m, const double pose[12], vf
   if (int rc = set_pose_dev(c, pose)) return rc;
   k_mark<<<mark_grid(c), 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
                                                 &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
-                                                c->req_bits, c->req_marked, &c->dstate->ctr);
-  k_alloc_scan<<<1, 1024, 0, st>>>(c->req_bits, s.bucket_count / 32, hash_view(c), c->req_marked, c->req_list,
-                                   c->req_excess_rank, s.bucket_count, &c->dstate->meta, &c->dstate->ctr, c->ranges,
-                                   c->frag_w * c->frag_h);
+                                                c->req_bits, &c->dstate->ctr);
+  if (int rc = launch_alloc_scan(c, st)) return rc;
   k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
                                                 c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
                                                 c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots,

@@ -64,7 +64,6 @@ struct IcpArgs {
 };
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);
-constexpr int kMarkedCap = 4096;  // == kSortCap in vf_alloc.cu
 struct ShardSpec {
   int count, index, shift;  // G shards, this shard, super-block shift s
   int halo;                 // also fuse bands whose surface block neighbours this shard's territory
@@ -79,10 +78,10 @@ __host__ __device__ inline int shard_owner(int bx, int by, int bz, const ShardSp
 
 __global__ void k_mark(const float* depth, IntrD in, const PoseD* pose, IntrD rgb_in, PoseD depth_to_rgb,
                        FrameParams* fp, HashView hv, float voxel_size, float mu, ShardSpec shard,
-                       unsigned long long* req_key, uint32_t* req_bits, int* req_marked, Counters* ctr);
-__global__ void k_alloc_scan(uint32_t* req_bits, int n_words, HashView hv, const int* req_marked, int* req_list,
-                             int* req_excess_rank, int max_requests, AllocMeta* meta, Counters* ctr, float2* ranges,
-                             int n_frag);
+                       unsigned long long* req_key, uint32_t* req_bits, Counters* ctr);
+constexpr int kCompactThreads = 256;  // k_alloc_compact: one bitmap word per thread
+__global__ void k_alloc_compact(uint32_t* req_bits, int n_words, HashView hv, int* req_list, int* req_excess_rank,
+                                unsigned long long* scan, AllocMeta* meta, Counters* ctr, float2* ranges, int n_frag);
 __global__ void k_alloc_apply(const float* depth, IntrD in, const FrameParams* fp, float voxel_size, float mu,
                               HashEntry* entries, uint32_t mask, int bucket_size, int ordered,
                               unsigned long long* req_key, const int* req_list, const int* req_excess_rank,
