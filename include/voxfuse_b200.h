@@ -157,6 +157,20 @@ int vf_process_frame(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb, vf_f
  * device pointers).  stats may be NULL: then nothing is read back and the call
  * does not synchronise. */
 int vf_process_frame_device(vf_ctx* ctx, const float* d_depth, const uint8_t* d_rgb, vf_frame_stats* stats);
+/* Streaming submission (no reference counterpart; process_frame split in two):
+ * vf_submit_frame enqueues the frame -- its H2D upload on a copy stream into
+ * one of VF_MAX_FRAMES_IN_FLIGHT staging slots, then the frame itself -- and
+ * returns without waiting, so the upload of frame n + 1 overlaps the
+ * processing of frame n.  vf_collect_frame waits for the OLDEST frame in
+ * flight and returns its stats (same values as vf_process_frame's).  The host
+ * buffers must stay unchanged until that frame is collected.  Submitting with
+ * VF_MAX_FRAMES_IN_FLIGHT frames outstanding, or collecting with none, is
+ * VF_ERR_STATE.  Other calls may be interleaved; they run in submission
+ * order. */
+#define VF_MAX_FRAMES_IN_FLIGHT 2
+int vf_submit_frame(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb);
+int vf_collect_frame(vf_ctx* ctx, vf_frame_stats* stats);
+int vf_frames_in_flight(const vf_ctx* ctx);
 /* IPipeline::process_raw_frame (pipeline.hpp:71, pipeline_impl.hpp:59-62):
  * a raw 16-bit disparity frame, converted on the device by
  * disparity_image_to_depth (view.hpp:18-28) with the calibration's a, b and
@@ -296,6 +310,10 @@ int vf_kernel_launches_per_frame(vf_ctx* ctx, int tracking_frame);
 long vf_readback_bytes(const vf_ctx* ctx);
 /* Evict the L2 by writing `bytes` of scratch on the context's stream (bench hygiene). */
 int vf_flush_l2(vf_ctx* ctx, size_t bytes);
+/* Sum of the device-timed durations of the vf_flush_l2 calls since the last
+ * call (synchronises the stream), so a streaming measurement can flush L2
+ * between frames in-stream and take the flushes out of its wall time. */
+int vf_flush_time(vf_ctx* ctx, double* ms);
 /* Self-test of the branch-free IEEE division used by integration against the
  * IEEE operator; returns the mismatch count.  mode 0: divisor p0, a = 0 and
  * every numerator with p2 <= |a| <= p1; mode 1: n random pairs, |a| <= p0,

@@ -33,6 +33,7 @@ ABI_VERSION = 2  # VF_ABI_VERSION in include/voxfuse_b200.h
 EXPORTS = [
     "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
     "vf_process_frame", "vf_process_frame_device", "vf_synchronize", "vf_read_stats",
+    "vf_submit_frame", "vf_collect_frame", "vf_frames_in_flight",
     "vf_process_raw_frame", "vf_process_raw_frame_device", "vf_disparity_to_depth",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
     "vf_get_surface_points", "vf_stage_forward_project", "vf_render_image",
@@ -45,7 +46,7 @@ EXPORTS = [
     "vf_shard_owner", "vf_shard_nccl_unique_id", "vf_shard_attach_nccl", "vf_shard_composite_local",
     "vf_device_alloc", "vf_device_free", "vf_memcpy_h2d", "vf_memcpy_d2h", "vf_host_alloc_pinned",
     "vf_host_free_pinned", "vf_event_record", "vf_event_elapsed_ms", "vf_set_profiling", "vf_stage_times",
-    "vf_kernel_launches_per_frame", "vf_readback_bytes", "vf_flush_l2", "vf_last_modified_voxels",
+    "vf_kernel_launches_per_frame", "vf_readback_bytes", "vf_flush_l2", "vf_flush_time", "vf_last_modified_voxels",
     "vf_selftest_division",
 ]
 
@@ -159,6 +160,9 @@ def load() -> C.CDLL:
         "vf_last_error": (C.c_char_p, [vp]),
         "vf_process_frame": (C.c_int, [vp, vp, vp, C.POINTER(VfFrameStats)]),
         "vf_process_frame_device": (C.c_int, [vp, vp, vp, C.POINTER(VfFrameStats)]),
+        "vf_submit_frame": (C.c_int, [vp, vp, vp]),
+        "vf_collect_frame": (C.c_int, [vp, C.POINTER(VfFrameStats)]),
+        "vf_frames_in_flight": (C.c_int, [vp]),
         "vf_synchronize": (C.c_int, [vp]),
         "vf_process_raw_frame": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(VfFrameStats)]),
         "vf_process_raw_frame_device": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(VfFrameStats)]),
@@ -213,6 +217,7 @@ def load() -> C.CDLL:
         "vf_kernel_launches_per_frame": (C.c_int, [vp, C.c_int]),
         "vf_readback_bytes": (C.c_long, [vp]),
         "vf_flush_l2": (C.c_int, [vp, C.c_size_t]),
+        "vf_flush_time": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "vf_last_modified_voxels": (C.c_long, [vp]),
         "vf_selftest_division": (C.c_long, [C.c_int, C.c_int, C.c_float, C.c_float, C.c_float, C.c_long]),
     }

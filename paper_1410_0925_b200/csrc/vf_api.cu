@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/voxfuse_b200.h"
@@ -62,6 +63,8 @@ IntrD intr_half(const IntrD& in) {
 }
 
 }  // namespace
+
+constexpr int kMaxFramesInFlight = VF_MAX_FRAMES_IN_FLIGHT;
 
 struct vf_ctx {
   vf_settings s;
@@ -116,6 +119,7 @@ struct vf_ctx {
   void* icp_ctl = nullptr;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> flush_ev;  // per vf_flush_l2 call, until vf_flush_time
   // sharding
   ShardSpec shard{1, 0, 2, 1};
   void* nccl_comm = nullptr;
@@ -157,6 +161,18 @@ struct vf_ctx {
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long profiled_frames = 0;
   int launches_last = 0;
+
+  // streaming submission (vf_submit_frame / vf_collect_frame): the upload of
+  // frame n + 1 runs on `copy` into a staging slot while frame n computes
+  cudaStream_t copy = nullptr;
+  float* depth_stage[kMaxFramesInFlight] = {};
+  uint8_t* rgb_stage[kMaxFramesInFlight] = {};
+  DevState* hstate_q[kMaxFramesInFlight] = {};  // pinned, one per slot
+  cudaEvent_t ev_up[kMaxFramesInFlight] = {}, ev_consumed[kMaxFramesInFlight] = {};
+  cudaEvent_t ev_done[kMaxFramesInFlight] = {}, ev_q0[kMaxFramesInFlight] = {}, ev_q1[kMaxFramesInFlight] = {};
+  int q_head = 0, q_count = 0;
+  int q_frame[kMaxFramesInFlight] = {};
+  bool q_track[kMaxFramesInFlight] = {};
 };
 
 #define VF_CUDA(ctx, call)                                                                  \
@@ -573,8 +589,8 @@ int read_state(vf_ctx* c) {
   return VF_OK;
 }
 
-void fill_stats(vf_ctx* c, bool tracked, int frame_index, vf_frame_stats* st) {
-  const DevState& h = *c->hstate;
+void fill_stats(vf_ctx* c, bool tracked, int frame_index, vf_frame_stats* st, const DevState* hs = nullptr) {
+  const DevState& h = hs ? *hs : *c->hstate;
   std::memset(st, 0, sizeof(*st));
   st->frame = frame_index;
   st->tracking_ok = tracked ? h.icp.ok : 1;
@@ -645,6 +661,83 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
   return VF_OK;
 }
 
+// Lazily created on the first vf_submit_frame: staging slots, the copy
+// stream and the per-slot events.
+int ensure_queue(vf_ctx* c) {
+  if (c->copy) return VF_OK;
+  VF_CUDA(c, cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  for (int k = 0; k < kMaxFramesInFlight; ++k) {
+    VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->depth_stage[k]), sizeof(float) * (size_t)c->npix));
+    if (c->vsize == 8)
+      VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->rgb_stage[k]), 3 * (size_t)c->rgbin.width * c->rgbin.height));
+    VF_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->hstate_q[k]), sizeof(DevState)));
+    for (cudaEvent_t* e : {&c->ev_up[k], &c->ev_consumed[k], &c->ev_done[k]})
+      VF_CUDA(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    VF_CUDA(c, cudaEventCreate(&c->ev_q0[k]));
+    VF_CUDA(c, cudaEventCreate(&c->ev_q1[k]));
+  }
+  return VF_OK;
+}
+
+// vf_submit_frame: enqueue one frame and return.  Copy stream: wait until the
+// slot's previous contents were consumed, H2D into the slot.  Main stream:
+// wait for the upload, D2D into the frame buffers, the frame's graph, D2H of
+// the frame's DevState into the slot's pinned copy.
+int submit_frame(vf_ctx* c, const float* depth, const uint8_t* rgb) {
+  if (c->q_count >= kMaxFramesInFlight) {
+    c->err = "vf_submit_frame: collect the oldest frame first";
+    return VF_ERR_STATE;
+  }
+  if (c->profiling) {
+    c->err = "vf_submit_frame: stage profiling needs vf_process_frame";
+    return VF_ERR_STATE;
+  }
+  if (int rc = ensure_queue(c)) return rc;
+  const int k = (c->q_head + c->q_count) % kMaxFramesInFlight;
+  const bool with_rgb = rgb != nullptr && c->vsize == 8;
+  const size_t dbytes = sizeof(float) * (size_t)c->npix, cbytes = 3 * (size_t)c->rgbin.width * c->rgbin.height;
+  VF_CUDA(c, cudaStreamWaitEvent(c->copy, c->ev_consumed[k], 0));
+  VF_CUDA(c, cudaMemcpyAsync(c->depth_stage[k], depth, dbytes, cudaMemcpyHostToDevice, c->copy));
+  if (with_rgb) VF_CUDA(c, cudaMemcpyAsync(c->rgb_stage[k], rgb, cbytes, cudaMemcpyHostToDevice, c->copy));
+  VF_CUDA(c, cudaEventRecord(c->ev_up[k], c->copy));
+  VF_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_up[k], 0));
+  VF_CUDA(c, cudaMemcpyAsync(c->depth, c->depth_stage[k], dbytes, cudaMemcpyDeviceToDevice, c->stream));
+  if (with_rgb) VF_CUDA(c, cudaMemcpyAsync(c->rgb, c->rgb_stage[k], cbytes, cudaMemcpyDeviceToDevice, c->stream));
+  VF_CUDA(c, cudaEventRecord(c->ev_consumed[k], c->stream));
+  c->rgb_valid = with_rgb;
+  const bool track = c->s.tracking && c->frame > 0 && c->maps_valid;
+  c->q_frame[k] = c->frame;
+  c->q_track[k] = track;
+  VF_CUDA(c, cudaEventRecord(c->ev_q0[k], c->stream));
+  if (int rc = run_frame(c, track, with_rgb)) return rc;
+  c->maps_valid = true;
+  ++c->frame;
+  VF_CUDA(c, cudaEventRecord(c->ev_q1[k], c->stream));
+  VF_CUDA(c, cudaMemcpyAsync(c->hstate_q[k], c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  VF_CUDA(c, cudaEventRecord(c->ev_done[k], c->stream));
+  ++c->q_count;
+  return VF_OK;
+}
+
+int collect_frame(vf_ctx* c, vf_frame_stats* stats) {
+  if (c->q_count == 0) {
+    c->err = "vf_collect_frame: no frame in flight";
+    return VF_ERR_STATE;
+  }
+  const int k = c->q_head;
+  VF_CUDA(c, cudaEventSynchronize(c->ev_done[k]));
+  c->q_head = (k + 1) % kMaxFramesInFlight;
+  --c->q_count;
+  const DevState* h = c->hstate_q[k];
+  if (stats) {
+    fill_stats(c, c->q_track[k], c->q_frame[k], stats, h);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev_q0[k], c->ev_q1[k]);
+    stats->ms_total = ms;
+  }
+  return h->ctr.error_flags ? VF_ERR_OVERFLOW : VF_OK;
+}
+
 template <typename T>
 int dalloc(vf_ctx* c, T** p, size_t bytes) {
   VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(p), bytes));
@@ -675,6 +768,18 @@ void free_all(vf_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->ev_join2) cudaEventDestroy(c->ev_join2);
+  for (int k = 0; k < kMaxFramesInFlight; ++k) {
+    if (c->depth_stage[k]) cudaFree(c->depth_stage[k]);
+    if (c->rgb_stage[k]) cudaFree(c->rgb_stage[k]);
+    if (c->hstate_q[k]) cudaFreeHost(c->hstate_q[k]);
+    for (cudaEvent_t e : {c->ev_up[k], c->ev_consumed[k], c->ev_done[k], c->ev_q0[k], c->ev_q1[k]})
+      if (e) cudaEventDestroy(e);
+  }
+  for (auto& e : c->flush_ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (c->copy) cudaStreamDestroy(c->copy);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -710,6 +815,8 @@ int reset_volume(vf_ctx* c) {
   if (int rc = reset_swap(c)) return rc;
   VF_CUDA(c, cudaStreamSynchronize(c->stream));
   VF_CUDA(c, cudaGetLastError());
+  if (c->copy) VF_CUDA(c, cudaStreamSynchronize(c->copy));
+  c->q_head = c->q_count = 0;
   c->frame = 0;
   c->maps_valid = false;
   return VF_OK;
@@ -731,8 +838,8 @@ int reset_swap(vf_ctx* c) {
 }
 
 int set_pose_dev(vf_ctx* c, const double* pose) {
-  *c->hpose = pose_from(pose);
-  VF_CUDA(c, cudaMemcpyAsync(&c->dstate->pose, c->hpose, sizeof(PoseD), cudaMemcpyHostToDevice, c->stream));
+  k_set_pose<<<1, 32, 0, c->stream>>>(&c->dstate->pose, pose_from(pose));
+  VF_CUDA(c, cudaGetLastError());
   return VF_OK;
 }
 
@@ -894,11 +1001,17 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   c->icp_grid = std::min(c->num_sms * std::min(occ, 2), kMaxIcpGrid);
   {
     // stage up to the whole level-0 share of each thread in shared memory,
-    // within a 160 KiB budget per CTA
+    // within what the SM leaves each of its resident ICP CTAs
     const long threads = (long)c->icp_grid * kIcpThreads;
     const long need = (c->npix + threads - 1) / threads;
     const size_t tables = sizeof(double) * (size_t)(c->din.width + c->din.height);
-    const long cap = (long)((160 * 1024 - tables) / (8 * kIcpThreads));
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_icp);
+    int sm_smem = 0;
+    cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
+    const long per_cta = std::min<long>(sm_smem / std::max(1, c->icp_grid / c->num_sms) - 1024, 200 * 1024) -
+                         (long)fa.sharedSizeBytes;
+    const long cap = std::max(1L, (long)((per_cta - (long)tables) / (8 * kIcpThreads)));
     c->icp_slots = (int)std::max(1L, std::min(need, cap));
     c->icp_smem = tables + (size_t)c->icp_slots * kIcpThreads * 8;
     cudaFuncSetAttribute(k_icp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
@@ -1037,6 +1150,18 @@ int vf_process_frame(vf_ctx* c, const float* depth_m, const uint8_t* rgb, vf_fra
 int vf_process_frame_device(vf_ctx* c, const float* d_depth, const uint8_t* d_rgb, vf_frame_stats* stats) {
   return frame_common(c, d_depth, d_rgb, true, stats);
 }
+
+int vf_submit_frame(vf_ctx* c, const float* depth_m, const uint8_t* rgb) {
+  if (!c || !depth_m) return VF_ERR_INVALID;
+  return submit_frame(c, depth_m, rgb);
+}
+
+int vf_collect_frame(vf_ctx* c, vf_frame_stats* stats) {
+  if (!c) return VF_ERR_INVALID;
+  return collect_frame(c, stats);
+}
+
+int vf_frames_in_flight(const vf_ctx* c) { return c ? c->q_count : VF_ERR_INVALID; }
 
 int vf_process_raw_frame(vf_ctx* c, const uint16_t* disparity, const uint8_t* rgb, int big_endian,
                          vf_frame_stats* stats) {
@@ -1723,7 +1848,29 @@ int vf_flush_l2(vf_ctx* c, size_t bytes) {
     VF_CUDA(c, cudaMalloc(&c->flush_buf, bytes));
     c->flush_bytes = bytes;
   }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  VF_CUDA(c, cudaEventCreate(&e0));
+  VF_CUDA(c, cudaEventCreate(&e1));
+  c->flush_ev.emplace_back(e0, e1);
+  VF_CUDA(c, cudaEventRecord(e0, c->stream));
   VF_CUDA(c, cudaMemsetAsync(c->flush_buf, (int)(c->frame & 0xFF), bytes, c->stream));
+  VF_CUDA(c, cudaEventRecord(e1, c->stream));
+  return VF_OK;
+}
+
+int vf_flush_time(vf_ctx* c, double* ms) {
+  if (!c || !ms) return VF_ERR_INVALID;
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  double total = 0;
+  for (auto& e : c->flush_ev) {
+    float t = 0;
+    cudaEventElapsedTime(&t, e.first, e.second);
+    total += t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->flush_ev.clear();
+  *ms = total;
   return VF_OK;
 }
 

@@ -115,6 +115,7 @@ __global__ void k_disparity_to_depth(const uint16_t* disp, int n, int big_endian
 __global__ void k_rebuild_alloc_list(const HashEntry* entries, int n, int* alloc_list, int cap, Counters* ctr);
 __global__ void k_init_ranges(float2* ranges, int n);
 __global__ void k_reset_visible(Counters* ctr);
+__global__ void k_set_pose(PoseD* dst, PoseD pose);
 __global__ void k_divtest_const(float b, uint32_t lo_bits, uint32_t n_bits, unsigned long long* mism);
 __global__ void k_divtest_rand(float amax, float bmin, float bmax, unsigned long long n, unsigned long long* mism);
 

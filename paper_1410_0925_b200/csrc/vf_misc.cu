@@ -169,6 +169,16 @@ __global__ void k_divtest_rand(float amax, float bmin, float bmax, unsigned long
   if (bad) atomicAdd(mism, bad);
 }
 
+// vf_set_pose: the pose travels as a kernel parameter, captured at launch, so
+// the host may set the next frame's pose while earlier frames are in flight.
+__global__ void k_set_pose(PoseD* dst, PoseD pose) {
+  if (threadIdx.x < 12) {
+    const double* src = threadIdx.x < 9 ? pose.r + threadIdx.x : pose.t + (threadIdx.x - 9);
+    double* d = threadIdx.x < 9 ? dst->r + threadIdx.x : dst->t + (threadIdx.x - 9);
+    *d = *src;
+  }
+}
+
 __global__ void k_reset_visible(Counters* ctr) {
   if (threadIdx.x == 0 && blockIdx.x == 0) ctr->visible_count = 0;
 }

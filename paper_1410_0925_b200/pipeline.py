@@ -16,6 +16,7 @@ Construction fails with ``VoxfuseError(VF_ERR_NO_DEVICE)`` without a GPU.
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 from dataclasses import dataclass, field
 
@@ -199,6 +200,7 @@ class Pipeline:
         h = C.c_void_p()
         check("vf_create", self._L.vf_create(C.byref(self._c_settings), C.byref(self._c_calib), device, C.byref(h)))
         self._h = h
+        self._in_flight = collections.deque()
         self.width, self.height = calib.depth.width, calib.depth.height
         rgb = calib.rgb or calib.depth
         self.rgb_width, self.rgb_height = rgb.width, rgb.height
@@ -236,6 +238,27 @@ class Pipeline:
         st = VfFrameStats()
         self._chk("vf_process_frame", self._L.vf_process_frame(self._h, _ptr(d), _ptr(c), C.byref(st)))
         return FrameStats.from_c(st)
+
+    def submit_frame(self, rgb, depth_m) -> None:
+        """vf_submit_frame: enqueue a frame and return; its upload overlaps the
+        previous frame's processing.  At most MAX_FRAMES_IN_FLIGHT (2) frames may be
+        outstanding; collect_frame returns them oldest first."""
+        d = _f32(depth_m, (self.height, self.width))
+        c = None if rgb is None else np.ascontiguousarray(rgb, dtype=np.uint8)
+        self._chk("vf_submit_frame", self._L.vf_submit_frame(self._h, _ptr(d), _ptr(c)))
+        self._in_flight.append((d, c))  # the host buffers stay alive until collected
+
+    def collect_frame(self) -> FrameStats:
+        """vf_collect_frame: wait for the oldest frame in flight, return its stats."""
+        st = VfFrameStats()
+        rc = self._L.vf_collect_frame(self._h, C.byref(st))
+        if rc != _abi.VF_ERR_STATE and self._in_flight:
+            self._in_flight.popleft()
+        self._chk("vf_collect_frame", rc)
+        return FrameStats.from_c(st)
+
+    def frames_in_flight(self) -> int:
+        return int(self._L.vf_frames_in_flight(self._h))
 
     def process_raw_frame(self, rgb, disparity, big_endian: bool = False) -> FrameStats:
         """IPipeline::process_raw_frame(rgb*, disparity) (pipeline_impl.hpp:59-62):

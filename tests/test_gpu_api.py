@@ -73,3 +73,48 @@ def test_surface_list_capacity_checked():
     buf = np.zeros((n - 1, 3), np.float32)
     assert L.vf_get_surface_points(p.handle, buf.ctypes.data_as(C.c_void_p), None, n - 1) == VF_ERR_INVALID
     p.close()
+
+
+@pytest.mark.parametrize("cfg_name,known_poses", [("T160", False), ("T160", True)])
+def test_streaming_submit_matches_process_frame(olib, cfg_name, known_poses):
+    """vf_submit_frame / vf_collect_frame (two frames in flight) produce the
+    same frames as blocking vf_process_frame: identical stats, poses, maps and
+    volume digest (same kernels, same order; only the upload overlaps)."""
+    from helpers import frames
+    cfg = CONFIGS[cfg_name]
+    seq = frames(olib, cfg, 8, rgb=False)
+    a, b = _create(), _create()
+    ref = []
+    for pose, d, _ in seq:
+        if known_poses:
+            a.set_pose(pose)
+        ref.append(a.process_frame(None, d))
+    got = []
+    for i, (pose, d, _) in enumerate(seq):
+        if known_poses:
+            b.set_pose(pose)
+        b.submit_frame(None, d)
+        if b.frames_in_flight() == 2:
+            got.append(b.collect_frame())
+    while b.frames_in_flight():
+        got.append(b.collect_frame())
+    assert [g.frame for g in got] == [r.frame for r in ref]
+    for g, r in zip(got, ref):
+        assert g.tracking_ok == r.tracking_ok and g.tracking_iterations == r.tracking_iterations
+        assert g.visible_blocks == r.visible_blocks and g.blocks_allocated == r.blocks_allocated
+        assert np.array_equal(np.asarray(g.pose), np.asarray(r.pose))
+    assert a.volume_digest() == b.volume_digest()
+    pa, na = a.tracking_state()
+    pb, nb = b.tracking_state()
+    assert np.array_equal(pa, pb) and np.array_equal(na, nb)
+    # queue discipline
+    L = _abi.load()
+    assert L.vf_collect_frame(b.handle, None) == VF_ERR_STATE
+    d = seq[0][1]
+    b.submit_frame(None, d)
+    b.submit_frame(None, d)
+    assert L.vf_submit_frame(b.handle, d.ctypes.data_as(C.c_void_p), None) == VF_ERR_STATE
+    b.collect_frame()
+    b.collect_frame()
+    a.close()
+    b.close()
