@@ -436,9 +436,11 @@ def run_ours(args, dist: Dist):
     integ_ms = stage_ms[2]
     integ_gbs = integ_bytes / (integ_ms * 1e-3) / 1e9 if integ_ms > 0 else 0.0
     dominant = max(stages, key=stages.get)
+    traffic = ncu_traffic(args.config)
     roofline = {
         "kernel": "k_integrate (TSDF integration)", "bound": "hbm", "achieved": integ_gbs, "peak": hbm_peak,
-        "unit": "GB/s", "frac": integ_gbs / hbm_peak, "traffic": None,
+        "unit": "GB/s", "frac": integ_gbs / hbm_peak, "traffic": traffic["bytes"] if traffic else None,
+        **({"traffic_source": traffic["source"]} if traffic else {}),
         "algorithmic_bytes_per_launch": integ_bytes, "ms_per_launch": integ_ms, "peak_source": peak_src,
         "note": f"dominant stage by time is {dominant}; integration is the HBM-graded kernel",
     }
@@ -498,6 +500,39 @@ def run_ours(args, dist: Dist):
                                               "reference pipeline (oracle/_ref) via process_frame"}
     if dist.rank == 0:
         print(json.dumps(line))
+
+
+# Committed `ncu --set full` captures of the roofline kernel per config
+# (profiles/): dram__bytes_read.sum + dram__bytes_write.sum of one launch.
+NCU_TRAFFIC = {
+    "C1": ("r1e_ncu.json", "c1_full", "k_integrate_s"),
+    "C3": ("r1e_ncu.json", "c3_integrate", "k_integrate_s"),
+    "C2": ("r1d_ncu_c2c4.json", "c2_rgb", "k_integrate_rgb"),
+}
+
+
+def ncu_traffic(config):
+    """DRAM bytes of one launch of the roofline kernel from the committed
+    capture, or None.  ncu replays with caches flushed; L2 is write-back, so
+    voxels written by the kernel drain to DRAM after it ends and the write
+    side of a launch whose working set fits L2 reads near zero."""
+    ent = NCU_TRAFFIC.get(config)
+    if not ent:
+        return None
+    f = ROOT / "profiles" / ent[0]
+    try:
+        rows = json.loads(f.read_text())[ent[1]]
+    except (OSError, KeyError, ValueError):
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows:
+        if r.get("kernel") == ent[2]:
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v, u = r[k].split()
+                tot += float(v) * scale[u]
+            return {"bytes": tot, "source": f"profiles/{ent[0]} [{ent[1]}] {ent[2]}: dram read + write per launch"}
+    return None
 
 
 def main():

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <vector>
 
 #include "b200_pipeline.hpp"
 #include "voxfuse/core/parallel.hpp"
@@ -40,7 +41,8 @@ struct vfa_config {  // same layout as vfr_config (oracle/ref_driver.cpp)
 };
 
 // Runs n frames through IPipeline.  engine: 0 = reference make_pipeline,
-// 1 = make_b200_pipeline.  Outputs per frame: pose (12), iterations, ok,
+// 1 = make_b200_pipeline, 2 = make_b200_pipeline driven through its streaming
+// extension (submit_frame / collect_frame, two frames in flight).  Outputs per frame: pose (12), iterations, ok,
 // visible blocks, allocated; final FNV digest and maps.
 int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, const std::uint8_t* rgb,
             double* poses, int* iters, int* ok, int* visible, std::uint64_t* digest, float* points,
@@ -81,8 +83,32 @@ int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, c
     k.depth.height = c->height;
     k.rgb = k.depth;
     std::unique_ptr<IPipeline> p =
-        engine == 1 ? voxfuse_b200::make_b200_pipeline(s, k) : make_pipeline(s, k);
+        engine >= 1 ? voxfuse_b200::make_b200_pipeline(s, k) : make_pipeline(s, k);
     const std::size_t npix = static_cast<std::size_t>(c->width) * c->height;
+    if (engine == 2) {
+      auto* b = dynamic_cast<voxfuse_b200::B200Pipeline*>(p.get());
+      if (!b) return -1;
+      std::vector<Image2D<float>> d(n_frames);
+      int next = 0;
+      auto collect = [&]() {
+        const FrameStats st = b->collect_frame();
+        const int f = st.frame;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) poses[f * 12 + i * 3 + j] = st.pose.rotation()(i, j);
+        for (int i = 0; i < 3; ++i) poses[f * 12 + 9 + i] = st.pose.translation()(i);
+        iters[f] = st.tracking_iterations;
+        ok[f] = st.tracking_ok ? 1 : 0;
+        visible[f] = st.visible_blocks;
+      };
+      for (; next < n_frames; ++next) {
+        d[next] = Image2D<float>(c->width, c->height, 0.0f);
+        std::memcpy(d[next].pixels().data(), depth + next * npix, sizeof(float) * npix);
+        b->submit_frame(nullptr, d[next]);
+        if (b->frames_in_flight() == VF_MAX_FRAMES_IN_FLIGHT) collect();
+      }
+      while (b->frames_in_flight() > 0) collect();
+      n_frames = 0;  // frames done; fall through to the outputs
+    }
     for (int f = 0; f < n_frames; ++f) {
       Image2D<float> d(c->width, c->height, 0.0f);
       std::memcpy(d.pixels().data(), depth + f * npix, sizeof(float) * npix);

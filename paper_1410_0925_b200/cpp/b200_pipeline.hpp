@@ -21,6 +21,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -157,6 +158,32 @@ class B200Pipeline final : public voxfuse::IPipeline {
     return finish_frame(st);
   }
 
+  // Streaming extension (not part of IPipeline): vf_submit_frame /
+  // vf_collect_frame with up to VF_MAX_FRAMES_IN_FLIGHT frames in flight, so
+  // the upload of frame n + 1 overlaps frame n.  collect_frame returns the
+  // oldest frame's stats (equal to what process_frame would have returned);
+  // the depth buffer must stay alive and unchanged until then.
+  void submit_frame(const voxfuse::Image2D<voxfuse::Vec3u8>* rgb, const voxfuse::Image2D<float>& depth_m) {
+    if (depth_m.width() != calib_.depth.width || depth_m.height() != calib_.depth.height)
+      throw std::invalid_argument("voxfuse_b200: depth image size does not match the calibration");
+    const std::uint8_t* rgb_ptr = nullptr;
+    if (rgb && !rgb->empty() && settings_.voxel_type == voxfuse::VoxelType::s_rgb)
+      rgb_ptr = reinterpret_cast<const std::uint8_t*>(rgb->pixels().data());
+    detail::check(vf_submit_frame(ctx_, depth_m.pixels().data(), rgb_ptr), "vf_submit_frame", ctx_);
+    pending_rgb_.push_back(rgb ? *rgb : voxfuse::Image2D<voxfuse::Vec3u8>());
+  }
+  voxfuse::FrameStats collect_frame() {
+    vf_frame_stats st;
+    const int rc = vf_collect_frame(ctx_, &st);
+    if (rc != VF_ERR_STATE && !pending_rgb_.empty()) {
+      if (!pending_rgb_.front().empty()) last_rgb_ = std::move(pending_rgb_.front());
+      pending_rgb_.pop_front();
+    }
+    detail::check(rc, "vf_collect_frame", ctx_);
+    return finish_frame(st);
+  }
+  int frames_in_flight() const { return vf_frames_in_flight(ctx_); }
+
  private:
   voxfuse::FrameStats finish_frame(const vf_frame_stats& st) {
     pose_ = detail::pose_from_array(st.pose);
@@ -257,6 +284,7 @@ class B200Pipeline final : public voxfuse::IPipeline {
   vf_ctx* ctx_ = nullptr;
   voxfuse::Pose pose_;
   voxfuse::Image2D<voxfuse::Vec3u8> last_rgb_;
+  std::deque<voxfuse::Image2D<voxfuse::Vec3u8>> pending_rgb_;  // rgb of the frames in flight
   mutable voxfuse::TrackingState state_;
   mutable bool maps_stale_ = true;
 };

@@ -97,3 +97,19 @@ def test_ipipeline_variants(olib, alib, variant):
         assert rot_angle(ref[0][i], gpu[0][i]) <= tol and centre_dist(ref[0][i], gpu[0][i]) <= tol, i
     hit_r, hit_g = ref[5][..., 3] > 0, gpu[5][..., 3] > 0
     assert (hit_r == hit_g).mean() >= 0.99
+
+
+def test_streaming_extension_identical(olib, alib):
+    """The adapter's streaming extension (submit_frame / collect_frame, two
+    frames in flight) returns the same tracked poses, stats, volume and maps as
+    its IPipeline::process_frame."""
+    cfg = CONFIGS["T160"]
+    fr = frames(olib, cfg, 10)
+    a = _run(alib, cfg, 1, fr)
+    b = _run(alib, cfg, 2, fr)
+    assert np.array_equal(a[0], b[0])
+    for i in (1, 2, 3):
+        assert np.array_equal(a[i], b[i])
+    assert a[4] == b[4]
+    assert np.array_equal(a[5].view(np.uint32), b[5].view(np.uint32))
+    assert np.array_equal(a[6].view(np.uint32), b[6].view(np.uint32))
