@@ -118,3 +118,42 @@ def test_streaming_submit_matches_process_frame(olib, cfg_name, known_poses):
     b.collect_frame()
     a.close()
     b.close()
+
+
+def test_streaming_rgb_swapping_matches_process_frame(olib):
+    """Streaming with the per-frame inputs and side branches on: VoxelSRgb with
+    RGB uploads, known poses set between submissions, host swapping over a pan
+    away and back: identical stats, volume and host store to vf_process_frame."""
+    import vf_py
+    from helpers import swap_config
+    from paper_1410_0925_b200 import make_pipeline, settings_from_config
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, pan_trajectory
+    cfg = swap_config("T160_swap_roundtrip").with_(voxel_type=2)
+    poses = pan_trajectory(24)
+    seq = [(pose, vf_py.render_depth(olib, cfg, pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES, 0.05, 100.0),
+            vf_py.render_rgb(olib, cfg, pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES)) for pose in poses]
+    s, c = settings_from_config(cfg)
+    a, b = make_pipeline(s, c), make_pipeline(s, c)
+    ref = []
+    for pose, d, col in seq:
+        a.set_pose(pose)
+        ref.append(a.process_frame(col, d))
+    got = []
+    for pose, d, col in seq:
+        b.set_pose(pose)
+        b.submit_frame(col, d)
+        if b.frames_in_flight() == 2:
+            got.append(b.collect_frame())
+    while b.frames_in_flight():
+        got.append(b.collect_frame())
+    assert len(got) == len(ref)
+    for g, r in zip(got, ref):
+        assert (g.frame, g.visible_blocks, g.blocks_allocated, g.swapped_in, g.swapped_out) == \
+            (r.frame, r.visible_blocks, r.blocks_allocated, r.swapped_in, r.swapped_out)
+    assert sum(r.swapped_out for r in ref) > 0 and sum(r.swapped_in for r in ref) > 0
+    assert a.volume_digest() == b.volume_digest()
+    assert a.store_count() == b.store_count()
+    sa, sb = a.store(), b.store()
+    assert sa.keys() == sb.keys() and all(np.array_equal(sa[k], sb[k]) for k in sa)
+    a.close()
+    b.close()
