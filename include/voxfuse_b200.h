@@ -169,6 +169,9 @@ int vf_process_frame_device(vf_ctx* ctx, const float* d_depth, const uint8_t* d_
  * order. */
 #define VF_MAX_FRAMES_IN_FLIGHT 2
 int vf_submit_frame(vf_ctx* ctx, const float* depth_m, const uint8_t* rgb);
+/* process_raw_frame's streaming form: the raw disparity frame (2 bytes per
+ * pixel) is uploaded and decoded on the device, as in vf_process_raw_frame. */
+int vf_submit_raw_frame(vf_ctx* ctx, const uint16_t* disparity, const uint8_t* rgb, int big_endian);
 int vf_collect_frame(vf_ctx* ctx, vf_frame_stats* stats);
 int vf_frames_in_flight(const vf_ctx* ctx);
 /* IPipeline::process_raw_frame (pipeline.hpp:71, pipeline_impl.hpp:59-62):

@@ -33,7 +33,7 @@ ABI_VERSION = 2  # VF_ABI_VERSION in include/voxfuse_b200.h
 EXPORTS = [
     "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
     "vf_process_frame", "vf_process_frame_device", "vf_synchronize", "vf_read_stats",
-    "vf_submit_frame", "vf_collect_frame", "vf_frames_in_flight",
+    "vf_submit_frame", "vf_submit_raw_frame", "vf_collect_frame", "vf_frames_in_flight",
     "vf_process_raw_frame", "vf_process_raw_frame_device", "vf_disparity_to_depth",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
     "vf_get_surface_points", "vf_stage_forward_project", "vf_render_image",
@@ -161,6 +161,7 @@ def load() -> C.CDLL:
         "vf_process_frame": (C.c_int, [vp, vp, vp, C.POINTER(VfFrameStats)]),
         "vf_process_frame_device": (C.c_int, [vp, vp, vp, C.POINTER(VfFrameStats)]),
         "vf_submit_frame": (C.c_int, [vp, vp, vp]),
+        "vf_submit_raw_frame": (C.c_int, [vp, vp, vp, C.c_int]),
         "vf_collect_frame": (C.c_int, [vp, C.POINTER(VfFrameStats)]),
         "vf_frames_in_flight": (C.c_int, [vp]),
         "vf_synchronize": (C.c_int, [vp]),

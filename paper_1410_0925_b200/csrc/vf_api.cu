@@ -683,7 +683,8 @@ int ensure_queue(vf_ctx* c) {
 // slot's previous contents were consumed, H2D into the slot.  Main stream:
 // wait for the upload, D2D into the frame buffers, the frame's graph, D2H of
 // the frame's DevState into the slot's pinned copy.
-int submit_frame(vf_ctx* c, const float* depth, const uint8_t* rgb) {
+int submit_frame(vf_ctx* c, const float* depth, const uint8_t* rgb, const uint16_t* disparity = nullptr,
+                 bool big_endian = false) {
   if (c->q_count >= kMaxFramesInFlight) {
     c->err = "vf_submit_frame: collect the oldest frame first";
     return VF_ERR_STATE;
@@ -697,11 +698,24 @@ int submit_frame(vf_ctx* c, const float* depth, const uint8_t* rgb) {
   const bool with_rgb = rgb != nullptr && c->vsize == 8;
   const size_t dbytes = sizeof(float) * (size_t)c->npix, cbytes = 3 * (size_t)c->rgbin.width * c->rgbin.height;
   VF_CUDA(c, cudaStreamWaitEvent(c->copy, c->ev_consumed[k], 0));
-  VF_CUDA(c, cudaMemcpyAsync(c->depth_stage[k], depth, dbytes, cudaMemcpyHostToDevice, c->copy));
+  // a raw disparity frame (2 bytes per pixel) shares the slot and is decoded
+  // straight from it into the frame's depth buffer
+  if (disparity)
+    VF_CUDA(c, cudaMemcpyAsync(c->depth_stage[k], disparity, sizeof(uint16_t) * (size_t)c->npix,
+                               cudaMemcpyHostToDevice, c->copy));
+  else
+    VF_CUDA(c, cudaMemcpyAsync(c->depth_stage[k], depth, dbytes, cudaMemcpyHostToDevice, c->copy));
   if (with_rgb) VF_CUDA(c, cudaMemcpyAsync(c->rgb_stage[k], rgb, cbytes, cudaMemcpyHostToDevice, c->copy));
   VF_CUDA(c, cudaEventRecord(c->ev_up[k], c->copy));
   VF_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_up[k], 0));
-  VF_CUDA(c, cudaMemcpyAsync(c->depth, c->depth_stage[k], dbytes, cudaMemcpyDeviceToDevice, c->stream));
+  if (disparity) {
+    k_disparity_to_depth<<<(c->npix + 255) / 256, 256, 0, c->stream>>>(
+        reinterpret_cast<const uint16_t*>(c->depth_stage[k]), c->npix, big_endian ? 1 : 0,
+        (float)c->calib.disparity_a, (float)c->calib.disparity_b, (float)c->calib.depth.fx, c->s.max_depth, c->depth);
+    VF_CUDA(c, cudaGetLastError());
+  } else {
+    VF_CUDA(c, cudaMemcpyAsync(c->depth, c->depth_stage[k], dbytes, cudaMemcpyDeviceToDevice, c->stream));
+  }
   if (with_rgb) VF_CUDA(c, cudaMemcpyAsync(c->rgb, c->rgb_stage[k], cbytes, cudaMemcpyDeviceToDevice, c->stream));
   VF_CUDA(c, cudaEventRecord(c->ev_consumed[k], c->stream));
   c->rgb_valid = with_rgb;
@@ -1154,6 +1168,11 @@ int vf_process_frame_device(vf_ctx* c, const float* d_depth, const uint8_t* d_rg
 int vf_submit_frame(vf_ctx* c, const float* depth_m, const uint8_t* rgb) {
   if (!c || !depth_m) return VF_ERR_INVALID;
   return submit_frame(c, depth_m, rgb);
+}
+
+int vf_submit_raw_frame(vf_ctx* c, const uint16_t* disparity, const uint8_t* rgb, int big_endian) {
+  if (!c || !disparity) return VF_ERR_INVALID;
+  return submit_frame(c, nullptr, rgb, disparity, big_endian != 0);
 }
 
 int vf_collect_frame(vf_ctx* c, vf_frame_stats* stats) {

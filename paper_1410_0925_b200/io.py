@@ -14,9 +14,10 @@ Host I/O, restated from the reference's behaviour (not its code):
   (proj/src/sequence.cpp:9-43).
 
 ``run_sequence`` feeds a scanned sequence to a ``Pipeline`` through
-``process_raw_frame`` with the P5 payload's raw big-endian bytes: the byte
-swap and disparity_image_to_depth run on the GPU (vf_process_raw_frame), the
-host only reads the file.
+``process_raw_frame`` (or its streaming form, the default) with the P5
+payload's raw big-endian bytes: the byte swap and disparity_image_to_depth
+run on the GPU (vf_process_raw_frame / vf_submit_raw_frame), the host only
+reads the files, overlapped with the GPU when streaming.
 """
 from __future__ import annotations
 
@@ -231,12 +232,21 @@ def scan_sequence_dir(path: str) -> SequenceScan:
     return scan
 
 
-def run_sequence(pipeline, scan: SequenceScan, limit: int | None = None):
+def run_sequence(pipeline, scan: SequenceScan, limit: int | None = None, streaming: bool = True):
     """Feed a scanned recorded sequence through IPipeline::process_raw_frame;
-    returns the per-frame FrameStats."""
+    returns the per-frame FrameStats.  streaming: the submit / collect form
+    with two frames in flight, so reading frame n + 1 from disk and its upload
+    overlap frame n on the GPU (same results)."""
     out = []
     for fp in scan.frames[:limit]:
         raw = read_pgm16_raw(fp.disparity_path)
         rgb = read_ppm(fp.rgb_path) if fp.rgb_path else None
-        out.append(pipeline.process_raw_frame(rgb, raw, big_endian=True))
+        if not streaming:
+            out.append(pipeline.process_raw_frame(rgb, raw, big_endian=True))
+            continue
+        pipeline.submit_raw_frame(rgb, raw, big_endian=True)
+        if pipeline.frames_in_flight() >= 2:
+            out.append(pipeline.collect_frame())
+    while streaming and pipeline.frames_in_flight() > 0:
+        out.append(pipeline.collect_frame())
     return out

@@ -248,6 +248,13 @@ class Pipeline:
         self._chk("vf_submit_frame", self._L.vf_submit_frame(self._h, _ptr(d), _ptr(c)))
         self._in_flight.append((d, c))  # the host buffers stay alive until collected
 
+    def submit_raw_frame(self, rgb, disparity, big_endian: bool = False) -> None:
+        """vf_submit_raw_frame: process_raw_frame's streaming form."""
+        d = np.ascontiguousarray(disparity, dtype=np.uint16).reshape(self.height, self.width)
+        c = None if rgb is None else np.ascontiguousarray(rgb, dtype=np.uint8)
+        self._chk("vf_submit_raw_frame", self._L.vf_submit_raw_frame(self._h, _ptr(d), _ptr(c), 1 if big_endian else 0))
+        self._in_flight.append((d, c))
+
     def collect_frame(self) -> FrameStats:
         """vf_collect_frame: wait for the oldest frame in flight, return its stats."""
         st = VfFrameStats()

@@ -34,7 +34,13 @@ def test_recorded_sequence_through_raw_frames(olib, tmp_path):
     scan = vio.scan_sequence_dir(str(tmp_path))
     assert [f.index for f in scan.frames] == [0, 1, 2, 3] and scan.disparity_only == 4
     p = make_pipeline(s, calib)
-    stats = vio.run_sequence(p, scan)
+    stats = vio.run_sequence(p, scan)  # streaming: vf_submit_raw_frame / vf_collect_frame
+    r = make_pipeline(s, calib)
+    stats_sync = vio.run_sequence(r, scan, streaming=False)  # vf_process_raw_frame
+    for a_, b_ in zip(stats, stats_sync):
+        assert a_.frame == b_.frame and np.array_equal(a_.pose, b_.pose)
+    assert entries_equal(p.entries(), r.entries()) and np.array_equal(p.voxels(), r.voxels())
+    r.close()
     q = make_pipeline(s, calib)
     for fp, st in zip(scan.frames, stats):
         depth = vf_py.disparity_to_depth(olib, vio.read_pgm16(fp.disparity_path), a, b, fx, s.max_depth)
