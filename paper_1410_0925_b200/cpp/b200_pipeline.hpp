@@ -162,7 +162,7 @@ class B200Pipeline final : public voxfuse::IPipeline {
   // vf_collect_frame with up to VF_MAX_FRAMES_IN_FLIGHT frames in flight, so
   // the upload of frame n + 1 overlaps frame n.  collect_frame returns the
   // oldest frame's stats (equal to what process_frame would have returned);
-  // the depth buffer must stay alive and unchanged until then.
+  // the depth (or disparity) buffer must stay alive and unchanged until then.
   void submit_frame(const voxfuse::Image2D<voxfuse::Vec3u8>* rgb, const voxfuse::Image2D<float>& depth_m) {
     if (depth_m.width() != calib_.depth.width || depth_m.height() != calib_.depth.height)
       throw std::invalid_argument("voxfuse_b200: depth image size does not match the calibration");
@@ -170,6 +170,15 @@ class B200Pipeline final : public voxfuse::IPipeline {
     if (rgb && !rgb->empty() && settings_.voxel_type == voxfuse::VoxelType::s_rgb)
       rgb_ptr = reinterpret_cast<const std::uint8_t*>(rgb->pixels().data());
     detail::check(vf_submit_frame(ctx_, depth_m.pixels().data(), rgb_ptr), "vf_submit_frame", ctx_);
+    pending_rgb_.push_back(rgb ? *rgb : voxfuse::Image2D<voxfuse::Vec3u8>());
+  }
+  void submit_raw_frame(const voxfuse::Image2D<voxfuse::Vec3u8>* rgb, const voxfuse::Image2D<std::uint16_t>& disparity) {
+    if (disparity.width() != calib_.depth.width || disparity.height() != calib_.depth.height)
+      throw std::invalid_argument("voxfuse_b200: disparity image size does not match the calibration");
+    const std::uint8_t* rgb_ptr = nullptr;
+    if (rgb && !rgb->empty() && settings_.voxel_type == voxfuse::VoxelType::s_rgb)
+      rgb_ptr = reinterpret_cast<const std::uint8_t*>(rgb->pixels().data());
+    detail::check(vf_submit_raw_frame(ctx_, disparity.pixels().data(), rgb_ptr, 0), "vf_submit_raw_frame", ctx_);
     pending_rgb_.push_back(rgb ? *rgb : voxfuse::Image2D<voxfuse::Vec3u8>());
   }
   voxfuse::FrameStats collect_frame() {
