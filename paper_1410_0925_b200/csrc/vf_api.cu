@@ -1032,9 +1032,11 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     cudaFuncSetAttribute(k_icp_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
     // Coarse levels (<= kClusterPixels pixels) go to one cluster of 16 CTAs
     // (non-portable size) or 8 if the device cannot co-schedule 16.
-    constexpr int kClusterPixels = 8192;
+    // (VF_ICP_CLUSTER_PIXELS / VF_ICP_CLUSTER_SIZE: tuning overrides)
+    const int kClusterPixels = std::getenv("VF_ICP_CLUSTER_PIXELS") ? std::atoi(std::getenv("VF_ICP_CLUSTER_PIXELS")) : 8192;
+    const int cs_want = std::getenv("VF_ICP_CLUSTER_SIZE") ? std::atoi(std::getenv("VF_ICP_CLUSTER_SIZE")) : 16;
     cudaFuncSetAttribute(k_icp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cs : {16, 8}) {
+    for (int cs : {cs_want, 8}) {
       cudaLaunchConfig_t q{};
       q.gridDim = dim3(cs);
       q.blockDim = dim3(kIcpThreads);
