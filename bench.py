@@ -445,6 +445,21 @@ def run_ours(args, dist: Dist):
         "algorithmic_bytes_per_launch": integ_bytes, "ms_per_launch": integ_ms, "peak_source": peak_src,
         "note": f"dominant stage by time is {dominant}; integration is the HBM-graded kernel",
     }
+    # The latency-bound stages against the same HBM peak, from the committed
+    # capture's DRAM bytes per launch over this run's event-timed stage: shows
+    # how far from memory-bound they are (C1 only; the capture is C1's).
+    if args.config == "C1":
+        stage_kernels = {"raycast": ("k_raycast",), "tracking": ("k_pyramid", "k_icp_cluster", "k_icp")}
+        rows = {}
+        for stage, kernels in stage_kernels.items():
+            b = sum((ncu_kernel_bytes("r1f_ncu.json", "c1_full", k) or 0.0) for k in kernels)
+            ms = stages.get(stage, 0.0)
+            if b > 0 and ms > 0:
+                gbs = b / (ms * 1e-3) / 1e9
+                rows[stage] = {"kernels": list(kernels), "dram_bytes": b, "ms": ms, "achieved_gbs": gbs,
+                               "frac_of_hbm": gbs / hbm_peak}
+        if rows:
+            roofline["latency_bound_stages"] = rows
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
@@ -512,6 +527,23 @@ NCU_TRAFFIC = {
 }
 
 
+def ncu_kernel_bytes(fname, section, kernel):
+    """dram read + write bytes of `kernel` in a committed capture, or None."""
+    try:
+        rows = json.loads((ROOT / "profiles" / fname).read_text())[section]
+    except (OSError, KeyError, ValueError):
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows:
+        if r.get("kernel") == kernel:
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v, u = r[k].split()
+                tot += float(v) * scale[u]
+            return tot
+    return None
+
+
 def ncu_traffic(config):
     """DRAM bytes of one launch of the roofline kernel from the committed
     capture, or None.  ncu replays with caches flushed; L2 is write-back, so
@@ -520,20 +552,10 @@ def ncu_traffic(config):
     ent = NCU_TRAFFIC.get(config)
     if not ent:
         return None
-    f = ROOT / "profiles" / ent[0]
-    try:
-        rows = json.loads(f.read_text())[ent[1]]
-    except (OSError, KeyError, ValueError):
+    b = ncu_kernel_bytes(*ent)
+    if b is None:
         return None
-    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for r in rows:
-        if r.get("kernel") == ent[2]:
-            tot = 0.0
-            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                v, u = r[k].split()
-                tot += float(v) * scale[u]
-            return {"bytes": tot, "source": f"profiles/{ent[0]} [{ent[1]}] {ent[2]}: dram read + write per launch"}
-    return None
+    return {"bytes": b, "source": f"profiles/{ent[0]} [{ent[1]}] {ent[2]}: dram read + write per launch"}
 
 
 def main():
