@@ -237,8 +237,13 @@ __global__ void __launch_bounds__(kCompactThreads) k_alloc_compact(uint32_t* __r
     const int b = __ffs(m) - 1;
     const int h = (w * 32 + b) * hv.bucket_size;
     bool has_free = false;
-    for (int j = 0; j < hv.bucket_size && !has_free; ++j)
-      has_free = load_entry_cg(hv.entries + h + j).block_state == kEntryUnallocated;
+    if (hv.bucket_size == 2) {  // both slots' loads in flight at once
+      const int s0 = load_entry_cg(hv.entries + h).block_state, s1 = load_entry_cg(hv.entries + h + 1).block_state;
+      has_free = s0 == kEntryUnallocated || s1 == kEntryUnallocated;
+    } else {
+      for (int j = 0; j < hv.bucket_size && !has_free; ++j)
+        has_free = load_entry_cg(hv.entries + h + j).block_state == kEntryUnallocated;
+    }
     if (!has_free) needs_ex |= 1u << b;
   }
   // block exclusive scan of (requests << 16 | excess): both stay below 2^16 per tile
@@ -348,17 +353,24 @@ __global__ void __launch_bounds__(256) k_alloc_apply(const float* __restrict__ d
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m.n; k += gridDim.x * blockDim.x) {
       const int bucket = req_list[k];
       const unsigned long long key = req_key[bucket];
+      const int h = bucket * bucket_size;
+      // The bucket's slot states, loaded before the request is decoded (one
+      // request per bucket per frame: nothing else writes this bucket now).
+      int st[2] = {0, 0};
+      if (bucket_size == 2) {
+        st[0] = entries[h].block_state;
+        st[1] = entries[h + 1].block_state;
+      }
       req_key[bucket] = 0ull;
       int bx, by, bz;
       decode_request(key, depth, in, c2w, voxel_size, mu, bx, by, bz);
       const int slot = vba_slots[m.vba_base - 1 - k];
-      const int h = bucket * bucket_size;
       int idx = -1;
       const int er = req_excess_rank[k];
       if (er < 0) {
         for (int j = 0; j < bucket_size; ++j) {
           HashEntry* e = entries + h + j;
-          if (e->block_state == kEntryUnallocated) {
+          if ((bucket_size == 2 ? st[j & 1] : e->block_state) == kEntryUnallocated) {
             e->x = (int16_t)bx;
             e->y = (int16_t)by;
             e->z = (int16_t)bz;
