@@ -1025,9 +1025,11 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device);
     const long per_cta = std::min<long>(sm_smem / std::max(1, c->icp_grid / c->num_sms) - 1024, 200 * 1024) -
                          (long)fa.sharedSizeBytes;
-    const long cap = std::max(1L, (long)((per_cta - (long)tables) / (8 * kIcpThreads)));
+    // the pipelined pixel pass's tap buffers: 2 stages x kInflight pixels x 8 taps
+    const size_t taps = (size_t)2 * kInflight * 8 * kIcpThreads * sizeof(float4) + 16;
+    const long cap = std::max(1L, (long)((per_cta - (long)tables - (long)taps) / (8 * kIcpThreads)));
     c->icp_slots = (int)std::max(1L, std::min(need, cap));
-    c->icp_smem = tables + (size_t)c->icp_slots * kIcpThreads * 8;
+    c->icp_smem = tables + (size_t)c->icp_slots * kIcpThreads * 8 + taps;
     cudaFuncSetAttribute(k_icp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
     cudaFuncSetAttribute(k_icp_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->icp_smem);
     // Coarse levels (<= kClusterPixels pixels) go to one cluster of 16 CTAs

@@ -120,6 +120,20 @@ __device__ __forceinline__ bool bilinear_taps(const float4 (&t)[4], double fx, d
   return true;
 }
 
+// 16-byte cp.async into shared memory (L1-allocating); n = 0 zero-fills
+// without reading global memory.
+__device__ __forceinline__ void cp_async16(float4* dst_smem, const float4* src, unsigned n) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+// What the front half of a pipelined ICP step hands its back half.
+struct IcpStage {
+  D3 pw[kInflight];
+  double fx[kInflight], fy[kInflight];
+  bool ok[kInflight];
+};
+
 struct Ctl {
   PoseD c2w, accepted, render;
   double pending[6];
@@ -158,6 +172,9 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
   double* s_uy = s_ux + a.lv[0].w;
   float* s_depth = reinterpret_cast<float*>(s_uy + a.lv[0].h);
   int* s_xy = reinterpret_cast<int*>(s_depth + a.max_slots * blockDim.x);
+  // map taps of the pixels in flight, two stages: [stage][pixel k][tap q][thread]
+  float4* s_taps = reinterpret_cast<float4*>(
+      (reinterpret_cast<uintptr_t>(s_xy + a.max_slots * blockDim.x) + 15) & ~static_cast<uintptr_t>(15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const bool timer = blockIdx.x == 0 && tid == 0 && a.trace;
   if (tid == 0) {
@@ -222,6 +239,124 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
       double acc[kAcc];
 #pragma unroll
       for (int i = 0; i < kAcc; ++i) acc[i] = 0;
+#ifndef VF_ICP_LEGACY_LOOP
+      // Software-pipelined pixel pass: the front half of step n + 1 (depth
+      // and tables from shared memory, the two FP64 transforms, projection,
+      // association test) runs and its eight map taps per pixel are copied
+      // into shared memory with cp.async before the back half of step n
+      // (bilinear blends, point-to-plane term, sums) consumes its own taps, so
+      // the tap round trip and the next transforms overlap the current terms.
+      const int total_slots = (npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride;
+      IcpStage st0, st1;
+      auto front = [&](int k0, int stage, IcpStage& S) {
+        float d[kInflight];
+        double ux[kInflight], uy[kInflight];
+#pragma unroll
+        for (int k = 0; k < kInflight; ++k) {
+          const int slot = k0 + k;
+          const int pix = blockIdx.x * blockDim.x + tid + slot * gstride;
+          if (slot < nslots) {
+            d[k] = s_depth[slot * blockDim.x + tid];
+            const int xy = s_xy[slot * blockDim.x + tid];
+            ux[k] = s_ux[xy & 0xFFFF];
+            uy[k] = s_uy[xy >> 16];
+          } else {
+            const bool in = slot < total_slots && pix < npix;
+            const int y = in ? pix / lv.w : 0, x = in ? pix - y * lv.w : 0;
+            d[k] = in ? __ldg(lv.depth + pix) : 0.0f;
+            ux[k] = s_ux[x];
+            uy[k] = s_uy[y];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kInflight; ++k) {
+          // unproject (intrinsics.hpp:39-43); (x - cx) / fx is tabulated per level
+          const D3 pc = mk(ux[k] * d[k], uy[k] * d[k], (double)d[k]);
+          S.pw[k] = apply(c2w, pc);
+          const D3 q = apply(render, S.pw[k]);
+          const double u = a.map.fx * q.x / q.z + a.map.cx;
+          const double v = a.map.fy * q.y / q.z + a.map.cy;
+          // sample_map_bilinear's bounds test (depth_tracker.hpp:39)
+          S.ok[k] = d[k] > 0.0f && q.z > 0.0 &&
+                    !(u < 0 || v < 0 || u > a.map.width - 1.001 || v > a.map.height - 1.001);
+          const int ix = S.ok[k] ? (int)u : 0, iy = S.ok[k] ? (int)v : 0;
+          S.fx[k] = u - ix;
+          S.fy[k] = v - iy;
+          const size_t i00 = (size_t)iy * a.map.width + ix;
+          const size_t off[4] = {i00, i00 + 1, i00 + a.map.width, i00 + a.map.width + 1};
+          const unsigned n = S.ok[k] ? 16u : 0u;  // 0: zero-fill, no global read
+          float4* dst = s_taps + (size_t)((stage * kInflight + k) * 8) * blockDim.x + tid;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            cp_async16(dst + t * blockDim.x, a.points + off[t], n);
+            cp_async16(dst + (4 + t) * blockDim.x, a.normals + off[t], n);
+          }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      auto back = [&](int stage, const IcpStage& S) {
+#pragma unroll
+        for (int k = 0; k < kInflight; ++k) {
+          if (!S.ok[k]) continue;
+          const float4* src = s_taps + (size_t)((stage * kInflight + k) * 8) * blockDim.x + tid;
+          float4 tp[4], tn[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            tp[t] = src[t * blockDim.x];
+            tn[t] = src[(4 + t) * blockDim.x];
+          }
+          D3 mp, mn;
+          if (!bilinear_taps(tp, S.fx[k], S.fy[k], a.dist_thr, mp)) continue;
+          if (!bilinear_taps(tn, S.fx[k], S.fy[k], 1.0f, mn)) continue;
+          const double nlen = sqrt(mn.x * mn.x + mn.y * mn.y + mn.z * mn.z);
+          if (nlen < 1e-6) continue;
+          // model_normal /= nlen: one refined reciprocal instead of three IEEE
+          // divisions (1-ulp differences, far below the 1e-9 H/g parity bar)
+          const double inv = rcp_fast(nlen);
+          mn = mk(mn.x * inv, mn.y * inv, mn.z * inv);
+          // icp_point_to_plane_term (depth_tracker.hpp:20-27)
+          const D3 w = S.pw[k];
+          const double r = (w.x - mp.x) * mn.x + (w.y - mp.y) * mn.y + (w.z - mp.z) * mn.z;
+          if (fabs(r) > (double)a.dist_thr) continue;
+          const D3 pr = rotation_only ? mk(w.x - rc.x, w.y - rc.y, w.z - rc.z) : w;
+          // Jacobian and sums feed only the 29 accumulators, whose reduction
+          // order differs from the reference's anyway (parity bar 1e-9), so
+          // they use fused multiply-adds; everything that decides association
+          // or rejection above keeps the reference's exact rounding.
+          const double j[6] = {fma(pr.y, mn.z, -(pr.z * mn.y)), fma(pr.z, mn.x, -(pr.x * mn.z)),
+                               fma(pr.x, mn.y, -(pr.y * mn.x)), mn.x, mn.y, mn.z};
+          int n = 0;
+#pragma unroll
+          for (int s2 = 0; s2 < 6; ++s2) {
+#pragma unroll
+            for (int t = s2; t < 6; ++t, ++n) acc[n] = fma(j[s2], j[t], acc[n]);
+            acc[21 + s2] = fma(j[s2], r, acc[21 + s2]);
+          }
+          acc[27] = fma(r, r, acc[27]);
+          acc[28] += 1.0;
+        }
+      };
+      if (total_slots > 0) front(0, 0, st0);
+      for (int k0 = 0; k0 < total_slots; k0 += 2 * kInflight) {
+        const bool more1 = k0 + kInflight < total_slots;
+        if (more1) {
+          front(k0 + kInflight, 1, st1);
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        back(0, st0);
+        if (!more1) break;
+        const bool more2 = k0 + 2 * kInflight < total_slots;
+        if (more2) {
+          front(k0 + 2 * kInflight, 0, st0);
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        back(1, st1);
+      }
+#else
       // kInflight pixels per step, each pipeline stage issued for all before it is
       // consumed, so their memory round trips (depth + tables, then the
       // eight map taps) overlap.
@@ -319,6 +454,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
         }
         VF_TF(3);
       }
+#endif
       // CTA reduction: transpose butterfly inside each warp, then one warp
       // combines the warp sums.
       {

@@ -13,7 +13,7 @@ namespace vf {
 #define VF_ICP_MIN_BLOCKS 1
 #endif
 #ifndef VF_ICP_INFLIGHT
-#define VF_ICP_INFLIGHT 2
+#define VF_ICP_INFLIGHT 1  // pixels per pipelined step (2 with VF_ICP_LEGACY_LOOP)
 #endif
 constexpr int kIcpThreads = VF_ICP_THREADS;
 constexpr int kInflight = VF_ICP_INFLIGHT;  // ICP pixels in flight per thread
