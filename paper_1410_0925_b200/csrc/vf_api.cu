@@ -9,6 +9,7 @@
 // (proj/include/voxfuse/engine/pipeline_impl.hpp:33-248).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -365,7 +366,24 @@ int enqueue_color(vf_ctx* c, cudaStream_t st, const PoseD* explicit_init, bool u
   a.explicit_init = explicit_init;
   a.result = &c->dstate->icp;
   a.update_state = update_state ? 1 : 0;
-  k_color_track<<<1, 1024, 0, st>>>(a);
+  a.partials = c->partials;
+  // one CTA per kColorThreads surface points (up to one per SM), over a
+  // cooperative grid: an evaluation is then one point per thread deep
+  const int g = std::max(1, std::min({c->num_sms, c->icp_grid, (c->surf_cap + kColorThreads - 1) / kColorThreads}));
+  if (g == 1) {
+    k_color_track<<<1, kColorThreads, 0, st>>>(a);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kColorThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VF_CUDA(c, cudaLaunchKernelEx(&cfg, k_color_track, a));
+  }
   VF_CUDA(c, cudaGetLastError());
   *launches += 2 * L + 1;
   return VF_OK;

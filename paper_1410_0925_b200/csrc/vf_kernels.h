@@ -163,10 +163,15 @@ struct ColorTrackArgs {
   const PoseD* explicit_init;  // nullptr: *state
   IcpResult* result;
   int update_state;
+  double* partials;  // grid launch: 2 x gridDim x 32 per-CTA sums (double-buffered)
 };
 __global__ void k_cpyr_base(const uint8_t* rgb, int n, float4* out);
 __global__ void k_cpyr_down(const float4* src, int sw, int sh, float4* dst);
 __global__ void k_cpyr_grad(const float4* src, int w, int h, float4* gx, float4* gy);
+#ifndef VF_COLOR_THREADS
+#define VF_COLOR_THREADS 256
+#endif
+constexpr int kColorThreads = VF_COLOR_THREADS;  // colour tracker CTA size (one point per thread per evaluation)
 __global__ void k_color_track(ColorTrackArgs a);
 __global__ void k_track_fail(const PoseD* state, IcpResult* res);
 

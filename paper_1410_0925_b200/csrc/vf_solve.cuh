@@ -361,6 +361,63 @@ __device__ __forceinline__ bool spd_solve_fast(const double* __restrict__ tot, d
   return true;
 }
 
+// Levenberg-Marquardt step of color_track (color_tracker.hpp:126-133): solve
+// (H with its diagonal scaled by 1 + lambda) x = -g, fully unrolled in
+// registers (unpivoted LDL^T; differs from Eigen's pivoted LDLT by rounding
+// only).  Returns false when the damped system is not numerically SPD, so the
+// caller takes the reference's pivoted path.
+__device__ __forceinline__ bool spd_solve_damped6(const double* __restrict__ tot, double lambda, double* twist) {
+  constexpr int N = 6;
+  double H[N][N];
+#pragma unroll
+  for (int s = 0, k = 0; s < N; ++s)
+#pragma unroll
+    for (int t = s; t < N; ++t, ++k) {
+      H[s][t] = tot[k];
+      H[t][s] = tot[k];
+    }
+#pragma unroll
+  for (int s = 0; s < N; ++s) H[s][s] *= (1.0 + lambda);
+  double L[N][N], D[N], Dinv[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double d = H[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= (L[j][k] * L[j][k]) * D[k];
+    if (!(d > 0) || !isfinite(d)) return false;
+    D[j] = d;
+    Dinv[j] = rcp_fast(d);
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      double sum = H[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) sum -= (L[i][k] * L[j][k]) * D[k];
+      L[i][j] = sum * Dinv[j];
+    }
+  }
+  double y[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = -tot[21 + i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) v -= L[i][k] * y[k];
+    y[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i] *= Dinv[i];
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    double v = y[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) v -= L[k][i] * twist[k];
+    twist[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (!isfinite(twist[i])) return false;
+  return true;
+}
+
 // Reduce 32 per-lane values across the warp with a transpose butterfly:
 // 31 shuffles instead of 5 per value.  On return lane l holds the warp sum
 // of value index l.

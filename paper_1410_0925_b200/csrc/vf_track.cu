@@ -24,6 +24,8 @@
 // one 1024-thread CTA: each evaluation is a block reduction of 29 FP64 sums,
 // thread 0 runs the damping / accept / reject logic, and nothing leaves the
 // SM until the pose is decided.
+#include <cooperative_groups.h>
+
 #include "vf_device.cuh"
 #include "vf_kernels.h"
 #include "vf_solve.cuh"
@@ -317,7 +319,7 @@ __device__ void evaluate_color(const float* __restrict__ pts, const float* __res
   double acc[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) acc[k] = 0.0;
-  for (int i = threadIdx.x * stride; i < n; i += blockDim.x * stride) {
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * stride; i < n; i += gridDim.x * blockDim.x * stride) {
     const D3 p = mk((double)pts[3 * i], (double)pts[3 * i + 1], (double)pts[3 * i + 2]);
     const D3 q = apply(w2c, p);
     if (q.z <= 0.0) continue;
@@ -356,11 +358,40 @@ __device__ void evaluate_color(const float* __restrict__ pts, const float* __res
   block_reduce32(acc, s_red, s_out);
 }
 
+// evaluate_color over a cooperative grid: every CTA reduces its share, the
+// per-CTA sums meet behind one grid barrier (double-buffered), and every CTA
+// adds them in CTA order, so all CTAs hold identical sums and take identical
+// decisions.  One CTA: evaluate_color itself.
+__device__ void evaluate_color_grid(const ColorTrackArgs& a, int n, const ColorLevel& lv, const PoseD& w2c,
+                                    double* s_red, double* s_out, int& buf) {
+  evaluate_color(a.points, a.colors, n, a.stride, lv, w2c, s_red, s_out);
+  if (gridDim.x == 1) return;
+  double* part = a.partials + (size_t)buf * gridDim.x * 32;
+  if (threadIdx.x < 29) part[(size_t)blockIdx.x * 32 + threadIdx.x] = s_out[threadIdx.x];
+  cooperative_groups::this_grid().sync();
+  if (threadIdx.x < 29) {
+    double t = 0.0;
+    int b = 0;
+    for (; b + 8 <= (int)gridDim.x; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcg(part + (size_t)(b + k) * 32 + threadIdx.x);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += v[k];
+    }
+    for (; b < (int)gridDim.x; ++b) t += __ldcg(part + (size_t)b * 32 + threadIdx.x);
+    s_out[threadIdx.x] = t;
+  }
+  __syncthreads();
+  buf ^= 1;
+}
+
 }  // namespace
 
-// color_track (color_tracker.hpp:107-154) in one CTA.  Writes the frame's
-// TrackingResult; the pose when ok and update_state.
-__global__ void __launch_bounds__(1024) k_color_track(ColorTrackArgs a) {
+// color_track (color_tracker.hpp:107-154), in one CTA or over a cooperative
+// grid (every CTA runs the same damping logic on the same sums).  Writes the
+// frame's TrackingResult; the pose when ok and update_state.
+__global__ void __launch_bounds__(kColorThreads) k_color_track(ColorTrackArgs a) {
   __shared__ double s_red[32 * 32];
   __shared__ double s_eval[32], s_trial[32];
   __shared__ PoseD s_pose, s_cand;
@@ -375,13 +406,30 @@ __global__ void __launch_bounds__(1024) k_color_track(ColorTrackArgs a) {
   if (threadIdx.x == 0) s_pose = init;
   __syncthreads();
   const bool have = n > 0;  // points.empty() -> not ok (color_tracker.hpp:111)
+  int buf = 0;
   for (int level = a.levels - 1; have && level >= 0; --level) {
     const ColorLevel& lv = a.lv[level];
     double lambda = 0.01;
-    evaluate_color(a.points, a.colors, n, a.stride, lv, s_pose, s_red, s_eval);
+    evaluate_color_grid(a, n, lv, s_pose, s_red, s_eval, buf);
     if ((long long)s_eval[28] < a.min_valid_points) continue;
     any_level_ok = true;
     for (int iter = 0; iter < a.max_iterations; ++iter) {
+#ifndef VF_COLOR_EXACT_LDLT
+      if (threadIdx.x == 0) {
+        double tw[6];
+        if (spd_solve_damped6(s_eval, lambda, tw)) {
+          s_flag = 0;
+          s_cand = pose_increment(s_pose, tw, false);
+          double tn = 0.0;
+          for (int p = 0; p < 6; ++p) tn += tw[p] * tw[p];
+          s_twist_norm = sqrt(tn);
+        } else {
+          s_flag = 2;  // not numerically SPD: the reference's pivoted path below
+        }
+      }
+      __syncthreads();
+      if (s_flag == 2)
+#endif
       if (threadIdx.x == 0) {
         s_flag = 0;
         double h[36];
@@ -404,7 +452,7 @@ __global__ void __launch_bounds__(1024) k_color_track(ColorTrackArgs a) {
       }
       __syncthreads();
       if (s_flag) break;
-      evaluate_color(a.points, a.colors, n, a.stride, lv, s_cand, s_red, s_trial);
+      evaluate_color_grid(a, n, lv, s_cand, s_red, s_trial, buf);
       ++iterations_total;
       const double ec = s_eval[28] > 0 ? s_eval[27] / s_eval[28] : 0.0;
       const double tc = s_trial[28] > 0 ? s_trial[27] / s_trial[28] : 0.0;
@@ -426,7 +474,7 @@ __global__ void __launch_bounds__(1024) k_color_track(ColorTrackArgs a) {
     final_cost = s_eval[28] > 0 ? s_eval[27] / s_eval[28] : 0.0;
     valid_points = (int)s_eval[28];
   }
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     IcpResult r;
     r.final_cost = final_cost;
     r.valid_points = valid_points;

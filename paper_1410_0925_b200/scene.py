@@ -270,6 +270,11 @@ CONFIGS = {
     # exhaust the 2^18-block pool after ~30 m and drop allocations).
     "C4": BenchConfig("C4", 640, 480, 0.005, frames=1000, use_swapping=True, swap_buffer_blocks=512,
                       scene="corridor"),
+    # the other trackers on the C1 / C2 frames:
+    # icp_ren = ICP on the coarser levels + Ren SDF refinement at full
+    # resolution; color = photometric tracking against the colour surface list
+    "C1R": BenchConfig("C1R", 640, 480, 0.005, tracker="icp_ren"),
+    "C2T": BenchConfig("C2T", 640, 480, 0.005, voxel_type=2, tracking=True, tracker="color"),
     "T320": BenchConfig(
         "T320", 320, 240, 0.01, mu=0.03, frames=6,
         hash=HashConfig(bucket_count=1 << 17, excess_count=1 << 14, block_count=1 << 15),
