@@ -173,8 +173,17 @@ __global__ void k_ren_ctl(const double* __restrict__ partials, int nparts, RenCt
   if (ctl->done) return;
   const int lane = threadIdx.x;
   double t = 0.0;
-  if (lane < 29)
-    for (int b = 0; b < nparts; ++b) t += partials[(size_t)b * 32 + lane];
+  if (lane < 29) {  // CTA order; eight loads in flight per step
+    int b = 0;
+    for (; b + 8 <= nparts; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = partials[(size_t)(b + k) * 32 + lane];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += v[k];
+    }
+    for (; b < nparts; ++b) t += partials[(size_t)b * 32 + lane];
+  }
   s_tot[lane] = t;
   __syncwarp();
   if (lane != 0) return;
@@ -193,18 +202,23 @@ __global__ void k_ren_ctl(const double* __restrict__ partials, int nparts, RenCt
     ctl->ok = 1;
     return;
   }
-  double h[36];
-  for (int a = 0, k = 0; a < 6; ++a)
-    for (int b = a; b < 6; ++b, ++k) h[a * 6 + b] = h[b * 6 + a] = tot[k];
-  Ldlt f;
-  f.compute(h, 6);
-  if (!well_conditioned(h, 6, f, max_condition)) {
-    ctl->done = 1;
-    return;
+  double twist[6];
+  // the register LDL^T with the condition bound (as K4's controller); the
+  // reference's pivoted LDLT + SVD test only when the bound is inconclusive
+  if (!spd_solve_fast<6>(tot, max_condition, twist)) {
+    double h[36];
+    for (int a = 0, k = 0; a < 6; ++a)
+      for (int b = a; b < 6; ++b, ++k) h[a * 6 + b] = h[b * 6 + a] = tot[k];
+    Ldlt f;
+    f.compute(h, 6);
+    if (!well_conditioned(h, 6, f, max_condition)) {
+      ctl->done = 1;
+      return;
+    }
+    double ng[6];
+    for (int a = 0; a < 6; ++a) ng[a] = -tot[21 + a];
+    f.solve(ng, twist);
   }
-  double ng[6], twist[6];
-  for (int a = 0; a < 6; ++a) ng[a] = -tot[21 + a];
-  f.solve(ng, twist);
   ctl->c2w = pose_increment(ctl->c2w, twist, false);
   ++ctl->iterations;
   double tn = 0.0;
