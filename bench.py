@@ -452,7 +452,7 @@ def run_ours(args, dist: Dist):
         stage_kernels = {"raycast": ("k_raycast",), "tracking": ("k_pyramid", "k_icp_cluster", "k_icp")}
         rows = {}
         for stage, kernels in stage_kernels.items():
-            b = sum((ncu_kernel_bytes("r1h_ncu.json", "c1_full", k) or 0.0) for k in kernels)
+            b = sum((ncu_kernel_bytes("r1i_ncu.json", "c1_full", k) or 0.0) for k in kernels)
             ms = stages.get(stage, 0.0)
             if b > 0 and ms > 0:
                 gbs = b / (ms * 1e-3) / 1e9
@@ -521,8 +521,8 @@ def run_ours(args, dist: Dist):
 # Committed `ncu --set full` captures of the roofline kernel per config
 # (profiles/): dram__bytes_read.sum + dram__bytes_write.sum of one launch.
 NCU_TRAFFIC = {
-    "C1": ("r1h_ncu.json", "c1_full", "k_integrate_s"),
-    "C3": ("r1h_ncu.json", "c3_integrate", "k_integrate_s"),
+    "C1": ("r1i_ncu.json", "c1_full", "k_integrate_s"),
+    "C3": ("r1i_ncu.json", "c3_integrate", "k_integrate_s"),
     "C2": ("r1d_ncu_c2c4.json", "c2_rgb", "k_integrate_rgb"),
 }
 
