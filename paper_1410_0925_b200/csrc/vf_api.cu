@@ -369,7 +369,8 @@ int enqueue_color(vf_ctx* c, cudaStream_t st, const PoseD* explicit_init, bool u
   a.partials = c->partials;
   // one CTA per kColorThreads surface points (up to one per SM), over a
   // cooperative grid: an evaluation is then one point per thread deep
-  const int g = std::max(1, std::min({c->num_sms, c->icp_grid, (c->surf_cap + kColorThreads - 1) / kColorThreads}));
+  int g = std::max(1, std::min({c->num_sms, c->icp_grid, (c->surf_cap + kColorThreads - 1) / kColorThreads}));
+  if (const char* e = std::getenv("VF_COLOR_GRID")) g = std::max(1, std::min(g, std::atoi(e)));  // tuning override
   if (g == 1) {
     k_color_track<<<1, kColorThreads, 0, st>>>(a);
   } else {
