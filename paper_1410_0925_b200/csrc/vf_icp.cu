@@ -15,6 +15,10 @@
 // so all CTAs agree on every branch without a second barrier.  Coarse levels
 // with few pixels run on CTA 0 alone with no grid barrier at all.
 //
+// The per-iteration pixel pass is software-pipelined one pixel deep: the next
+// pixel's transforms run and its map taps are fetched into shared memory with
+// cp.async while the current pixel's terms are summed.
+//
 // Controller arithmetic: the twist comes from the same pivoted LDLT as the
 // reference's Eigen call; the SVD condition test is first decided by the
 // rigorous bound cond <= |H|_F |H^-1|_F (exact answer whenever the bound is

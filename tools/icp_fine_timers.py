@@ -1,5 +1,8 @@
 """ICP pixel-pass sub-phase timers (SM cycles, CTA 0 thread 0, first pixel pair):
-needs a library built with -DVF_ICP_FINE_TIMERS (VOXFUSE_B200_LIB=...)."""
+needs a library built with -DVF_ICP_FINE_TIMERS -DVF_ICP_LEGACY_LOOP
+-DVF_ICP_INFLIGHT=2 (VOXFUSE_B200_LIB=...): the sub-phases exist only in the
+non-pipelined loop; tools/icp_timers.py gives the per-phase totals of the
+default build."""
 import os
 os.environ.setdefault("VF_ICP_TRACE", "1")
 import sys
