@@ -46,7 +46,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "frames/sec (alloc+integrate+raycast+ICP) at 640x480; voxel updates/sec"
+METRIC = "frames/sec (alloc+integrate+raycast+ICP) at 640\u00d7480; voxel updates/sec"  # BASELINE.json metric, verbatim
 UNIT = "frames/s"
 
 
