@@ -101,3 +101,14 @@ def test_no_fp32x2_contraction_in_sass():
         n_ptx = len(re.findall(r"\bfma\.r[nzmp]\.f32x2\b", ptx))
         n_sass = len(re.findall(r"\bFFMA2\b", sass))
         assert n_ptx == n_sass, f"{src}: {n_sass} FFMA2 in SASS vs {n_ptx} fma.f32x2 in PTX"
+
+
+def test_bench_metric_is_the_baseline_metric():
+    """bench.py reports BASELINE.json's metric verbatim (both arms)."""
+    import json
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    import bench
+    assert bench.METRIC == json.loads((root / "BASELINE.json").read_text())["metric"]
