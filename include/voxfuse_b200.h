@@ -308,6 +308,15 @@ int vf_event_elapsed_ms(vf_ctx* ctx, int slot_a, int slot_b, float* ms);
  * vf_stage_times returns accumulated milliseconds per stage. */
 int vf_set_profiling(vf_ctx* ctx, int enabled);
 int vf_stage_times(vf_ctx* ctx, double* ms_out /* 8 */, long* frames);
+/* FrameStats::ms_* per frame (pipeline.hpp:56-57; the reference fills them on
+ * every frame, pipeline_impl.hpp:66-120): when enabled, the blocking calls
+ * (vf_process_frame / _device / vf_process_raw_frame) return the stage times
+ * of that frame in vf_frame_stats.ms_tracking .. ms_raycast, from event
+ * records inside the frame graph (no extra launches, no serialisation; the
+ * side branch -- range image and swap engine -- overlaps integration, so
+ * ms_swapping is the wait for it).  The streaming pair returns ms_total only.
+ * Off by default in the C ABI; the IPipeline adapter turns it on. */
+int vf_set_stage_timing(vf_ctx* ctx, int enabled);
 int vf_kernel_launches_per_frame(vf_ctx* ctx, int tracking_frame);
 /* Bytes of the per-frame stats readback (the D2H of vf_process_frame). */
 long vf_readback_bytes(const vf_ctx* ctx);

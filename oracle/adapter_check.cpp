@@ -19,6 +19,12 @@ using namespace voxfuse;
 
 extern "C" {
 
+// FrameStats::ms_* of the last frame vfa_run processed through
+// IPipeline::process_frame (tracking, allocation, integration, swapping,
+// raycast, total; pipeline.hpp:56-57)
+static double g_last_ms[6];
+void vfa_last_stage_ms(double* out) { std::memcpy(out, g_last_ms, sizeof(g_last_ms)); }
+
 struct vfa_config {  // same layout as vfr_config (oracle/ref_driver.cpp)
   int voxel_type;
   float voxel_size, mu;
@@ -118,6 +124,9 @@ int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, c
         std::memcpy(col.pixels().data(), rgb + f * npix * 3, npix * 3);
       }
       const FrameStats st = p->process_frame(rgb ? &col : nullptr, d);
+      const double ms[6] = {st.ms_tracking, st.ms_allocation, st.ms_integration,
+                            st.ms_swapping, st.ms_raycast, st.ms_total};
+      std::memcpy(g_last_ms, ms, sizeof(ms));
       const Pose& pose = p->pose();
       for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) poses[f * 12 + i * 3 + j] = pose.rotation()(i, j);

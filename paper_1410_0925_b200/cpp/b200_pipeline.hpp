@@ -130,6 +130,8 @@ class B200Pipeline final : public voxfuse::IPipeline {
     const int rc = vf_create(&s, &c, device, &ctx_);
     if (rc == VF_ERR_INVALID) throw std::invalid_argument("voxfuse_b200: invalid settings");
     detail::check(rc, "vf_create", nullptr);
+    // the reference fills FrameStats::ms_* on every frame (pipeline_impl.hpp:66-120)
+    detail::check(vf_set_stage_timing(ctx_, 1), "vf_set_stage_timing", ctx_);
   }
   ~B200Pipeline() override {
     // swap_store_path (pipeline.hpp:23): the reference streams records into a
@@ -210,7 +212,14 @@ class B200Pipeline final : public voxfuse::IPipeline {
     fs.swap.swapped_out = st.swapped_out;
     fs.swap.bytes_in = st.swap_bytes_in;
     fs.swap.bytes_out = st.swap_bytes_out;
-    fs.ms_total = st.ms_total;  // GPU time of the frame (CUDA events)
+    // GPU time of the frame and of its stages (CUDA events in the frame graph;
+    // the streaming calls carry ms_total only)
+    fs.ms_tracking = st.ms_tracking;
+    fs.ms_allocation = st.ms_allocation;
+    fs.ms_integration = st.ms_integration;
+    fs.ms_swapping = st.ms_swapping;
+    fs.ms_raycast = st.ms_raycast;
+    fs.ms_total = st.ms_total;
     return fs;
   }
 

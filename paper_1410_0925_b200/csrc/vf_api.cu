@@ -153,12 +153,14 @@ struct vf_ctx {
   bool rgb_valid = false;
 
   // graphs: [tracking][rgb]
-  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  // frame graphs per [tracking][rgb][stage timing]
+  cudaGraphExec_t graph[2][2][2] = {};
   bool graphs_ok = true;
 
   cudaEvent_t ev[kNumEvents] = {};
   cudaEvent_t ev_frame0 = nullptr, ev_frame1 = nullptr;
   bool profiling = false;
+  bool stage_timing = false;  // per-frame FrameStats::ms_* (event nodes in the frame graph)
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long profiled_frames = 0;
   int launches_last = 0;
@@ -282,7 +284,7 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
 }
 
 void stage_mark(vf_ctx* c, int slot) {
-  if (c->profiling) cudaEventRecord(c->ev[slot], c->stream);
+  if (c->profiling || c->stage_timing) cudaEventRecord(c->ev[slot], c->stream);
 }
 
 // VF_DEBUG_SYNC=1: synchronise and check after every launch (debugging only).
@@ -574,7 +576,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
 
 int run_frame(vf_ctx* c, bool track, bool with_rgb) {
   if (c->s.use_graphs && c->graphs_ok && !c->profiling && !debug_sync()) {
-    cudaGraphExec_t& g = c->graph[track][with_rgb];
+    cudaGraphExec_t& g = c->graph[track][with_rgb][c->stage_timing];
     if (!g) {
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
@@ -675,6 +677,17 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev_frame0, c->ev_frame1);
     stats->ms_total = ms;
+    if (c->stage_timing || c->profiling) {
+      // FrameStats::ms_tracking .. ms_raycast (pipeline.hpp:56-57) from the
+      // stage marks of this frame: tracking, allocation, integration, the
+      // wait for the side branch (range image + swap engine), raycast
+      double* out[5] = {&stats->ms_tracking, &stats->ms_allocation, &stats->ms_integration, &stats->ms_swapping,
+                        &stats->ms_raycast};
+      for (int i = 0; i < 5; ++i) {
+        float m = 0;
+        if (cudaEventElapsedTime(&m, c->ev[i], c->ev[i + 1]) == cudaSuccess) *out[i] = m;
+      }
+    }
     if (c->hstate->ctr.error_flags) return VF_ERR_OVERFLOW;
   }
   return VF_OK;
@@ -684,17 +697,24 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
 // stream and the per-slot events.
 int ensure_queue(vf_ctx* c) {
   if (c->copy) return VF_OK;
-  VF_CUDA(c, cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  // Every resource is created only if still missing, and the copy stream --
+  // the "queue is ready" flag -- last: a failure part way leaves c->copy null,
+  // so the next submit retries the missing pieces instead of running with
+  // null staging buffers or events.
   for (int k = 0; k < kMaxFramesInFlight; ++k) {
-    VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->depth_stage[k]), sizeof(float) * (size_t)c->npix));
-    if (c->vsize == 8)
+    if (!c->depth_stage[k])
+      VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->depth_stage[k]), sizeof(float) * (size_t)c->npix));
+    if (c->vsize == 8 && !c->rgb_stage[k])
       VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->rgb_stage[k]), 3 * (size_t)c->rgbin.width * c->rgbin.height));
-    VF_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->hstate_q[k]), sizeof(DevState)));
+    if (!c->hstate_q[k]) VF_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->hstate_q[k]), sizeof(DevState)));
     for (cudaEvent_t* e : {&c->ev_up[k], &c->ev_consumed[k], &c->ev_done[k]})
-      VF_CUDA(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    VF_CUDA(c, cudaEventCreate(&c->ev_q0[k]));
-    VF_CUDA(c, cudaEventCreate(&c->ev_q1[k]));
+      if (!*e) VF_CUDA(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    if (!c->ev_q0[k]) VF_CUDA(c, cudaEventCreate(&c->ev_q0[k]));
+    if (!c->ev_q1[k]) VF_CUDA(c, cudaEventCreate(&c->ev_q1[k]));
   }
+  cudaStream_t copy = nullptr;
+  VF_CUDA(c, cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+  c->copy = copy;
   return VF_OK;
 }
 
@@ -779,9 +799,10 @@ int dalloc(vf_ctx* c, T** p, size_t bytes) {
 
 void free_all(vf_ctx* c) {
   if (c->nccl_comm) nccl_comm_destroy(c->nccl_comm);
-  for (auto& row : c->graph)
-    for (auto& g : row)
-      if (g) cudaGraphExecDestroy(g);
+  for (auto& plane : c->graph)
+    for (auto& row : plane)
+      for (auto& g : row)
+        if (g) cudaGraphExecDestroy(g);
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
                   c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
@@ -983,7 +1004,11 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   }
   if (s->shard_count > 1) {
     if (s->shard_count > kMaxShards || s->shard_index < 0 || s->shard_index >= s->shard_count || s->shard_shift < 0 ||
-        s->shard_shift > 8) {
+        s->shard_shift > 8 ||
+        // Only ICP is shard-safe: it reads the composited maps, identical on
+        // every rank.  The Ren and colour trackers read the shard's own voxels,
+        // so each rank would compute a different pose (vf_shard.cu header).
+        s->tracker_type != VF_TRACKER_ICP) {
       free_all(c);
       delete c;
       return VF_ERR_INVALID;
@@ -1810,6 +1835,11 @@ int vf_set_profiling(vf_ctx* c, int enabled) {
   c->profiled_frames = 0;
   return VF_OK;
 }
+int vf_set_stage_timing(vf_ctx* c, int enabled) {
+  if (!c) return VF_ERR_INVALID;
+  c->stage_timing = enabled != 0;
+  return VF_OK;
+}
 int vf_stage_times(vf_ctx* c, double* ms_out, long* frames) {
   if (!c || !ms_out) return VF_ERR_INVALID;
   for (int i = 0; i < 8; ++i) ms_out[i] = c->stage_ms[i];
@@ -1849,12 +1879,13 @@ int vf_shard_attach_nccl(vf_ctx* c, const void* id, int nranks, int rank) {
     c->err = "ncclCommInitRank failed";
     return VF_ERR_CUDA;
   }
-  for (auto& row : c->graph)  // the frame graph now ends with the composite
-    for (auto& g : row)
-      if (g) {
-        cudaGraphExecDestroy(g);
-        g = nullptr;
-      }
+  for (auto& plane : c->graph)  // the frame graph now ends with the composite
+    for (auto& row : plane)
+      for (auto& g : row)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
   return VF_OK;
 }
 

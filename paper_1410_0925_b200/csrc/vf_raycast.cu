@@ -10,11 +10,14 @@
 // values are positive, so integer order is float order); min/max commute, so
 // the result equals the reference's serial fold.
 //
-// K3b: one CTA per 16x16 fragment (one range per CTA), one thread per pixel.
-// The reference probes the hash table for every voxel sample (1 per march
-// step, 8 per trilinear, 48 per normal).  Each thread keeps a 4-entry cache
-// of block -> VBA slot (misses included) in registers; the table does not
-// change during the raycast, so the values read — and therefore every
+// K3b: 128-thread CTAs cover half a 16x16 fragment (one range per CTA), one
+// thread per pixel, each warp an 8x4 pixel patch.  The reference probes the
+// hash table for every voxel sample (1 per march step, 8 per trilinear, 48
+// per normal).  Each thread keeps a direct-mapped 8-way cache of block -> VBA
+// slot (misses included) in shared memory, laid out [way][thread] so lookups
+// are bank-conflict free, the way chosen by block-coordinate parity so the
+// 2x2x2 blocks of a trilinear stencil never evict each other.  The table does
+// not change during the raycast, so the values read — and therefore every
 // floating-point decision — are identical to the uncached reference.
 #include "vf_device.cuh"
 #include "vf_kernels.h"

@@ -161,13 +161,19 @@ class FrameStats:
     swapped_out: int = 0
     bytes_in: int = 0
     bytes_out: int = 0
+    ms_tracking: float = 0.0  # per-stage ms (pipeline.hpp:56), with set_stage_timing(True)
+    ms_allocation: float = 0.0
+    ms_integration: float = 0.0
+    ms_swapping: float = 0.0
+    ms_raycast: float = 0.0
 
     @classmethod
     def from_c(cls, s: VfFrameStats) -> "FrameStats":
         return cls(s.frame, bool(s.tracking_ok), s.tracking_iterations, s.tracking_cost, s.blocks_allocated,
                    s.allocation_dropped, s.visible_blocks, np.array(s.pose[:]), s.ms_total, s.allocation_requested,
                    s.allocated_total, s.tracking_valid_points, s.error_flags, s.swapped_in, s.swapped_out,
-                   s.swap_bytes_in, s.swap_bytes_out)
+                   s.swap_bytes_in, s.swap_bytes_out, s.ms_tracking, s.ms_allocation, s.ms_integration,
+                   s.ms_swapping, s.ms_raycast)
 
 
 def _ptr(a):
@@ -192,6 +198,10 @@ class Pipeline:
     """IPipeline over one device-resident voxel-block hash volume."""
 
     def __init__(self, settings: EngineSettings, calib: Calibration, device: int = 0):
+        if settings.shard_count > 1 and settings.tracker_type != TRACKER_TYPES["icp"]:
+            # mirrors vf_create: only ICP reads the composited (rank-identical)
+            # maps; Ren / colour read the shard's own voxels and would diverge
+            raise ValueError("spatial sharding (shard_count > 1) requires the ICP tracker")
         self._L = _abi.load()
         self._settings = settings
         self._calib = calib
@@ -509,6 +519,11 @@ class Pipeline:
     # -- profiling --
     def set_profiling(self, enabled: bool) -> None:
         self._chk("vf_set_profiling", self._L.vf_set_profiling(self._h, int(enabled)))
+
+    def set_stage_timing(self, enabled: bool) -> None:
+        """Fill FrameStats.ms_tracking .. ms_raycast on every blocking frame
+        (pipeline.hpp:56-57) from event records inside the frame graph."""
+        self._chk("vf_set_stage_timing", self._L.vf_set_stage_timing(self._h, int(enabled)))
 
     def stage_times(self):
         ms = np.zeros(8)

@@ -60,6 +60,23 @@ def test_ipipeline_frame0_identical(olib, alib):
     assert np.array_equal(ref[8], gpu[8]), "get_image(depth_colourized) differs"
 
 
+def test_ipipeline_frame_stats_stage_ms(olib, alib):
+    """FrameStats::ms_* (pipeline.hpp:56-57) come back through IPipeline on a
+    tracked frame, as the reference fills them (pipeline_impl.hpp:66-120):
+    every stage > 0 except swapping (off), stages summing to about ms_total."""
+    cfg = CONFIGS["C1"]
+    fr = frames(olib, cfg, 3)
+    lib_ms = (C.c_double * 6)()
+    alib.vfa_last_stage_ms.argtypes = [C.c_void_p]
+    for engine in (0, 1):
+        _run(alib, cfg, engine, fr)
+        alib.vfa_last_stage_ms(lib_ms)
+        trk, alloc, integ, swap, ray, total = list(lib_ms)
+        assert total > 0 and trk > 0 and alloc > 0 and integ > 0 and ray > 0, (engine, list(lib_ms))
+        assert swap >= 0
+        assert trk + alloc + integ + swap + ray <= total * 1.05 + 0.05, (engine, list(lib_ms))
+
+
 def test_ipipeline_tracked_sequence(olib, alib):
     cfg = CONFIGS["C1"]
     fr = frames(olib, cfg, 5)

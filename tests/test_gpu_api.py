@@ -37,6 +37,48 @@ def test_invalid_settings_rejected(overrides):
     assert e.value.status == VF_ERR_INVALID
 
 
+def test_sharding_requires_icp():
+    """Only ICP reads the rank-identical composited maps; Ren / colour would
+    track against the shard's own voxels, so vf_create refuses them (and the
+    Python mirror raises before reaching it)."""
+    from dataclasses import replace
+    s, c = settings_from_config(CONFIGS["T160"])
+    bad = replace(s, shard_count=2, shard_index=0, tracker_type=2)
+    with pytest.raises(ValueError):
+        make_pipeline(bad, c)
+    L = _abi.load()
+    h = C.c_void_p()
+    cs, cc = bad.to_c(), c.to_c()
+    assert L.vf_create(C.byref(cs), C.byref(cc), 0, C.byref(h)) == VF_ERR_INVALID
+    ok = replace(s, shard_count=2, shard_index=0, tracker_type=0)
+    make_pipeline(ok, c).close()
+
+
+def test_stage_timing_fills_frame_stats():
+    """vf_set_stage_timing: the blocking call returns this frame's stage times
+    (FrameStats::ms_*, pipeline.hpp:56-57) from the replayed graph."""
+    p = _create()
+    from paper_1410_0925_b200.scene import trajectory
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import vf_py
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES
+    olib = vf_py.oracle_lib()
+    cfg = CONFIGS["T160"]
+    poses = trajectory(4)
+    frames = [vf_py.render_depth(olib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) for i in range(4)]
+    st = p.process_frame(None, frames[0])
+    assert st.ms_tracking == 0 and st.ms_raycast == 0  # off by default
+    p.set_stage_timing(True)
+    for i in range(1, 4):
+        st = p.process_frame(None, frames[i])
+        parts = [st.ms_tracking, st.ms_allocation, st.ms_integration, st.ms_swapping, st.ms_raycast]
+        assert st.tracking_ok and all(x >= 0 for x in parts) and st.ms_tracking > 0 and st.ms_raycast > 0
+        assert sum(parts) <= st.ms_total * 1.05 + 0.02, (parts, st.ms_total)
+    p.close()
+
+
 def test_calls_in_the_wrong_state():
     p = _create()
     L = _abi.load()
