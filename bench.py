@@ -20,14 +20,15 @@ once, outside the timed region.
 * cpu_baseline: the reference's own code (oracle/_ref, shim-built) on the
   host cores, bounded sample, rank 0 at N=1 only.
 * --impl reference: that CPU reference as the arm of record.
-Under torchrun (N>1), by default every rank runs its own copy of the camera
-sequence on its own GPU — the frames of one sequence are sequential (each is tracked
-against the previous frame's raycast), so sequences are the units sharded
-across ranks, with no data-path collective ("scaling": "weak").  --mode shard
-runs config 5 instead: one volume spatially sharded by block hash across the
-GPUs, every rank on the same frames, maps composited per pixel with NCCL
-inside the frame graph; that adds capacity, not frames/s, and is reported as
-"strong".
+N>1 (`--gpus N` re-launches itself under torch.distributed.run, one rank
+per GPU): by default config 5 — one volume (the C5 corridor) spatially
+sharded by block hash across the GPUs, every rank on the same frames,
+allocation / integration / raycast on its own shard, maps composited per
+pixel with NCCL collectives inside the frame graph, ICP replicated on the
+composited maps ("scaling": "strong": it adds capacity and shares the voxel
+work, the frame is still one sequential step).  `--mode replica` runs an
+independent copy of the sequence per GPU instead (no data-path collective,
+"weak").  `--dry-run` launches the ranks and forms the process group only.
 """
 from __future__ import annotations
 
@@ -55,15 +56,70 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C1")
+    ap.add_argument("--config", default=None,
+                    help="default: C1 at N=1; C5 (the sharded corridor) at N>1 in shard mode")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample inside our arm")
+    ap.add_argument("--ref-seconds", type=float, default=240.0, help="--impl reference: time budget")
     ap.add_argument("--l2-flush-mib", type=int, default=256)
-    ap.add_argument("--mode", default="replica", choices=["shard", "replica"],
-                    help="N>1: independent sequences per GPU (default) or one volume sharded across the GPUs "
-                         "(config 5, NCCL map composite)")
+    ap.add_argument("--mode", default=None, choices=["shard", "replica"],
+                    help="N>1: one volume spatially sharded by block hash across the GPUs (default; config 5, "
+                         "NCCL nearest-depth map composite in the frame graph) or independent sequences per GPU")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the ranks and set up the process group, report them, run nothing on the GPU")
     return ap.parse_args()
+
+
+def resolve(args, world: int):
+    """Mode and config after the launch: N>1 defaults to config 5 sharded."""
+    if world > 1:
+        args.mode = args.mode or "shard"
+        args.config = args.config or ("C5" if args.mode == "shard" else "C1")
+    else:
+        args.mode = "single"
+        args.config = args.config or "C1"
+    return args
+
+
+def free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run this command under
+    torch.distributed.run with one rank per GPU (rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def config_dict(cfg, args, world: int) -> dict:
+    """The `config` of the JSON line -- identical in both arms."""
+    fx, fy, cx, cy, w, h = cfg.intrinsics
+    rgb = cfg.voxel_type == 2
+    sharded = world > 1 and args.mode == "shard"
+    return {
+        "workload": f"{cfg.name}: {w}x{h} depth, {cfg.voxel_size * 1000:.0f} mm voxels, mu {cfg.mu * 1000:.0f} mm, "
+                    f"{'VoxelSRgb' if rgb else 'VoxelS'}, hash {cfg.hash.bucket_count}x{cfg.hash.bucket_size}"
+                    f"+{cfg.hash.excess_count} / {cfg.hash.block_count} blocks"
+                    f"{' per shard' if sharded else ''}, "
+                    f"{'ICP tracking on' if cfg.tracking else 'known poses'}"
+                    + (f", {cfg.scene} scene" if cfg.scene != "box_room" else "")
+                    + (f", swapping B={cfg.swap_buffer_blocks}" if cfg.use_swapping else ""),
+        "frames": f"{args.warmup} warm-up (incl. frame 0) then frames {args.warmup}..{args.warmup + args.steps - 1} timed",
+        "parallelism": (f"volume sharded by block hash over {world} GPUs (NCCL map composite)" if sharded
+                        else f"one sequence per GPU x{world}" if world > 1 else "single GPU"),
+        "l2": f"flushed between frames ({args.l2_flush_mib} MiB write, outside the timed intervals)",
+        "graphs": True,
+    }
 
 
 # ---------------------------------------------------------------------------
@@ -204,7 +260,11 @@ def cpu_reference_run(cfg, n_frames: int, budget_s: float, threads: int = 0):
 
 
 def run_reference_arm(args, dist: Dist):
-    from paper_1410_0925_b200.scene import CONFIGS
+    """The reference's own CPU pipeline (oracle/_ref: the unmodified reference
+    sources, shim-built) on the SAME frames as our arm: frames 0..W-1 untimed
+    (frame 0 fixes the pose), frames W..W+K-1 timed one step each, all host
+    threads in the reference's pool (parallel.cpp:67-71).  Rank 0 only."""
+    from paper_1410_0925_b200.scene import CONFIGS, scene_for, trajectory_for
 
     cfg = CONFIGS[args.config]
     if dist.rank != 0:
@@ -215,34 +275,58 @@ def run_reference_arm(args, dist: Dist):
     if not vf_py.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libvoxfuse_ref.so not built"}))
         return
-    budget = max(5.0, min(60.0, args.cpu_seconds))
-    frames_each = max(1, min(args.steps, 10))
-    times, vps = [], []
-    res = None
-    for _ in range(max(1, min(args.warmup, 1))):
-        cpu_reference_run(cfg, 1, budget)  # warm-up: page in, pool spin-up
-    for _ in range(max(1, min(args.steps, 3))):
-        res = cpu_reference_run(cfg, frames_each, budget / 3)
-        times.append(res["fps"])
-        vps.append(res["voxel_updates_per_s"])
-    fps = float(np.mean(times))
-    fx, fy, cx, cy, w, h = cfg.intrinsics
-    sample = (f"{cfg.name}: frames 1..{res['frames']} of the tracked sequence per step (frame 0 untimed), "
-              f"{len(times)} steps, reference pipeline via make_pipeline/process_frame")
+    spheres, planes, far = scene_for(cfg)
+    lib = vf_py.ref_lib()
+    lib.lib.vfr_set_threads(os.cpu_count() or 1)
+    cores = int(lib.lib.vfr_get_threads())
+    n_frames = args.warmup + args.steps
+    poses = trajectory_for(cfg, n_frames)
+    vol = vf_py.Volume(lib, cfg, tracking=cfg.tracking)
+    rgb = cfg.voxel_type == 2
+    budget = max(60.0, args.ref_seconds)
+    times, vox = [], 0
+    stage = np.zeros(5)  # FrameStats::ms_* (pipeline.hpp:56-57)
+    for i in range(n_frames):
+        d = vf_py.render_depth(lib, cfg, poses[i], spheres, planes, 0.05, far)
+        c = vf_py.render_rgb(lib, cfg, poses[i], spheres, planes, 0.05, far) if rgb else None
+        t0 = time.perf_counter()
+        st = vol.process(d, c, None if cfg.tracking else poses[i])
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            vox += st.visible_blocks * 512
+            stage += [st.ms_tracking, st.ms_allocation, st.ms_integration, st.ms_swapping, st.ms_raycast]
+            if sum(times) > budget:  # bounded: a slow config stops early and says so
+                break
+    vol.close()
+    total = float(sum(times))
+    fps = len(times) / total
+    names = ("tracking", "allocation", "integration", "swapping", "raycast")
+    sample = (f"{cfg.name}: frames {args.warmup}..{args.warmup + len(times) - 1} of the sequence timed one per step "
+              f"after {args.warmup} untimed (frame 0 included), the reference pipeline via make_pipeline/process_frame")
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": len(times), "warmup": 1, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} {w}x{h} {cfg.voxel_size * 1000:.0f}mm voxels, {cfg.scene} scene"
-                               + (f", swapping B={cfg.swap_buffer_blocks}" if cfg.use_swapping else ""),
-                   "l2": "n/a (CPU)"},
-        "voxel_updates_per_s": float(np.mean(vps)),
-        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": res["cores"], "kind": "reference",
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(times),
+        "higher_is_better": True, "scaling": "strong" if args.mode == "shard" else "weak", "vs_baseline": None,
+        "dtype": "f32 (TSDF/raycast) + f64 (allocation DDA, ICP)", "data": data_desc(cfg, n_frames),
+        "config": config_dict(cfg, args, dist.world),
+        "voxel_updates_per_s": vox / total,
+        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "build": "the reference's unmodified sources, -O3, against the scalar Eigen shim "
+                                  "(oracle/eigen_shim: no SIMD Eigen on the box)",
                          "sample": sample},
-        "stage_ms": res["stage_ms"],
+        "stage_ms": {k: float(v) / max(len(times), 1) for k, v in zip(names, stage)},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **({"budget_stop": f"stopped after {total:.0f} s ({len(times)} of {args.steps} steps)"}
+           if len(times) < args.steps else {}),
     }
     print(json.dumps(line))
+
+
+def data_desc(cfg, n_frames: int) -> str:
+    if cfg.scene == "corridor":
+        return f"synthetic (corridor + pillars, {n_frames}-frame walk at 5 cm/frame)"
+    return "synthetic (box room + spheres, 100-frame small-motion trajectory)"
 
 
 # ---------------------------------------------------------------------------
@@ -255,6 +339,12 @@ def run_ours(args, dist: Dist):
 
     L = _abi.load()
     cfg = CONFIGS[args.config]
+    if dist.world > 1 and not os.environ.get("VF_BENCH_ONE_DEVICE"):
+        import torch
+
+        if torch.cuda.device_count() < dist.world:
+            raise SystemExit(f"bench.py --gpus {dist.world}: only {torch.cuda.device_count()} GPU(s) visible "
+                             "(VF_BENCH_ONE_DEVICE=1 runs every rank on GPU 0 for a plumbing test)")
     # VF_BENCH_ONE_DEVICE=1 puts every rank on GPU 0 (exercises the N>1 plumbing on a one-GPU box)
     device = 0 if os.environ.get("VF_BENCH_ONE_DEVICE") else dist.local_rank
     fx, fy, cx, cy, w, h = cfg.intrinsics
@@ -466,19 +556,8 @@ def run_ours(args, dist: Dist):
         "warmup": args.warmup, "ms_per_step": 1000.0 * t_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None,
         "dtype": "f32 (TSDF/raycast) + f64 (allocation DDA, ICP)",
-        "data": (f"synthetic (GPU-rendered corridor + pillars, {n_frames}-frame walk at 5 cm/frame)"
-                 if cfg.scene == "corridor" else
-                 "synthetic (GPU-rendered box room + spheres, 100-frame small-motion trajectory)"),
-        "config": {
-            "workload": f"{cfg.name}: {w}x{h} depth, {cfg.voxel_size * 1000:.0f} mm voxels, mu {cfg.mu * 1000:.0f} mm, "
-                        f"{'VoxelSRgb' if rgb else 'VoxelS'}, hash {cfg.hash.bucket_count}x{cfg.hash.bucket_size}"
-                        f"+{cfg.hash.excess_count} / {cfg.hash.block_count} blocks, "
-                        f"{'ICP tracking on' if cfg.tracking else 'known poses'}",
-            "parallelism": (f"volume sharded by block hash over {dist.world} GPUs (NCCL map composite)" if sharded
-                            else f"one sequence per GPU x{dist.world}" if dist.world > 1 else "single GPU"),
-            "l2": f"flushed between frames ({args.l2_flush_mib} MiB write, outside the timed intervals)",
-            "graphs": True,
-        },
+        "data": data_desc(cfg, n_frames),
+        "config": config_dict(cfg, args, dist.world),
         "voxel_updates_per_s": vox_updates,
         "stage_ms": stages,
         # per-stage throughput in the units of SURVEY.md §8(d)
@@ -511,6 +590,8 @@ def run_ours(args, dist: Dist):
         ref = cpu_reference_run(cfg, min(n_frames - 1, 30), args.cpu_seconds)
         if ref:
             line["cpu_baseline"] = {"value": ref["fps"], "unit": UNIT, "cores": ref["cores"], "kind": "reference",
+                                    "build": "the reference's unmodified sources, -O3, against the scalar Eigen "
+                                             "shim (oracle/eigen_shim: no SIMD Eigen on the box)",
                                     "stage_ms": ref["stage_ms"],
                                     "sample": f"{cfg.name} frames 1..{ref['frames']} ({ref['seconds']:.1f} s), "
                                               "reference pipeline (oracle/_ref) via process_frame"}
@@ -558,10 +639,31 @@ def ncu_traffic(config):
     return {"bytes": b, "source": f"profiles/{ent[0]} [{ent[1]}] {ent[2]}: dram read + write per launch"}
 
 
+def dry_run(args, dist: Dist):
+    """Ranks up, process group formed, config resolved; nothing on the GPU."""
+    info = {"rank": dist.rank, "local_rank": dist.local_rank, "world": dist.world, "pid": os.getpid()}
+    ranks = [info]
+    if dist.pg:
+        ranks = [None] * dist.world
+        dist.pg.all_gather_object(ranks, info)
+    if dist.rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": args.gpus, "world": dist.world, "mode": args.mode,
+                          "config": args.config, "impl": args.impl, "ranks": ranks}))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     dist = Dist(args.gpus)
+    resolve(args, dist.world)
+    if dist.world > 1 and args.mode == "shard":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines in the log (rank check)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     try:
+        if args.dry_run:
+            dry_run(args, dist)
+            return
         if args.impl == "reference":
             run_reference_arm(args, dist)
         else:

@@ -1,7 +1,7 @@
 """Benchmark configurations and the synthetic scene they are quoted on.
 
-BASELINE.json names five configurations; this module pins the three that run
-on one GPU (C1, C2, C3) plus small parity cases, following SURVEY.md §8(d):
+BASELINE.json names five configurations; this module pins all five (C1-C4
+on one GPU, C5 sharded across GPUs) plus small parity cases, following SURVEY.md §8(d):
 
 * camera: the paper's depth intrinsics, 640x480, fx 573.71, fy 574.394,
   cx 346.471, cy 249.031 (reference PAPER.md:798-800); 1280x960 doubles the
@@ -270,6 +270,12 @@ CONFIGS = {
     # exhaust the 2^18-block pool after ~30 m and drop allocations).
     "C4": BenchConfig("C4", 640, 480, 0.005, frames=1000, use_swapping=True, swap_buffer_blocks=512,
                       scene="corridor"),
+    # configs[4]: the large-scale scene spatially sharded by block hash
+    # across 2/4/8 GPUs (bench.py --gpus N default): the corridor walk,
+    # tracked, each shard with the reference's default pool of 2^18 blocks
+    # (512 MiB of VoxelS) -- G shards hold G x 2^18 blocks, the capacity one
+    # default volume runs out of after ~30 m of corridor (C4 swaps instead).
+    "C5": BenchConfig("C5", 640, 480, 0.005, frames=1000, scene="corridor"),
     # the other trackers on the C1 / C2 frames:
     # icp_ren = ICP on the coarser levels + Ren SDF refinement at full
     # resolution; color = photometric tracking against the colour surface list

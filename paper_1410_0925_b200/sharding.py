@@ -95,13 +95,19 @@ class LocalShardGroup:
             s.close()
 
 
-def attach_nccl(pipe: Pipeline, rank: int, world: int, dist) -> None:
-    """One process per GPU: share rank 0's NCCL id over `dist` and attach."""
+def share_nccl_id(rank: int, dist) -> bytes:
+    """Rank 0 creates the NCCL unique id (vf_shard_nccl_unique_id, no GPU
+    needed) and every rank receives it over the host process group."""
     L = _abi.load()
     buf = (C.c_uint8 * 128)()
     if rank == 0:
         _abi.check("vf_shard_nccl_unique_id", L.vf_shard_nccl_unique_id(buf))
     obj = [bytes(buf)]
     dist.broadcast_object_list(obj, src=0)
-    idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
-    _abi.check("vf_shard_attach_nccl", L.vf_shard_attach_nccl(pipe.handle, idb, world, rank))
+    return obj[0]
+
+
+def attach_nccl(pipe: Pipeline, rank: int, world: int, dist) -> None:
+    """One process per GPU: share rank 0's NCCL id over `dist` and attach."""
+    idb = (C.c_uint8 * 128).from_buffer_copy(share_nccl_id(rank, dist))
+    _abi.check("vf_shard_attach_nccl", _abi.load().vf_shard_attach_nccl(pipe.handle, idb, world, rank))

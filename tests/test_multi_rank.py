@@ -100,3 +100,32 @@ def test_nearest_depth_composite_world2():
     want_p[none] = 0
     want_n[none] = 0
     assert np.array_equal(o0p, want_p) and np.array_equal(o0n, want_n)
+
+
+def _nccl_id_worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from paper_1410_0925_b200.sharding import share_nccl_id
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = share_nccl_id(rank, dist)
+    dist.destroy_process_group()
+    q.put((rank, uid))
+
+
+def test_product_nccl_id_shared_world2():
+    """The product's communicator bootstrap (sharding.attach_nccl up to the
+    device attach): rank 0's ncclGetUniqueId, through the library, reaches
+    every rank of a real 2-process group byte for byte."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in procs), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][1] == res[1][1] and len(res[0][1]) == 128 and any(res[0][1])
