@@ -35,7 +35,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define VF_ABI_VERSION 2
+#define VF_ABI_VERSION 3
 
 enum vf_status {
   VF_OK = 0,
@@ -93,7 +93,17 @@ typedef struct vf_settings {
   int tracker_type; /* vf_tracker_type */
   float ren_sigma;
   int skip_points;
+  /* TSDF integration arithmetic (no reference counterpart):
+   *   VF_INTEGRATION_EXACT (0, default): the reference's FP32 operation
+   *     sequence, bit-exact (integration.hpp:40-148);
+   *   VF_INTEGRATION_FAST (1): the same voxels, pixels and update rule with
+   *     FMA-contracted camera transform, approximate reciprocals and an FMA
+   *     blend; parity bar: SDF within 1 LSB of int16 and weight exact on
+   *     >= 99.9 % of voxels (SURVEY §8(c) TSDF tolerance). VoxelS only. */
+  int integration_mode;
 } vf_settings;
+
+enum vf_integration_mode { VF_INTEGRATION_EXACT = 0, VF_INTEGRATION_FAST = 1 };
 
 enum vf_tracker_type { /* TrackerType (tracking_state.hpp:10) */
   VF_TRACKER_ICP = 0,

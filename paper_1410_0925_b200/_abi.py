@@ -28,7 +28,7 @@ STATUS_NAMES = {
 }
 
 # Every symbol include/voxfuse_b200.h declares (checked by tests/test_abi.py).
-ABI_VERSION = 2  # VF_ABI_VERSION in include/voxfuse_b200.h
+ABI_VERSION = 3  # VF_ABI_VERSION in include/voxfuse_b200.h
 
 EXPORTS = [
     "vf_abi_version", "vf_struct_size", "vf_default_settings", "vf_create", "vf_destroy", "vf_last_error",
@@ -86,6 +86,7 @@ class VfSettings(C.Structure):
         ("tracker_type", C.c_int),
         ("ren_sigma", C.c_float),
         ("skip_points", C.c_int),
+        ("integration_mode", C.c_int),
     ]
 
 

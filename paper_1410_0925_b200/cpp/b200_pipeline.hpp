@@ -111,6 +111,7 @@ inline vf_settings to_vf_settings(const voxfuse::EngineSettings& s) {
                                                             : VF_TRACKER_ICP;
   c.ren_sigma = s.tracker.ren_sigma;
   c.skip_points = s.tracker.skip_points ? 1 : 0;
+  c.integration_mode = VF_INTEGRATION_EXACT;  // the drop-in keeps the reference's arithmetic
   return c;
 }
 

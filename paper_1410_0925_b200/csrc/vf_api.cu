@@ -284,7 +284,16 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
 }
 
 void stage_mark(vf_ctx* c, int slot) {
-  if (c->profiling || c->stage_timing) cudaEventRecord(c->ev[slot], c->stream);
+  if (!(c->profiling || c->stage_timing)) return;
+  // Under stream capture a plain record only marks a dependency; External
+  // makes it a real event-record node of the frame graph (outside a capture
+  // the flag is refused, so the plain record is used there).
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(c->ev[slot], c->stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(c->ev[slot], c->stream);
 }
 
 // VF_DEBUG_SYNC=1: synchronise and check after every launch (debugging only).
@@ -525,7 +534,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     VF_CUDA(c, cudaEventRecord(c->ev_join, c->side));
   }
   const bool color = c->vsize == 8;
-  launch_integrate(c->num_sms * int_grid_mult(), st, color, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+  launch_integrate(c->num_sms * int_grid_mult(), st, color, s.integration_mode == VF_INTEGRATION_FAST, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
                    with_rgb ? c->rgb : nullptr, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
                    s.stop_integrating_at_max);
   VF_LAUNCHED(c, "k_integrate");
@@ -984,7 +993,9 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     return VF_ERR_CUDA;
   }
   c->vsize = s->voxel_type == VF_VOXEL_S_RGB ? 8 : 4;
-  if (s->tracker_type < VF_TRACKER_ICP || s->tracker_type > VF_TRACKER_ICP_REN ||
+  if (s->integration_mode < VF_INTEGRATION_EXACT || s->integration_mode > VF_INTEGRATION_FAST ||
+      (s->integration_mode == VF_INTEGRATION_FAST && c->vsize != 4) ||
+      s->tracker_type < VF_TRACKER_ICP || s->tracker_type > VF_TRACKER_ICP_REN ||
       (s->tracker_type == VF_TRACKER_COLOR && c->vsize != 8)) {
     // "colour tracker requires a voxel type with colour information" (pipeline_impl.hpp:55-57)
     free_all(c);
@@ -1634,7 +1645,7 @@ int vf_stage_integrate(vf_ctx* c, const float* depth_m, const uint8_t* rgb, cons
   if (with_rgb && upload(c, c->rgb, rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height, false)) return VF_ERR_CUDA;
   if (int rc = set_pose_dev(c, pose)) return rc;
   k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
-  launch_integrate(c->num_sms * int_grid_mult(), st, c->vsize == 8, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
+  launch_integrate(c->num_sms * int_grid_mult(), st, c->vsize == 8, s.integration_mode == VF_INTEGRATION_FAST, c->entries, c->visible_list, &c->dstate->ctr, c->voxels, c->depth,
                    with_rgb ? c->rgb : nullptr, &c->dstate->fp, s.voxel_size, s.mu, s.max_weight,
                    s.stop_integrating_at_max);
   VF_CUDA(c, cudaGetLastError());

@@ -93,7 +93,7 @@ __global__ void k_integrate_s(const HashEntry* entries, const int* visible_list,
                               const float* depth, const FrameParams* fp, float vs, float mu, int max_weight,
                               int stop_at_max);
 // Launches k_integrate_s / k_integrate_rgb with their dynamic shared memory (staging ring).
-void launch_integrate(int grid, cudaStream_t st, bool color, const HashEntry* entries, const int* visible_list,
+void launch_integrate(int grid, cudaStream_t st, bool color, bool fast, const HashEntry* entries, const int* visible_list,
                       const Counters* ctr, void* voxels, const float* depth, const uint8_t* rgb,
                       const FrameParams* fp, float vs, float mu, int max_weight, int stop_at_max);
 __global__ void k_integrate_rgb(const HashEntry* entries, const int* visible_list, const Counters* ctr, void* voxels,

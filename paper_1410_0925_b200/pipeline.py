@@ -108,6 +108,7 @@ class EngineSettings:
     tracker_type: int = 0  # TrackerType: 0 icp, 1 color, 2 icp_ren (tracking_state.hpp:10)
     ren_sigma: float = 10.0
     skip_points: bool = False
+    integration_mode: int = 0  # 0 exact (bit-exact), 1 fast (<= 1 LSB tolerance; VoxelS)
 
     def to_c(self) -> VfSettings:
         s = VfSettings()
