@@ -21,6 +21,9 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libvoxfuse_ref.so"
+# the same reference build with Eigen's halving reduction association
+# (eigen_shim VF_SHIM_HALVING; `make -C oracle ref_halving`)
+REF_HALVING_SO = HERE / "_ref_halving" / "libvoxfuse_ref.so"
 
 ENTRY_DTYPE = np.dtype(
     [("x", "<i2"), ("y", "<i2"), ("z", "<i2"), ("pad", "<i2"), ("offset", "<i4"), ("block_state", "<i4")]
@@ -239,6 +242,16 @@ def ref_lib() -> RefLib:
 
 def ref_available() -> bool:
     return REF_SO.exists()
+
+
+def ref_halving_lib() -> RefLib:
+    if "rh" not in _cache:
+        _cache["rh"] = RefLib(REF_HALVING_SO)
+    return _cache["rh"]
+
+
+def ref_halving_available() -> bool:
+    return REF_HALVING_SO.exists()
 
 
 class Volume:

@@ -42,14 +42,16 @@ def voxels_digest(v: np.ndarray, vsize: int) -> str:
     return sha(v.reshape(-1, vsize)[:, : vsize - 1])
 
 
-def run(lib, cfg, n, tracking, rgb=False):
-    poses = trajectory(n)
+def run(lib, cfg, n, tracking, rgb=False, epilogues=True):
+    from paper_1410_0925_b200.scene import scene_for, trajectory_for
+    spheres, planes, far = scene_for(cfg)
+    poses = trajectory_for(cfg, n)
     vol = vf_py.Volume(lib, cfg, tracking)
     vsize = 8 if cfg.voxel_type == 2 else 4
     out = []
     for i in range(n):
-        d = vf_py.render_depth(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
-        c = vf_py.render_rgb(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES) if rgb else None
+        d = vf_py.render_depth(lib, cfg, poses[i], spheres, planes, 0.05, far)
+        c = vf_py.render_rgb(lib, cfg, poses[i], spheres, planes, 0.05, far) if rgb else None
         st = vol.process(d, c, None if tracking else poses[i])
         pts, nrm = vol.maps()
         out.append({
@@ -70,6 +72,11 @@ def run(lib, cfg, n, tracking, rgb=False):
             "volume_digest": str(vol.digest()) if tracking else None,
             "ranges_sha": sha(vol.ranges()) if not tracking else None,
         })
+        if cfg.use_swapping:
+            out[-1].update({"swapped_in": int(st.swapped_in), "swapped_out": int(st.swapped_out),
+                            "states_sha": sha(vol.swap_states()), "store_count": int(vol.store_count())})
+        if not epilogues:
+            continue
         # raycast epilogues (raycast.hpp:441-509, pipeline_impl.hpp:125-137, 218-221)
         sp, sc = vol.surface_points()
         out[-1]["surface_count"] = int(len(sp))
@@ -131,6 +138,11 @@ def main():
         "T320_known_pose": run(lib, CONFIGS["T320"].with_(tracking=False), 3, tracking=False),
         "C2_known_pose_rgb": run(lib, CONFIGS["C2"], 2, tracking=False, rgb=True),
     }
+    # the large configurations (BASELINE configs[2], configs[3]): C3 frame 0
+    # (1280x960, 2 mm, 2^20 blocks) and the first tracked corridor frames of
+    # C4 with host swapping
+    gold["C3_tracking"] = run(lib, CONFIGS["C3"], 1, tracking=True, epilogues=False)
+    gold["C4_corridor_tracking"] = run(lib, CONFIGS["C4"], 3, tracking=True, epilogues=False)
     for name in SWAP_CASES:
         gold[name] = run_swap(lib, name)
     cfg = CONFIGS["C1"]

@@ -1,0 +1,138 @@
+"""Long tracked sequences on every BASELINE configuration that tracks, against
+the REFERENCE itself (oracle/_ref: its own sources, one worker thread so the
+allocation winner is defined; the restatement when _ref is absent).
+
+* C1 (configs[0]): the whole 100-frame box-room sequence, including the
+  frames the bench times;
+* C3 (configs[2]): 10 tracked frames at 1280x960, 2 mm, 2^20 blocks;
+* C4 (configs[3]): 50 tracked frames of the corridor walk with host swapping.
+
+Bars: per frame, the same tracking_ok and poses within
+1e-4 rad / 0.1 mm; over the sequence, the accumulated drift from the
+ground-truth trajectory within 0.1 mm of the reference's own drift; at the
+end, allocated block sets >= 99.9 % identical, SDF within 64 LSB on >= 99 %
+of common voxels and weights within 1 on >= 99.9 %, raycast hit masks
+>= 99.9 % identical.  Tracked poses agree to the ICP's convergence tolerance
+only, which is what these statistics quantify; the measured
+numbers are printed and, with VF_PARITY_OUT=<file>, written as JSON.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import vf_py
+from helpers import allocated_blocks, centre_dist, rot_angle
+from paper_1410_0925_b200 import make_pipeline, settings_from_config
+from paper_1410_0925_b200.scene import CONFIGS, scene_for, trajectory_for
+
+pytestmark = pytest.mark.gpu
+
+ROT_BAR, CENTRE_BAR = 1e-4, 1e-4
+RESULTS = {}
+
+
+@pytest.fixture(scope="module")
+def checker(olib):
+    if vf_py.ref_available():
+        lib = vf_py.ref_lib()
+        lib.lib.vfr_set_threads(1)
+        return "reference (oracle/_ref, 1 worker)", lib
+    return "oracle (C restatement)", olib
+
+
+def _all_entries(entries):
+    """positions of every entry holding a block (resident or swapped out)"""
+    e = entries[entries["block_state"] >= -1]
+    return set(zip(e["x"].tolist(), e["y"].tolist(), e["z"].tolist()))
+
+
+def _run(checker, name, n):
+    label, lib = checker
+    cfg = CONFIGS[name]
+    spheres, planes, far = scene_for(cfg)
+    poses = trajectory_for(cfg, n)
+    s, c = settings_from_config(cfg)
+    p = make_pipeline(s, c)
+    r = vf_py.Volume(lib, cfg, tracking=True)
+    rows = []
+    for i in range(n):
+        d = vf_py.render_depth(lib, cfg, poses[i], spheres, planes, 0.05, far)
+        sg, sr = p.process_frame(None, d), r.process(d)
+        pg, pr = p.pose(), r.pose()
+        rows.append({
+            "frame": i, "ok": [bool(sg.tracking_ok), bool(sr.tracking_ok)],
+            "iters": [int(sg.tracking_iterations), int(sr.tracking_iterations)],
+            "rot": rot_angle(pg, pr), "centre": centre_dist(pg, pr),
+            "drift_gpu": centre_dist(pg, poses[i]), "drift_ref": centre_dist(pr, poses[i]),
+            "visible": [int(sg.visible_blocks), int(sr.visible_blocks)],
+            "swap": [[int(sg.swapped_in), int(sg.swapped_out)], [int(sr.swapped_in), int(sr.swapped_out)]],
+        })
+    eg, er = p.entries(), r.entries()
+    sets = (_all_entries(eg), _all_entries(er))
+    bg, br = allocated_blocks(eg, p.voxels(), 4), allocated_blocks(er, r.voxels(), 4)
+    keys = sorted(set(bg) & set(br))
+    sdf_g = np.stack([bg[k][:, :2].copy().view(np.int16)[:, 0] for k in keys]).astype(np.int64)
+    sdf_r = np.stack([br[k][:, :2].copy().view(np.int16)[:, 0] for k in keys]).astype(np.int64)
+    w_g = np.stack([bg[k][:, 2] for k in keys]).astype(np.int64)
+    w_r = np.stack([br[k][:, 2] for k in keys]).astype(np.int64)
+    dsdf, dw = np.abs(sdf_g - sdf_r), np.abs(w_g - w_r)
+    hit_g = p.tracking_state()[0][..., 3] > 0
+    hit_r = r.maps()[0][..., 3] > 0
+    p.close()
+    r.close()
+    common = len(sets[0] & sets[1])
+    out = {
+        "checker": label, "frames": n,
+        "tracking_ok_equal": all(x["ok"][0] == x["ok"][1] for x in rows),
+        "iterations_equal_frames": sum(x["iters"][0] == x["iters"][1] for x in rows),
+        "max_rot_rad": max(x["rot"] for x in rows), "max_centre_m": max(x["centre"] for x in rows),
+        "max_drift_delta_m": max(abs(x["drift_gpu"] - x["drift_ref"]) for x in rows),
+        "final_drift_m": [rows[-1]["drift_gpu"], rows[-1]["drift_ref"]],
+        "blocks": [len(sets[0]), len(sets[1])], "blocks_common_frac": common / max(len(sets[0]), len(sets[1])),
+        "voxels_compared": int(dsdf.size),
+        "sdf_exact_frac": float(np.mean(dsdf == 0)), "sdf_le1_frac": float(np.mean(dsdf <= 1)),
+        "sdf_le64_frac": float(np.mean(dsdf <= 64)), "sdf_max": int(dsdf.max()),
+        "weight_exact_frac": float(np.mean(dw == 0)), "weight_le1_frac": float(np.mean(dw <= 1)),
+        "hit_agreement": float(np.mean(hit_g == hit_r)),
+        "swap_totals": [[sum(x["swap"][0][0] for x in rows), sum(x["swap"][0][1] for x in rows)],
+                        [sum(x["swap"][1][0] for x in rows), sum(x["swap"][1][1] for x in rows)]],
+        "per_frame": rows,
+    }
+    RESULTS[name] = out
+    path = os.environ.get("VF_PARITY_OUT")
+    if path:
+        with open(path, "w") as f:
+            json.dump(RESULTS, f, indent=1)
+    print(f"{name}: " + json.dumps({k: v for k, v in out.items() if k != "per_frame"}))
+    return out
+
+
+def _assert_bars(out):
+    assert out["tracking_ok_equal"]
+    assert out["max_rot_rad"] <= ROT_BAR and out["max_centre_m"] <= CENTRE_BAR, out
+    assert out["max_drift_delta_m"] <= 1e-4, out
+    assert out["blocks_common_frac"] >= 0.999
+    assert out["sdf_le64_frac"] >= 0.99 and out["weight_le1_frac"] >= 0.999
+    assert out["hit_agreement"] >= 0.999
+
+
+def test_c1_full_sequence_vs_reference(checker):
+    """BASELINE configs[0]: all 100 frames (the bench times frames 5..104 of
+    the same trajectory)."""
+    _assert_bars(_run(checker, "C1", 100))
+
+
+def test_c3_tracked_vs_reference(checker):
+    _assert_bars(_run(checker, "C3", 10))
+
+
+def test_c4_corridor_with_swapping_vs_reference(checker):
+    out = _run(checker, "C4", 50)
+    _assert_bars(out)
+    # the swap engine moves the same blocks (counts within 1 % over the walk)
+    (gi, go), (ri, ro) = out["swap_totals"]
+    assert abs(go - ro) <= 0.01 * max(ro, 1) + 2 and abs(gi - ri) <= 0.01 * max(ri, 1) + 2, out["swap_totals"]

@@ -48,15 +48,17 @@ def test_sdf_to_float_identity():
 
 
 def _check_run(lib, cfg, frames_gold, tracking, rgb=False):
-    poses = trajectory(len(frames_gold))
+    from paper_1410_0925_b200.scene import scene_for, trajectory_for
+    spheres, planes, far = scene_for(cfg)
+    poses = trajectory_for(cfg, len(frames_gold))
     vol = vf_py.Volume(lib, cfg, tracking)
     vsize = 8 if cfg.voxel_type == 2 else 4
     for i, g in enumerate(frames_gold):
-        d = vf_py.render_depth(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        d = vf_py.render_depth(lib, cfg, poses[i], spheres, planes, 0.05, far)
         assert sha(d) == g["depth_sha"], f"frame {i}: synthetic depth differs"
         c = None
         if rgb:
-            c = vf_py.render_rgb(lib, cfg, poses[i], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+            c = vf_py.render_rgb(lib, cfg, poses[i], spheres, planes, 0.05, far)
             assert sha(c) == g["rgb_sha"]
         st = vol.process(d, c, None if tracking else poses[i])
         assert int(st.tracking_ok) == g["tracking_ok"]
@@ -76,6 +78,9 @@ def _check_run(lib, cfg, frames_gold, tracking, rgb=False):
             assert str(vol.digest()) == g["volume_digest"], f"frame {i}: FNV volume digest"
         if g.get("ranges_sha") is not None:
             assert sha(vol.ranges()) == g["ranges_sha"]
+        if "swapped_in" in g:  # swap engine (swap.hpp)
+            assert (int(st.swapped_in), int(st.swapped_out)) == (g["swapped_in"], g["swapped_out"]), f"frame {i}"
+            assert sha(vol.swap_states()) == g["states_sha"] and vol.store_count() == g["store_count"]
         if "surface_points_sha" in g:  # raycast epilogues (raycast.hpp:441-509)
             sp, sc = vol.surface_points()
             assert len(sp) == g["surface_count"], f"frame {i}: surface point count"
@@ -91,6 +96,19 @@ def test_oracle_golden_tracking_T160(olib):
     """4 tracked frames: poses bit-identical to the reference's, entries,
     voxels, maps, visible set and the reference's volume_digest."""
     _check_run(olib, CONFIGS["T160"], GOLD["T160_tracking"], tracking=True)
+
+
+def test_oracle_golden_tracking_C3(olib):
+    """BASELINE configs[2] (1280x960, 2 mm, 2^20 blocks): frame 0 pinned to
+    the reference: entries, voxels, maps, visible set."""
+    _check_run(olib, CONFIGS["C3"], GOLD["C3_tracking"], tracking=True)
+
+
+def test_oracle_golden_tracking_C4_corridor(olib):
+    """BASELINE configs[3]: the first tracked corridor frames with host
+    swapping on, pinned to the reference (poses, entries, voxels, maps, swap
+    states and store)."""
+    _check_run(olib, CONFIGS["C4"], GOLD["C4_corridor_tracking"], tracking=True)
 
 
 def test_oracle_golden_known_pose_T320(olib):
@@ -203,3 +221,32 @@ def test_disparity_to_depth_matches_reference(olib, rlib):
         r = vf_py.disparity_to_depth(rlib, d, a, b, fx, mx)
         assert np.array_equal(o.view(np.uint32), r.view(np.uint32))
         assert (o > 0).any() and (o == 0).any()
+
+
+def test_eigen_association_bound_known_pose():
+    """The shim-built reference in Eigen's halving association
+    (oracle/_ref_halving) against the left-to-right build on 4 known-pose C1
+    frames: the delta a stock-Eigen reference could show against the GPU
+    path, which is bit-exact to the left-to-right build (test_gpu_parity.py).
+    Stays inside the §8(c) tolerances (tests/test_gpu_eigen_assoc.py checks
+    the GPU against the halving build directly)."""
+    if not (vf_py.ref_available() and vf_py.ref_halving_available()):
+        pytest.skip("oracle/_ref and oracle/_ref_halving need /root/reference at build time")
+    from assoc_stats import compare
+    from helpers import frames
+    ra, rh = vf_py.ref_lib(), vf_py.ref_halving_lib()
+    ra.lib.vfr_set_threads(1)
+    rh.lib.vfr_set_threads(1)
+    cfg = CONFIGS["C1"].with_(tracking=False)
+    va, vh = vf_py.Volume(ra, cfg, False), vf_py.Volume(rh, cfg, False)
+    for pose, d, _ in frames(ra, cfg, 4):
+        va.process(d, None, pose)
+        vh.process(d, None, pose)
+    out = compare(va.entries(), va.voxels(), vh.entries(), vh.voxels(), va.maps(), vh.maps(), cfg.voxel_size)
+    va.close()
+    vh.close()
+    print(out)
+    assert out["blocks_common_frac"] == 1.0
+    assert out["sdf_le1_frac"] >= 0.999 and out["weight_exact_frac"] >= 0.999
+    assert out["hit_agreement"] >= 0.999 and out["point_within_half_voxel_frac"] >= 0.999
+    assert out["sdf_exact_frac"] < 1.0 or out["maps_bit_exact_frac"] < 1.0  # the two builds do differ
