@@ -408,13 +408,16 @@ def run_ours(args, dist: Dist):
                 swaps.append((st.swapped_in, st.swapped_out, st.swap_bytes_in + st.swap_bytes_out,
                               st.allocation_dropped))
                 modified.append(L.vf_last_modified_voxels(hctx))
+        counters = None
         if collect_stages:
             stage, nprof = p.stage_times()
             stage = stage / max(nprof, 1)
+            counters = p.raycast_counters()  # last frame's raycast re-run with counters (untimed)
         launches = sum(p.kernel_launches_per_frame(cfg.tracking and i > 0) for i in range(args.warmup, n_frames))
         if not cfg.tracking:
             launches += n_frames - args.warmup  # k_set_pose per known-pose frame
         p.close()
+        run_device.counters = counters
         return np.array(ms_frames), np.array(vis_blocks), np.array(modified), stage, launches
 
     # --- timed pass (graphs on) ---
@@ -567,6 +570,7 @@ def run_ours(args, dist: Dist):
         # per-stage throughput in the units of SURVEY.md §8(d)
         "stage_throughput": {
             "raycast_rays_per_s": npix / (stages["raycast"] * 1e-3) if stages["raycast"] > 0 else None,
+            **raycast_rates(run_device.counters, stages["raycast"]),
             "integration_voxel_visits_per_s": nvis * 512 / (integ_ms * 1e-3) if integ_ms > 0 else None,
             "allocation_pixels_per_s": npix / (stages["allocation"] * 1e-3) if stages["allocation"] > 0 else None,
         },
@@ -601,6 +605,19 @@ def run_ours(args, dist: Dist):
                                               "reference pipeline (oracle/_ref) via process_frame"}
     if dist.rank == 0:
         print(json.dumps(line))
+
+
+def raycast_rates(cnt, ray_ms: float) -> dict:
+    """SURVEY.md §8(d) K3 units from the counting re-run of the last frame's
+    raycast (vf_raycast_counters): hash-table probes (our block-cache misses),
+    voxel reads (each a hash probe in the reference's sampler), rays, hits."""
+    if not cnt or ray_ms <= 0:
+        return {}
+    t = ray_ms * 1e-3
+    return {"raycast_table_probes_per_frame": cnt["table_probes"], "raycast_voxel_reads_per_frame": cnt["voxel_reads"],
+            "raycast_rays_marched_per_frame": cnt["rays"], "raycast_hits_per_frame": cnt["hits"],
+            "raycast_table_probes_per_s": cnt["table_probes"] / t, "raycast_voxel_reads_per_s": cnt["voxel_reads"] / t,
+            "raycast_probe_cache_hit_rate": 1.0 - cnt["table_probes"] / max(cnt["voxel_reads"], 1)}
 
 
 def roofline_large(args, device: int, hbm_peak: float, peak_src: str) -> dict:

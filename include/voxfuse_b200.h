@@ -327,6 +327,12 @@ int vf_stage_times(vf_ctx* ctx, double* ms_out /* 8 */, long* frames);
  * ms_swapping is the wait for it).  The streaming pair returns ms_total only.
  * Off by default in the C ABI; the IPipeline adapter turns it on. */
 int vf_set_stage_timing(vf_ctx* ctx, int enabled);
+/* Measurement only (not on the frame path): re-runs the last frame's raycast
+ * (render_maps, raycast.hpp:415-435) with counters -- identical maps -- and
+ * returns {hash-table probes (block-cache misses), voxel reads (each one
+ * hash probe in the reference's HashSdfSampler::read, raycast.hpp:73-76),
+ * rays marched, rays hit}. */
+int vf_raycast_counters(vf_ctx* ctx, unsigned long long* out /* 4 */);
 int vf_kernel_launches_per_frame(vf_ctx* ctx, int tracking_frame);
 /* Bytes of the per-frame stats readback (the D2H of vf_process_frame). */
 long vf_readback_bytes(const vf_ctx* ctx);

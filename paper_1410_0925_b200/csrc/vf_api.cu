@@ -160,7 +160,8 @@ struct vf_ctx {
   cudaEvent_t ev[kNumEvents] = {};
   cudaEvent_t ev_frame0 = nullptr, ev_frame1 = nullptr;
   bool profiling = false;
-  bool stage_timing = false;  // per-frame FrameStats::ms_* (event nodes in the frame graph)
+  bool stage_timing = false;
+  long l2_persist_bytes = 0;  // hash-table bytes under the persisting access-policy window  // per-frame FrameStats::ms_* (event nodes in the frame graph)
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long profiled_frames = 0;
   int launches_last = 0;
@@ -444,6 +445,42 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
                                                              c->din, s.voxel_size, s.mu, c->points, c->normals);
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
+}
+
+// The hash table (34 MiB at the default 2^20 x 2 + 2^17 entries) is the
+// object every stage probes (allocation's DDA cells, the raycast's block
+// lookups, visibility, the swap scan).  An access-policy window on the
+// context's streams marks it persisting in L2, so the
+// voxel and map traffic of a frame streams past it instead of evicting it.
+// VF_L2_PERSIST=0 turns it off (measurement runs).
+void persist_hash_table(vf_ctx* c) {
+  static const bool on = [] {
+    const char* e = std::getenv("VF_L2_PERSIST");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on) return;
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+  if (max_persist <= 0 || max_window <= 0) return;
+  const size_t table = sizeof(HashEntry) * (size_t)c->entry_count;
+  size_t carve = 0;
+  cudaDeviceGetLimit(&carve, cudaLimitPersistingL2CacheSize);
+  const size_t want = std::min(table, (size_t)max_persist);
+  if (carve < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) carve = want;
+  if (carve == 0) {
+    cudaGetLastError();
+    return;
+  }
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = c->entries;
+  v.accessPolicyWindow.num_bytes = std::min(table, (size_t)max_window);
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)carve / (float)v.accessPolicyWindow.num_bytes);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  for (cudaStream_t st : {c->stream, c->side}) cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
+  c->l2_persist_bytes = (long)std::min(carve, (size_t)v.accessPolicyWindow.num_bytes);
 }
 
 // k_mark's grid: one thread per pixel, 32 x 8 pixel tiles.
@@ -1195,6 +1232,7 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaEventCreate(&c->ev_frame0);
   cudaEventCreate(&c->ev_frame1);
+  persist_hash_table(c);
   if ((rc = reset_volume(c))) {
     free_all(c);
     delete c;
@@ -1844,6 +1882,24 @@ int vf_set_profiling(vf_ctx* c, int enabled) {
   c->profiling = enabled != 0;
   for (double& m : c->stage_ms) m = 0;
   c->profiled_frames = 0;
+  return VF_OK;
+}
+int vf_raycast_counters(vf_ctx* c, unsigned long long* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  if (!c->maps_valid) {
+    c->err = "vf_raycast_counters: no frame processed yet";
+    return VF_ERR_STATE;
+  }
+  unsigned long long* d = nullptr;
+  VF_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&d), 4 * sizeof(unsigned long long), c->stream));
+  VF_CUDA(c, cudaMemsetAsync(d, 0, 4 * sizeof(unsigned long long), c->stream));
+  k_raycast_count<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, c->stream>>>(
+      hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels), c->vsize / 4, c->ranges, &c->dstate->fp, c->din,
+      c->s.voxel_size, c->s.mu, c->points, c->normals, d);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaMemcpyAsync(out, d, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  VF_CUDA(c, cudaFreeAsync(d, c->stream));
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
   return VF_OK;
 }
 int vf_set_stage_timing(vf_ctx* c, int enabled) {

@@ -104,6 +104,9 @@ __global__ void k_ranges(const HashEntry* entries, const int* visible_list, cons
                          int frag_w);
 __global__ void k_raycast(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
                           IntrD in, float vs, float mu, float4* points, float4* normals);
+__global__ void k_raycast_count(HashView hv, const uint32_t* vox, int vstride, const float2* ranges,
+                                const FrameParams* fp, IntrD in, float vs, float mu, float4* points, float4* normals,
+                                unsigned long long* counters);
 __global__ void k_pyramid(const float* depth0, int w0, int h0, int levels, float* out);
 __global__ void k_icp(IcpArgs a);
 __global__ void k_icp_cluster(IcpArgs a);

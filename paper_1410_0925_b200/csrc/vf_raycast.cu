@@ -96,11 +96,21 @@ __device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { retu
 // 16-byte lookups are conflict-free.  The way is the parity of the block
 // coordinates, so the 2x2x2 blocks a trilinear stencil can straddle never
 // evict each other.
-template <int kStride>  // 32-bit words per voxel: 1 (VoxelS) or 2 (VoxelSRgb)
-struct Sampler {
+// kCount: the measurement build (k_raycast_count) also counts table probes
+// (cache misses) and voxel reads (each a hash probe in the reference).
+template <bool kCount>
+struct SamplerCounts {  // empty base in the frame-path build (no size, no stack)
+};
+template <>
+struct SamplerCounts<true> {
+  unsigned n_probe = 0, n_read = 0;
+};
+template <int kStride, bool kCount = false>  // kStride: 32-bit words per voxel, 1 (VoxelS) or 2 (VoxelSRgb)
+struct Sampler : SamplerCounts<kCount> {
   HashView hv;
   const uint32_t* vox;  // first 4 bytes of each voxel: sdf (lo 16), w_depth (byte 2)
   int4* cache;          // this thread's column of the shared cache: (block, first word of the block or -1)
+  __device__ Sampler(const HashView& h, const uint32_t* v, int4* c) : hv(h), vox(v), cache(c) {}
 
   __device__ __forceinline__ void init() {
 #pragma unroll
@@ -109,7 +119,9 @@ struct Sampler {
   __device__ __forceinline__ int lookup(int x, int y, int z) {
     const int w = (x & 1) | ((y & 1) << 1) | ((z & 1) << 2);
     const int4 c = cache[w * kRayThreads];
+    if constexpr (kCount) ++this->n_read;
     if (c.x == x && c.y == y && c.z == z) return c.w;
+    if constexpr (kCount) ++this->n_probe;
     const int slot = probe(hv, x, y, z);
     const int s = slot < 0 ? -1 : slot * (kBlockVolume * kStride);
     cache[w * kRayThreads] = make_int4(x, y, z, s);
@@ -254,11 +266,12 @@ __device__ __forceinline__ bool march(TSampler& smp, F3 start, F3 dir, float tot
 
 // K3b: render_maps (raycast.hpp:415-435).  128-thread CTAs cover half a
 // 16x16 fragment (16 x 8 pixels), so every CTA reads one range.
-template <int kStride>
+template <int kStride, bool kCount = false>
 __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t* __restrict__ vox,
                                              const float2* __restrict__ ranges, const FrameParams* __restrict__ fp,
                                              const IntrD& in, float vs, float mu, float4* __restrict__ points,
-                                             float4* __restrict__ normals, int4* s_cache) {
+                                             float4* __restrict__ normals, int4* s_cache,
+                                             unsigned long long* counters = nullptr) {
   const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
   // Each warp traces an 8 x 4 pixel patch of the CTA's 16 x 8 half fragment
   // (2 x 2 warps): neighbouring rays march similar lengths, so the warp
@@ -291,7 +304,7 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
   float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
   if (total > 0) {
     dir = F3{dir.x / total, dir.y / total, dir.z / total};
-    Sampler<kStride> smp{hv, vox, s_cache + threadIdx.x};
+    Sampler<kStride, kCount> smp{hv, vox, s_cache + threadIdx.x};
     smp.init();
     F3 hw;
     if (march(smp, start, dir, total, mu / vs, vs, hw)) {
@@ -300,6 +313,12 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
         out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
         out_n = make_float4(n.x, n.y, n.z, 1.0f);
       }
+    }
+    if constexpr (kCount) {
+      atomicAdd(counters + 0, (unsigned long long)smp.n_probe);
+      atomicAdd(counters + 1, (unsigned long long)smp.n_read);
+      atomicAdd(counters + 2, 1ull);
+      if (out_p.w != 0.0f) atomicAdd(counters + 3, 1ull);
     }
   }
   points[pix] = out_p;
@@ -315,6 +334,19 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     raycast_body<1>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
   else
     raycast_body<2>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
+}
+
+// Measurement twin of k_raycast (vf_raycast_counters, never on the frame
+// path): same maps, plus counters {table probes, voxel reads, rays, hits}.
+__global__ void __launch_bounds__(kRayThreads)
+    k_raycast_count(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
+                    const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
+                    float4* __restrict__ normals, unsigned long long* counters) {
+  __shared__ int4 s_cache[kCacheWays * kRayThreads];
+  if (vstride == 1)
+    raycast_body<1, true>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache, counters);
+  else
+    raycast_body<2, true>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache, counters);
 }
 
 }  // namespace vf

@@ -521,6 +521,12 @@ class Pipeline:
     def set_profiling(self, enabled: bool) -> None:
         self._chk("vf_set_profiling", self._L.vf_set_profiling(self._h, int(enabled)))
 
+    def raycast_counters(self) -> dict:
+        """Re-run the last raycast with counters (measurement only, same maps)."""
+        out = (C.c_ulonglong * 4)()
+        self._chk("vf_raycast_counters", self._L.vf_raycast_counters(self._h, out))
+        return {"table_probes": out[0], "voxel_reads": out[1], "rays": out[2], "hits": out[3]}
+
     def set_stage_timing(self, enabled: bool) -> None:
         """Fill FrameStats.ms_tracking .. ms_raycast on every blocking frame
         (pipeline.hpp:56-57) from event records inside the frame graph."""

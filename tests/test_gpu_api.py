@@ -199,3 +199,28 @@ def test_streaming_rgb_swapping_matches_process_frame(olib):
     assert sa.keys() == sb.keys() and all(np.array_equal(sa[k], sb[k]) for k in sa)
     a.close()
     b.close()
+
+
+def test_raycast_counters_rerun_is_identical():
+    """vf_raycast_counters re-runs the last raycast with counters: the maps
+    are unchanged and the counts are consistent (hits == valid map pixels,
+    every table probe is a voxel read that missed the block cache)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import vf_py
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, trajectory
+    s, c = settings_from_config(CONFIGS["C1"])
+    p = make_pipeline(s, c)
+    olib = vf_py.oracle_lib()
+    for pose in trajectory(3):
+        p.process_frame(None, vf_py.render_depth(olib, CONFIGS["C1"], pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES))
+    pts0, nrm0 = p.tracking_state()
+    cnt = p.raycast_counters()
+    pts1, nrm1 = p.tracking_state()
+    assert np.array_equal(pts0.view(np.uint32), pts1.view(np.uint32))
+    assert np.array_equal(nrm0.view(np.uint32), nrm1.view(np.uint32))
+    assert cnt["hits"] == int((pts1[..., 3] > 0).sum())
+    assert 0 < cnt["rays"] <= p.width * p.height
+    assert 0 < cnt["table_probes"] < cnt["voxel_reads"]
+    p.close()
