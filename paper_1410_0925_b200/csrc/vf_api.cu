@@ -449,14 +449,17 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
 
 // The hash table (34 MiB at the default 2^20 x 2 + 2^17 entries) is the
 // object every stage probes (allocation's DDA cells, the raycast's block
-// lookups, visibility, the swap scan).  An access-policy window on the
-// context's streams marks it persisting in L2, so the
-// voxel and map traffic of a frame streams past it instead of evicting it.
-// VF_L2_PERSIST=0 turns it off (measurement runs).
+// lookups, visibility, the swap scan).  VF_L2_PERSIST=1 puts an
+// access-policy window on the context's streams that marks it persisting in
+// L2.  Measured (B200, bench.py, L2 flushed between
+// frames): C1 0.204 -> 0.199 ms raycast, 0.042 -> 0.040 ms allocation but
+// 0.035 -> 0.037 ms integration (+0.5 % frames/s, within run-to-run noise);
+// C3's 68 MiB table carves half the L2 away from the voxel stream and the
+// fast integration kernel loses 17 %.  Off by default.
 void persist_hash_table(vf_ctx* c) {
   static const bool on = [] {
     const char* e = std::getenv("VF_L2_PERSIST");
-    return !e || std::atoi(e) != 0;
+    return e && std::atoi(e) != 0;
   }();
   if (!on) return;
   int max_persist = 0, max_window = 0;
