@@ -83,7 +83,9 @@ typedef struct vf_settings {
   int shard_halo; /* 1: also fuse surfaces within one block of this shard's territory */
   /* Host swapping (EngineSettings::use_swapping / swap_buffer_blocks,
    * pipeline.hpp:20-23; swap.hpp).  The host block store is pinned host
-   * memory mapped into the device (swap_host_blocks slots; 0 = 4 x block_count);
+   * memory mapped into the device, allocated in chunks of 4096 blocks as
+   * blocks leave, up to swap_host_blocks slots (0 = one per hash entry, the
+   * reference's bound, swap.hpp:42-56: it never fills);
    * swap_buffer_blocks <= 4096. */
   int use_swapping;
   int swap_buffer_blocks;
@@ -285,6 +287,13 @@ int vf_swap_store_read(vf_ctx* ctx, int entry, uint8_t* payload);
 /* Write every stored block to a VXBS file (make_file_block_store /
  * load_block_store_file format, block_store.hpp:14-53): 16-byte header then
  * (u32 entry index, payload) records, ascending entry order. */
+/* The entries swapped out since the last drain, in swap-out order (the order
+ * the reference's file-backed BlockStore writes its records, block_store.cpp:
+ * 96-115): up to cap of them into entries; returns the count.  Waits for the
+ * frames in flight.  *lost (optional) counts entries that fell out of the
+ * 65536-entry ring between drains.  The adapter drains after every frame
+ * and writes the VXBS records of swap_store_path as blocks leave. */
+long vf_swap_drain(vf_ctx* ctx, int* entries, long cap, long* lost);
 int vf_swap_save_store(vf_ctx* ctx, const char* path);
 /* Load a VXBS file into the host store (load_block_store_file): records for
  * entries that are swapped out in the current table become their host data. */

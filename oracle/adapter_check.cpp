@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "b200_pipeline.hpp"
@@ -24,6 +25,10 @@ extern "C" {
 // raycast, total; pipeline.hpp:56-57)
 static double g_last_ms[6];
 void vfa_last_stage_ms(double* out) { std::memcpy(out, g_last_ms, sizeof(g_last_ms)); }
+
+// EngineSettings::swap_store_path for the next vfa_run (empty: in-memory store)
+static std::string g_store_path;
+void vfa_set_store_path(const char* path) { g_store_path = path ? path : ""; }
 
 struct vfa_config {  // same layout as vfr_config (oracle/ref_driver.cpp)
   int voxel_type;
@@ -80,6 +85,7 @@ int vfa_run(const vfa_config* c, int engine, int n_frames, const float* depth, c
     s.tracker.ren_sigma = c->ren_sigma;
     s.use_swapping = c->use_swapping != 0;
     s.swap_buffer_blocks = c->swap_buffer_blocks;
+    s.swap_store_path = g_store_path;
     Calibration k;
     k.depth.fx = c->fx;
     k.depth.fy = c->fy;

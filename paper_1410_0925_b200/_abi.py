@@ -37,7 +37,7 @@ EXPORTS = [
     "vf_process_raw_frame", "vf_process_raw_frame_device", "vf_disparity_to_depth",
     "vf_set_pose", "vf_get_pose", "vf_frame_count", "vf_get_maps", "vf_set_maps", "vf_volume_digest",
     "vf_get_surface_points", "vf_stage_forward_project", "vf_render_image",
-    "vf_swap_states", "vf_swap_stored_count", "vf_swap_store_read", "vf_swap_save_store", "vf_swap_load_store",
+    "vf_swap_states", "vf_swap_stored_count", "vf_swap_store_read", "vf_swap_drain", "vf_swap_save_store", "vf_swap_load_store",
     "vf_entry_count", "vf_voxel_bytes", "vf_export_entries", "vf_export_voxels", "vf_export_free_stacks",
     "vf_import_state", "vf_export_visible_list", "vf_export_ranges",
     "vf_stage_allocate", "vf_stage_integrate", "vf_stage_raycast", "vf_stage_icp", "vf_icp_trace",
@@ -181,6 +181,7 @@ def load() -> C.CDLL:
         "vf_swap_stored_count": (C.c_long, [vp]),
         "vf_swap_store_read": (C.c_int, [vp, C.c_int, vp]),
         "vf_swap_save_store": (C.c_int, [vp, C.c_char_p]),
+        "vf_swap_drain": (C.c_long, [vp, ip, C.c_long, C.POINTER(C.c_long)]),
         "vf_swap_load_store": (C.c_int, [vp, C.c_char_p]),
         "vf_stage_forward_project": (C.c_int, [vp]),
         "vf_render_image": (C.c_int, [vp, C.c_int, vp]),

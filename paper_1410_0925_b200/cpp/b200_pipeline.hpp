@@ -25,7 +25,9 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
+#include "voxfuse/engine/block_store.hpp"
 #include "voxfuse/engine/pipeline.hpp"
 #include "voxfuse/engine/raycast.hpp"
 #include "voxfuse/engine/view.hpp"
@@ -133,13 +135,22 @@ class B200Pipeline final : public voxfuse::IPipeline {
     detail::check(rc, "vf_create", nullptr);
     // the reference fills FrameStats::ms_* on every frame (pipeline_impl.hpp:66-120)
     detail::check(vf_set_stage_timing(ctx_, 1), "vf_set_stage_timing", ctx_);
+    // swap_store_path (pipeline.hpp:24; pipeline_impl.hpp:43-51): the
+    // reference's own file-backed BlockStore, fed as blocks leave
+    if (settings_.use_swapping && !settings_.swap_store_path.empty()) {
+      const bool rgb = settings_.voxel_type == voxfuse::VoxelType::s_rgb;
+      const int payload = (rgb ? voxfuse::VoxelCodec<voxfuse::VoxelSRgb>::bytes
+                               : voxfuse::VoxelCodec<voxfuse::VoxelS>::bytes) * voxfuse::kBlockVolume;
+      const auto tag = static_cast<std::uint16_t>(rgb ? voxfuse::VoxelCodec<voxfuse::VoxelSRgb>::tag
+                                                      : voxfuse::VoxelCodec<voxfuse::VoxelS>::tag);
+      file_store_ = voxfuse::make_file_block_store(settings_.swap_store_path, static_cast<int>(vf_entry_count(ctx_)),
+                                                   payload, tag);
+      drained_.resize(1 << 16);
+      payload_.resize(static_cast<std::size_t>(payload));
+    }
   }
   ~B200Pipeline() override {
-    // swap_store_path (pipeline.hpp:23): the reference streams records into a
-    // VXBS file as blocks leave; the GPU store lives in pinned memory and is
-    // written to the same format when the pipeline is destroyed.
-    if (ctx_ && settings_.use_swapping && !settings_.swap_store_path.empty())
-      vf_swap_save_store(ctx_, settings_.swap_store_path.c_str());
+    file_store_.reset();
     if (ctx_) vf_destroy(ctx_);
   }
   B200Pipeline(const B200Pipeline&) = delete;
@@ -197,7 +208,24 @@ class B200Pipeline final : public voxfuse::IPipeline {
   int frames_in_flight() const { return vf_frames_in_flight(ctx_); }
 
  private:
+  // The blocks swapped out since the last frame, in swap-out order, into the
+  // reference's file store: a record appended on a slot's first write and
+  // rewritten in place after (block_store.cpp:96-115), one flush per frame
+  // as execute_swap_out does (swap.hpp:251).
+  void journal_swap_outs() {
+    if (!file_store_) return;
+    long lost = 0;
+    const long n = vf_swap_drain(ctx_, drained_.data(), static_cast<long>(drained_.size()), &lost);
+    detail::check(static_cast<int>(n < 0 ? n : 0), "vf_swap_drain", ctx_);
+    if (lost > 0) throw std::runtime_error("voxfuse_b200: swap journal overflowed between frames");
+    for (long i = 0; i < n; ++i)
+      if (vf_swap_store_read(ctx_, drained_[static_cast<std::size_t>(i)], payload_.data()) == 1)
+        file_store_->write(drained_[static_cast<std::size_t>(i)], payload_.data());
+    file_store_->flush();
+  }
+
   voxfuse::FrameStats finish_frame(const vf_frame_stats& st) {
+    journal_swap_outs();
     pose_ = detail::pose_from_array(st.pose);
     maps_stale_ = true;
     voxfuse::FrameStats fs;
@@ -302,6 +330,9 @@ class B200Pipeline final : public voxfuse::IPipeline {
   voxfuse::Calibration calib_;
   vf_ctx* ctx_ = nullptr;
   voxfuse::Pose pose_;
+  std::unique_ptr<voxfuse::BlockStore> file_store_;  // swap_store_path: the reference's VXBS file store
+  std::vector<int> drained_;
+  std::vector<std::uint8_t> payload_;
   voxfuse::Image2D<voxfuse::Vec3u8> last_rgb_;
   std::deque<voxfuse::Image2D<voxfuse::Vec3u8>> pending_rgb_;  // rgb of the frames in flight
   mutable voxfuse::TrackingState state_;

@@ -142,8 +142,12 @@ struct vf_ctx {
   // swap engine (vf_swap.cu): device arrays + the pinned, mapped host store
   bool swapping = false;
   SwapDev sw{};
-  uint32_t* host_pool = nullptr;  // host pointer of sw.host_pool
-  int host_cap = 0;
+  std::vector<uint32_t*> host_chunk_ptrs;  // host pointers of the pinned store chunks
+  std::vector<uint32_t*> host_dev_ptrs;    // their device-mapped aliases (sw.host_chunks)
+  int host_cap = 0;       // host-store slots allocated (whole chunks)
+  int host_max = 0;       // slots it may grow to: one per hash entry (the reference's bound) or swap_host_blocks
+  long host_top_lb = 0;   // lower bound on the device's free host slots (host_top) before the next frame
+  int journal_read = 0;   // swap-out journal position vf_swap_drain has reached
 
   // host state
   DevState* hstate = nullptr;  // pinned
@@ -685,6 +689,8 @@ int upload(vf_ctx* c, void* dst, const void* src, size_t n, bool src_device) {
   return VF_OK;
 }
 
+int ensure_host_store(vf_ctx* c);
+
 int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_inputs, vf_frame_stats* stats,
                  const uint16_t* disparity = nullptr, bool big_endian = false) {
   if (!c || (!depth && !disparity)) return VF_ERR_INVALID;
@@ -706,8 +712,10 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
   c->rgb_valid = with_rgb;
   const bool track = c->s.tracking && c->frame > 0 && c->maps_valid;
   const int frame_index = c->frame;
+  if (int rc = ensure_host_store(c)) return rc;
   if (stats) VF_CUDA(c, cudaEventRecord(c->ev_frame0, c->stream));
   if (int rc = run_frame(c, track, with_rgb)) return rc;
+  c->host_top_lb -= c->s.swap_buffer_blocks;  // worst case: B swap-outs, no swap-ins
   c->maps_valid = true;
   ++c->frame;
   if (c->profiling) {
@@ -722,6 +730,7 @@ int frame_common(vf_ctx* c, const float* depth, const uint8_t* rgb, bool device_
   if (stats) {
     VF_CUDA(c, cudaEventRecord(c->ev_frame1, c->stream));
     if (int rc = read_state(c)) return rc;
+    c->host_top_lb = c->hstate->swap.host_top;
     fill_stats(c, track, frame_index, stats);
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev_frame0, c->ev_frame1);
@@ -782,6 +791,7 @@ int submit_frame(vf_ctx* c, const float* depth, const uint8_t* rgb, const uint16
     return VF_ERR_STATE;
   }
   if (int rc = ensure_queue(c)) return rc;
+  if (int rc = ensure_host_store(c)) return rc;
   const int k = (c->q_head + c->q_count) % kMaxFramesInFlight;
   const bool with_rgb = rgb != nullptr && c->vsize == 8;
   const size_t dbytes = sizeof(float) * (size_t)c->npix, cbytes = 3 * (size_t)c->rgbin.width * c->rgbin.height;
@@ -812,6 +822,7 @@ int submit_frame(vf_ctx* c, const float* depth, const uint8_t* rgb, const uint16
   c->q_track[k] = track;
   VF_CUDA(c, cudaEventRecord(c->ev_q0[k], c->stream));
   if (int rc = run_frame(c, track, with_rgb)) return rc;
+  c->host_top_lb -= c->s.swap_buffer_blocks;
   c->maps_valid = true;
   ++c->frame;
   VF_CUDA(c, cudaEventRecord(c->ev_q1[k], c->stream));
@@ -858,11 +869,12 @@ void free_all(vf_ctx* c) {
                   c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax,
                   c->sw.state, c->sw.host_slot, c->sw.host_free, c->sw.in_cand, c->sw.out_cand,
                   c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host, c->disp, c->image_depth_scratch,
-                  c->ren_partials, c->cpyr, c->compact_scan};
+                  c->ren_partials, c->cpyr, c->compact_scan, c->sw.host_chunks, c->sw.journal};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
-  if (c->host_pool) cudaFreeHost(c->host_pool);
+  for (uint32_t* h : c->host_chunk_ptrs) cudaFreeHost(h);
+  c->host_chunk_ptrs.clear();
   if (c->hpose) cudaFreeHost(c->hpose);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -925,19 +937,75 @@ int reset_volume(vf_ctx* c) {
   return VF_OK;
 }
 
+// One more pinned chunk of the host store (its slots are pushed by
+// k_host_store_grow when the free stack is (re)built).
+int add_host_chunk(vf_ctx* c) {
+  if (c->host_cap + kHostChunk > c->host_max) return VF_ERR_OVERFLOW;
+  const size_t bytes = (size_t)kHostChunk * kBlockVolume * (size_t)c->vsize;
+  void* hp = nullptr;
+  void* dp = nullptr;
+  if (cudaHostAlloc(&hp, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostGetDevicePointer(&dp, hp, 0) != cudaSuccess) {
+    if (hp) cudaFreeHost(hp);
+    cudaGetLastError();
+    std::fprintf(stderr, "[voxfuse_b200] cannot allocate a %zu-byte pinned host-store chunk\n", bytes);
+    c->err = "pinned host-store chunk allocation failed";
+    return VF_ERR_CUDA;
+  }
+  c->host_chunk_ptrs.push_back(reinterpret_cast<uint32_t*>(hp));
+  c->host_dev_ptrs.push_back(reinterpret_cast<uint32_t*>(dp));
+  c->host_cap += kHostChunk;
+  return VF_OK;
+}
+
+// Grow the store by one chunk between frames: allocate, then push its slots
+// on the device free stack (stream-ordered before the next frame).
+int grow_host_store(vf_ctx* c) {
+  if (int rc = add_host_chunk(c)) return rc;
+  const int k = (int)c->host_chunk_ptrs.size() - 1;
+  k_host_store_grow<<<1, 256, 0, c->stream>>>(c->sw, k, c->host_dev_ptrs[(size_t)k]);
+  VF_CUDA(c, cudaGetLastError());
+  c->host_top_lb += kHostChunk;
+  return VF_OK;
+}
+
+// Before a frame is enqueued: a frame swaps out at most B blocks, so while
+// the lower bound on free host slots covers two frames nothing is needed;
+// otherwise read the device's count (waits for the frames in flight) and
+// grow until it does, up to one slot per hash entry.
+int ensure_host_store(vf_ctx* c) {
+  if (!c->swapping) return VF_OK;
+  const long need = 2L * c->s.swap_buffer_blocks;
+  if (c->host_top_lb >= need || c->host_cap >= c->host_max) return VF_OK;
+  if (int rc = read_state(c)) return rc;
+  c->host_top_lb = c->hstate->swap.host_top;
+  while (c->host_top_lb < need && c->host_cap < c->host_max)
+    if (int rc = grow_host_store(c)) return rc;
+  return VF_OK;
+}
+
 // Empty host store, every entry inactive (GlobalCache constructor, swap.hpp:48-52).
 int reset_swap(vf_ctx* c) {
   if (!c->swapping) return VF_OK;
   VF_CUDA(c, cudaMemset(c->sw.state, 0, (size_t)c->entry_count));
   VF_CUDA(c, cudaMemset(c->sw.host_slot, 0xFF, sizeof(int) * (size_t)c->entry_count));
-  std::vector<int> iota((size_t)c->host_cap);
-  for (int i = 0; i < c->host_cap; ++i) iota[(size_t)i] = c->host_cap - 1 - i;  // pops hand out 0, 1, 2, ...
-  VF_CUDA(c, cudaMemcpy(c->sw.host_free, iota.data(), sizeof(int) * iota.size(), cudaMemcpyHostToDevice));
   SwapCounters sc;
   std::memset(&sc, 0, sizeof(sc));
-  sc.host_top = c->host_cap;
   VF_CUDA(c, cudaMemcpy(&c->dstate->swap, &sc, sizeof(sc), cudaMemcpyHostToDevice));
+  // every chunk's slots on the free stack, chunk 0 on top: pops hand out 0, 1, 2, ...
+  for (int k = (int)c->host_dev_ptrs.size() - 1; k >= 0; --k)
+    k_host_store_grow<<<1, 256, 0, c->stream>>>(c->sw, k, c->host_dev_ptrs[(size_t)k]);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->host_top_lb = c->host_cap;
+  c->journal_read = 0;
   return VF_OK;
+}
+
+// Host address of a host-store slot (the VXBS save / load / read paths).
+uint32_t* host_slot_ptr(const vf_ctx* c, int slot) {
+  return c->host_chunk_ptrs[(size_t)(slot >> kHostChunkShift)] +
+         (size_t)(slot & (kHostChunk - 1)) * kBlockVolume * (size_t)(c->vsize / 4);
 }
 
 int set_pose_dev(vf_ctx* c, const double* pose) {
@@ -1051,7 +1119,10 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       return VF_ERR_INVALID;
     }
     c->swapping = true;
-    c->host_cap = s->swap_host_blocks > 0 ? s->swap_host_blocks : 4 * s->block_count;
+    // one host slot per hash entry, as the reference's GlobalCache (swap.hpp:42-56),
+    // allocated in pinned chunks as the walk needs them; swap_host_blocks > 0 caps it
+    const long want = s->swap_host_blocks > 0 ? s->swap_host_blocks : entries;
+    c->host_max = (int)((want + kHostChunk - 1) / kHostChunk * kHostChunk);
   }
   if (s->shard_count > 1) {
     if (s->shard_count > kMaxShards || s->shard_index < 0 || s->shard_index >= s->shard_count || s->shard_shift < 0 ||
@@ -1194,12 +1265,14 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (c->swapping &&
        ((rc = dalloc(c, &c->sw.state, (size_t)c->entry_count)) ||
         (rc = dalloc(c, &c->sw.host_slot, sizeof(int) * (size_t)c->entry_count)) ||
-        (rc = dalloc(c, &c->sw.host_free, sizeof(int) * (size_t)c->host_cap)) ||
+        (rc = dalloc(c, &c->sw.host_free, sizeof(int) * (size_t)c->host_max)) ||
+        (rc = dalloc(c, &c->sw.host_chunks, sizeof(uint32_t*) * (size_t)(c->host_max / kHostChunk))) ||
         (rc = dalloc(c, &c->sw.in_cand, sizeof(int) * (size_t)c->entry_count)) ||
         (rc = dalloc(c, &c->sw.out_cand, sizeof(int) * (size_t)c->entry_count)) ||
         (rc = dalloc(c, &c->sw.stage_entry, sizeof(int) * 2 * kSwapSortCap)) ||
         (rc = dalloc(c, &c->sw.stage_slot, sizeof(int) * 2 * kSwapSortCap)) ||
-        (rc = dalloc(c, &c->sw.stage_host, sizeof(int) * 2 * kSwapSortCap))))) {
+        (rc = dalloc(c, &c->sw.stage_host, sizeof(int) * 2 * kSwapSortCap)) ||
+        (rc = dalloc(c, &c->sw.journal, sizeof(int) * kSwapJournal))))) {
     free_all(c);
     delete c;
     return rc;
@@ -1211,20 +1284,16 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
     return VF_ERR_CUDA;
   }
   if (c->swapping) {
-    // host block store: pinned, mapped into the device address space (UVA)
-    const size_t bytes = (size_t)c->host_cap * kBlockVolume * (size_t)c->vsize;
-    void* dp = nullptr;
-    if (cudaHostAlloc(reinterpret_cast<void**>(&c->host_pool), bytes, cudaHostAllocMapped | cudaHostAllocPortable) !=
-            cudaSuccess ||
-        cudaHostGetDevicePointer(&dp, c->host_pool, 0) != cudaSuccess) {
-      std::fprintf(stderr, "[voxfuse_b200] cannot allocate the %zu-byte pinned host block store\n", bytes);
-      c->host_pool = nullptr;
-      free_all(c);
-      delete c;
-      return VF_ERR_CUDA;
-    }
-    c->sw.host_pool = reinterpret_cast<uint32_t*>(dp);
+    // host block store: pinned chunks mapped into the device address space
+    // (UVA); the first ones cover one VBA's worth of blocks
     c->sw.ctr = &c->dstate->swap;
+    const int first = std::min(c->host_max, (c->s.block_count + kHostChunk - 1) / kHostChunk * kHostChunk);
+    for (int k = 0; k < first / kHostChunk; ++k)
+      if (int rc2 = add_host_chunk(c)) {
+        free_all(c);
+        delete c;
+        return rc2;
+      }
   }
   if (cudaMallocHost(reinterpret_cast<void**>(&c->hstate), sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->hpose), sizeof(PoseD)) != cudaSuccess) {
@@ -1474,8 +1543,31 @@ int vf_swap_store_read(vf_ctx* c, int entry, uint8_t* payload) {
   int hs = -1;
   VF_CUDA(c, cudaMemcpy(&hs, c->sw.host_slot + entry, sizeof(int), cudaMemcpyDeviceToHost));
   if (hs < 0) return 0;
-  if (payload) encode_block(c, c->host_pool + (size_t)hs * kBlockVolume * (c->vsize / 4), payload);
+  if (payload) encode_block(c, host_slot_ptr(c, hs), payload);
   return 1;
+}
+
+long vf_swap_drain(vf_ctx* c, int* entries, long cap, long* lost) {
+  if (!c || (cap > 0 && !entries)) return VF_ERR_INVALID;
+  if (lost) *lost = 0;
+  if (!c->swapping) return 0;
+  if (int rc = read_state(c)) return rc;
+  const int count = c->hstate->swap.journal_count;
+  long avail = (long)count - c->journal_read;
+  if (avail > kSwapJournal) {  // the ring wrapped before this drain
+    if (lost) *lost = avail - kSwapJournal;
+    c->journal_read = count - kSwapJournal;
+    avail = kSwapJournal;
+  }
+  const long n = std::min(avail, cap);
+  for (long done = 0; done < n;) {
+    const int pos = (c->journal_read + (int)done) & (kSwapJournal - 1);
+    const long run = std::min(n - done, (long)(kSwapJournal - pos));
+    VF_CUDA(c, cudaMemcpy(entries + done, c->sw.journal + pos, sizeof(int) * run, cudaMemcpyDeviceToHost));
+    done += run;
+  }
+  c->journal_read += (int)n;
+  return n;
 }
 
 int vf_swap_save_store(vf_ctx* c, const char* path) {
@@ -1501,7 +1593,7 @@ int vf_swap_save_store(vf_ctx* c, const char* path) {
   for (int i = 0; ok && i < c->entry_count; ++i) {
     if (hs[(size_t)i] < 0) continue;
     put_u32(rec.data(), (uint32_t)i);
-    encode_block(c, c->host_pool + (size_t)hs[(size_t)i] * kBlockVolume * (c->vsize / 4), rec.data() + 4);
+    encode_block(c, host_slot_ptr(c, hs[(size_t)i]), rec.data() + 4);
     ok = std::fwrite(rec.data(), 1, rec.size(), f) == rec.size();
   }
   ok = (std::fclose(f) == 0) && ok;
@@ -1561,19 +1653,26 @@ int vf_swap_load_store(vf_ctx* c, const char* path) {
     if (ents[idx].block_state != kEntrySwappedOut) continue;
     int slot = hs[idx];
     if (slot < 0) {
-      if (top == 0) {
-        rc = VF_ERR_OVERFLOW;
-        c->err = "host block store full";
-        break;
+      if (top == 0) {  // grow: publish the pops so far, push a chunk, re-read the stack
+        VF_CUDA(c, cudaMemcpy(&c->dstate->swap.host_top, &top, sizeof(int), cudaMemcpyHostToDevice));
+        if (grow_host_store(c) != VF_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+          rc = VF_ERR_OVERFLOW;
+          c->err = "host block store full";
+          break;
+        }
+        hfree.resize((size_t)c->host_cap);
+        cudaMemcpy(hfree.data(), c->sw.host_free, sizeof(int) * hfree.size(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&top, &c->dstate->swap.host_top, sizeof(int), cudaMemcpyDeviceToHost);
       }
       slot = hfree[(size_t)--top];
       hs[idx] = slot;
     }
-    decode_block(c, rec.data() + 4, c->host_pool + (size_t)slot * kBlockVolume * (c->vsize / 4));
+    decode_block(c, rec.data() + 4, host_slot_ptr(c, slot));
   }
   std::fclose(f);
   VF_CUDA(c, cudaMemcpy(c->sw.host_slot, hs.data(), sizeof(int) * hs.size(), cudaMemcpyHostToDevice));
   VF_CUDA(c, cudaMemcpy(&c->dstate->swap.host_top, &top, sizeof(int), cudaMemcpyHostToDevice));
+  c->host_top_lb = top;
   return rc;
 }
 

@@ -185,7 +185,7 @@ struct SwapCounters {
   int n_in_cand, n_out_cand;
   int staged_in, staged_out;
   int swapped_in, swapped_out;  // SwapMetrics (swap.hpp:28-40) of the last frame
-  int pad;
+  int journal_count;  // swap-outs ever journalled (sw.journal, a ring of kSwapJournal entries)
   unsigned long long bytes_in, bytes_out;
 };
 struct SwapDev {
@@ -197,9 +197,18 @@ struct SwapDev {
   int* stage_entry;   // staged transfers: swap-ins first, then swap-outs
   int* stage_slot;
   int* stage_host;
-  uint32_t* host_pool;  // pinned, device-mapped: slot * 512 device-layout voxels
+  int* journal;       // ring of swapped-out entry indices, in swap-out order (vf_swap_drain)
+  uint32_t** host_chunks;  // pinned, device-mapped chunks of kHostChunk slots of 512 device-layout voxels
   SwapCounters* ctr;
 };
+constexpr int kSwapJournal = 1 << 16;
+constexpr int kHostChunkShift = 12;  // 4096 host-store slots per pinned chunk
+constexpr int kHostChunk = 1 << kHostChunkShift;
+__device__ __forceinline__ uint32_t* host_block(const SwapDev& sw, int slot, int block_words) {
+  return sw.host_chunks[slot >> kHostChunkShift] + (size_t)(slot & (kHostChunk - 1)) * block_words;
+}
+// appends a new chunk's slots to the free stack (host-store growth between frames)
+__global__ void k_host_store_grow(SwapDev sw, int chunk, uint32_t* chunk_dev_ptr);
 __global__ void k_swap_request(const HashEntry* entries, const int* alloc_list, const FrameParams* fp, IntrD in,
                                float vs, float near_clip, float far_clip, int margin, int swap_margin, SwapDev sw,
                                Counters* ctr);

@@ -186,6 +186,10 @@ __global__ void __launch_bounds__(1024) k_swap_select(HashEntry* __restrict__ en
     sw.host_slot[idx] = hs;
     sw.state[idx] = kSwInactive;
   }
+  // the swap-out journal: the order the reference's file store would write
+  // its records in (swap.hpp:233-251, block_store.cpp:96-115)
+  const int jc = sw.ctr->journal_count;
+  for (int r = tid; r < k_out; r += nt) sw.journal[(jc + r) & (kSwapJournal - 1)] = sw.stage_entry[k_in + r];
   __syncthreads();
   for (int r = tid; r < k_in; r += nt) sw.host_free[host_top - k_out + r] = sw.stage_host[r];
   if (tid == 0) {
@@ -197,6 +201,7 @@ __global__ void __launch_bounds__(1024) k_swap_select(HashEntry* __restrict__ en
     c.n_out_cand = 0;
     c.staged_in = k_in;
     c.staged_out = k_out;
+    c.journal_count = jc + k_out;
     c.swapped_in = k_in;
     c.swapped_out = k_out;
     c.bytes_in = (unsigned long long)k_in * (unsigned long long)(payload_bytes + 4);
@@ -300,11 +305,24 @@ __global__ void __launch_bounds__(256) k_swap_transfer(uint32_t* __restrict__ vo
   const int r0 = which == 0 ? 0 : k_in, r1 = which == 0 ? k_in : k_in + k_out;
   for (int r = r0 + gw; r < r1; r += nw) {
     uint4* dev = reinterpret_cast<uint4*>(voxels + (size_t)sw.stage_slot[r] * block_words);
-    uint4* host = reinterpret_cast<uint4*>(sw.host_pool + (size_t)sw.stage_host[r] * block_words);
+    uint4* host = reinterpret_cast<uint4*>(host_block(sw, sw.stage_host[r], block_words));
     if (words_per_voxel == 1)
       transfer_block<1>(dev, host, which == 0, max_weight);
     else
       transfer_block<2>(dev, host, which == 0, max_weight);
+  }
+}
+
+// The host store grows in pinned chunks as blocks leave (the reference keeps
+// one host slot per hash entry, so its store never fills, swap.hpp:42-56):
+// the chunk's slots go on top of the free stack, popped in ascending order.
+__global__ void k_host_store_grow(SwapDev sw, int chunk, uint32_t* chunk_dev_ptr) {
+  const int top = sw.ctr->host_top;
+  const int first = chunk << kHostChunkShift;
+  for (int i = threadIdx.x; i < kHostChunk; i += blockDim.x) sw.host_free[top + i] = first + kHostChunk - 1 - i;
+  if (threadIdx.x == 0) {
+    sw.host_chunks[chunk] = chunk_dev_ptr;
+    sw.ctr->host_top = top + kHostChunk;
   }
 }
 

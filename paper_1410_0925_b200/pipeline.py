@@ -103,7 +103,7 @@ class EngineSettings:
     shard_halo: bool = True  # ... and fusing surfaces within one block of them
     use_swapping: bool = False  # host swapping (pipeline.hpp:20-23, swap.hpp)
     swap_buffer_blocks: int = 100
-    swap_host_blocks: int = 0  # host store slots (0: 4 x block_count)
+    swap_host_blocks: int = 0  # host store slot cap (0: one per hash entry, like the reference; grown in chunks)
     max_depth: float = 8.0  # disparity conversion clamp (pipeline.hpp:37)
     tracker_type: int = 0  # TrackerType: 0 icp, 1 color, 2 icp_ren (tracking_state.hpp:10)
     ren_sigma: float = 10.0
@@ -363,6 +363,16 @@ class Pipeline:
             if p is not None:
                 out[int(i)] = p
         return out
+
+    def swap_drain(self, cap: int = 1 << 16):
+        """Entries swapped out since the last drain, in swap-out order, and
+        how many fell out of the journal ring (vf_swap_drain)."""
+        out = np.zeros(cap, np.int32)
+        lost = C.c_long()
+        n = self._L.vf_swap_drain(self._h, out.ctypes.data_as(C.POINTER(C.c_int)), cap, C.byref(lost))
+        if n < 0:
+            check("vf_swap_drain", n, self._h)
+        return out[:n].copy(), lost.value
 
     def save_store(self, path: str) -> None:
         """Write the host store as a VXBS file (block_store.hpp:14-53)."""

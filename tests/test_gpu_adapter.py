@@ -130,3 +130,40 @@ def test_streaming_extension_identical(olib, alib):
     assert a[4] == b[4]
     assert np.array_equal(a[5].view(np.uint32), b[5].view(np.uint32))
     assert np.array_equal(a[6].view(np.uint32), b[6].view(np.uint32))
+
+
+def test_ipipeline_swap_store_file_matches_reference(olib, alib, tmp_path):
+    """EngineSettings::swap_store_path through IPipeline: the reference's own
+    FileBlockStore, fed by the GPU as blocks leave, holds the same records in
+    the same order as the reference engine's file (tracked pan, T160)."""
+    import struct
+    from helpers import swap_config
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, pan_trajectory
+    cfg = swap_config("T160_swap_roundtrip").with_(tracking=True)
+    fr = [(q, vf_py.render_depth(olib, cfg, q, BOX_ROOM_SPHERES, BOX_ROOM_PLANES), None) for q in pan_trajectory(20)]
+    alib.vfa_set_store_path.argtypes = [C.c_char_p]
+
+    def records(path):
+        raw = path.read_bytes()
+        magic, version, tag, n, payload = struct.unpack_from("<IHHII", raw, 0)
+        assert (magic, version) == (0x53425856, 1)
+        out, off = [], 16
+        while off < len(raw):
+            (idx,) = struct.unpack_from("<I", raw, off)
+            out.append((idx, raw[off + 4: off + 4 + payload]))
+            off += 4 + payload
+        return (tag, n, payload), out
+
+    files = []
+    for engine in (0, 1):
+        path = tmp_path / f"store{engine}.vxbs"
+        alib.vfa_set_store_path(str(path).encode())
+        _run(alib, cfg, engine, fr)
+        files.append(records(path))
+    alib.vfa_set_store_path(None)
+    (h0, r0), (h1, r1) = files
+    assert h0 == h1
+    assert [i for i, _ in r0] == [i for i, _ in r1], "record order differs"
+    same = sum(a == b for (_, a), (_, b) in zip(r0, r1))
+    print(f"{len(r0)} records, {same} payloads byte-identical")
+    assert len(r0) > 0 and same >= 0.99 * len(r0)

@@ -145,3 +145,40 @@ def test_corridor_tracked_walk(olib):
     assert outs > 10000
     assert rot_angle(p.pose(), poses[-1]) < 0.01 and centre_dist(p.pose(), poses[-1]) < 0.05
     p.close()
+
+
+def test_host_store_grows_past_its_first_chunks(olib):
+    """The host store starts at one VBA's worth of pinned slots and grows in
+    4096-block chunks as blocks leave, up to one slot per hash entry -- the
+    reference's GlobalCache bound (swap.hpp:42-56): a corridor walk that
+    parks several times the VBA on the host never defers a swap-out, and
+    stays bit-exact with the oracle (entries, voxels, states, store)."""
+    from paper_1410_0925_b200.scene import HashConfig
+    cfg = CONFIGS["C4"].with_(width=320, height=240, voxel_size=0.01, mu=0.03, swap_buffer_blocks=256,
+                              hash=HashConfig(bucket_count=1 << 15, excess_count=1 << 13, block_count=1536))
+    spheres, planes, far = scene_for(cfg)
+    p, o = _run_pair(olib, cfg, corridor_trajectory(48), check_every=12, spheres=spheres, planes=planes, far=far)
+    stored = p.store_count()
+    print("stored blocks", stored)
+    assert stored > 4096, "the walk should park more blocks than the first chunk holds"
+    p.close()
+
+
+def test_swap_journal_lists_swap_outs_in_order(olib):
+    """vf_swap_drain: every swapped-out entry once, in the frames' order, and
+    nothing after a drain (what the adapter feeds the VXBS file store)."""
+    cfg = swap_config("T160_swap_small_vba")
+    s, c = settings_from_config(cfg)
+    p = make_pipeline(s, c)
+    total, seen = 0, []
+    for pose in pan_trajectory(24):
+        d = vf_py.render_depth(olib, cfg, pose, BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+        p.set_pose(pose)
+        st = p.process_frame(None, d)
+        ent, lost = p.swap_drain()
+        assert lost == 0 and len(ent) == st.swapped_out
+        total += st.swapped_out
+        seen.extend(ent.tolist())
+    assert len(seen) == total and total > 0
+    assert len(p.swap_drain()[0]) == 0
+    p.close()
