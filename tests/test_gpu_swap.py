@@ -154,10 +154,11 @@ def test_host_store_grows_past_its_first_chunks(olib):
     parks several times the VBA on the host never defers a swap-out, and
     stays bit-exact with the oracle (entries, voxels, states, store)."""
     from paper_1410_0925_b200.scene import HashConfig
-    cfg = CONFIGS["C4"].with_(width=320, height=240, voxel_size=0.01, mu=0.03, swap_buffer_blocks=256,
+    cfg = CONFIGS["C4"].with_(tracking=False, width=320, height=240, voxel_size=0.01, mu=0.03, swap_buffer_blocks=512,
                               hash=HashConfig(bucket_count=1 << 15, excess_count=1 << 13, block_count=1536))
     spheres, planes, far = scene_for(cfg)
-    p, o = _run_pair(olib, cfg, corridor_trajectory(48), check_every=12, spheres=spheres, planes=planes, far=far)
+    walk = corridor_trajectory(48, step=0.3)  # 14 m at known poses: blocks leave the swap frustum fast
+    p, o = _run_pair(olib, cfg, walk, check_every=12, spheres=spheres, planes=planes, far=far)
     stored = p.store_count()
     print("stored blocks", stored)
     assert stored > 4096, "the walk should park more blocks than the first chunk holds"
