@@ -176,6 +176,23 @@ def corridor_trajectory(n_frames: int, step: float = 0.05) -> np.ndarray:
     return out
 
 
+def look_around_trajectory(n_frames: int, step: float = 0.02, amp: float = 0.6, period: int = 120) -> np.ndarray:
+    """Corridor walk (2 cm per frame) while the camera looks from side to side
+    (yaw +-0.6 rad, at most ~1.8 deg per frame): wall blocks leave the
+    enlarged swap frustum and come back, so swap-ins and fuse_voxels
+    (swap.hpp:96-131, 136-198) run every few frames, not only swap-outs."""
+    out = np.zeros((n_frames, 12))
+    for i in range(n_frames):
+        a = 2.0 * math.pi * i / period
+        centre = np.array([0.1 * math.sin(a), 0.0, step * i])
+        r_w2c = _rot_y(amp * math.sin(a)).T
+        out[i, :9] = r_w2c.reshape(-1)
+        out[i, 9:] = -r_w2c @ centre
+    out[0, :9] = np.eye(3).reshape(-1)
+    out[0, 9:] = 0.0
+    return out
+
+
 def scene_for(cfg):
     """(spheres, planes, far) of a config's scene."""
     if getattr(cfg, "scene", "box_room") == "corridor":
@@ -184,6 +201,8 @@ def scene_for(cfg):
 
 
 def trajectory_for(cfg, n_frames: int) -> np.ndarray:
+    if getattr(cfg, "walk", "default") == "look_around":
+        return look_around_trajectory(n_frames)
     if getattr(cfg, "scene", "box_room") == "corridor":
         return corridor_trajectory(n_frames)
     return trajectory(n_frames)
@@ -235,6 +254,7 @@ class BenchConfig:
     swap_buffer_blocks: int = 100
     scene: str = "box_room"  # box_room | corridor
     tracker: str = "icp"  # TrackerType: icp | color | icp_ren (tracking_state.hpp:10)
+    walk: str = "default"  # default (scene's own) | look_around (corridor, swaps in as well as out)
 
     @property
     def intrinsics(self):
@@ -270,6 +290,15 @@ CONFIGS = {
     # exhaust the 2^18-block pool after ~30 m and drop allocations).
     "C4": BenchConfig("C4", 640, 480, 0.005, frames=1000, use_swapping=True, swap_buffer_blocks=512,
                       scene="corridor"),
+    # C4 at BASELINE.md's swap budget B = 100 blocks per frame: the walk
+    # allocates faster than 100 blocks leave, so allocations are dropped once
+    # the pool fills (reported in the bench line's swap section)
+    "C4B100": BenchConfig("C4B100", 640, 480, 0.005, frames=1000, use_swapping=True, swap_buffer_blocks=100,
+                          scene="corridor"),
+    # the corridor walked while looking from side to side at B = 100: blocks
+    # leave and return, so the timed frames include swap-ins and fuse_voxels
+    "C4R": BenchConfig("C4R", 640, 480, 0.005, frames=1000, use_swapping=True, swap_buffer_blocks=100,
+                       scene="corridor", walk="look_around"),
     # configs[4]: the large-scale scene spatially sharded by block hash
     # across 2/4/8 GPUs (bench.py --gpus N default): the corridor walk,
     # tracked, each shard with the reference's default pool of 2^18 blocks

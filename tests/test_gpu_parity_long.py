@@ -136,3 +136,12 @@ def test_c4_corridor_with_swapping_vs_reference(checker):
     # the swap engine moves the same blocks (counts within 1 % over the walk)
     (gi, go), (ri, ro) = out["swap_totals"]
     assert abs(go - ro) <= 0.01 * max(ro, 1) + 2 and abs(gi - ri) <= 0.01 * max(ri, 1) + 2, out["swap_totals"]
+
+
+def test_c4_look_around_swaps_in_vs_reference(checker):
+    """C4R: the corridor walked while looking side to side at B = 100: swap-ins
+    and fuse_voxels on a tracked sequence, against the reference."""
+    out = _run(checker, "C4R", 60)
+    _assert_bars(out)
+    (gi, go), (ri, ro) = out["swap_totals"]
+    assert ri > 0 and abs(gi - ri) <= 0.01 * ri + 2 and abs(go - ro) <= 0.01 * ro + 2, out["swap_totals"]

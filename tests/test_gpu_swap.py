@@ -183,3 +183,17 @@ def test_swap_journal_lists_swap_outs_in_order(olib):
     assert len(seen) == total and total > 0
     assert len(p.swap_drain()[0]) == 0
     p.close()
+
+
+def test_corridor_look_around_swaps_in_bit_exact(olib):
+    """C4R's walk (config 4 scene, B = 100 as BASELINE states) at known poses:
+    blocks leave the enlarged frustum and come back, so swap-ins with
+    fuse_voxels (swap.hpp:96-131, 136-198) run alongside swap-outs -- entries,
+    voxels, states and the host store stay bit-exact with the oracle."""
+    from paper_1410_0925_b200.scene import trajectory_for
+    cfg = CONFIGS["C4R"].with_(tracking=False)
+    spheres, planes, far = scene_for(cfg)
+    p, o = _run_pair(olib, cfg, trajectory_for(cfg, 44), check_every=11, spheres=spheres, planes=planes, far=far)
+    ins = o.store_count()
+    p.close()
+    assert ins > 0
