@@ -67,6 +67,9 @@ def parse():
                     help="N>1: one volume spatially sharded by block hash across the GPUs (default; config 5, "
                          "NCCL nearest-depth map composite in the frame graph) or independent sequences per GPU")
     ap.add_argument("--no-roofline-large", action="store_true", help="skip the C3 integration roofline leg")
+    ap.add_argument("--shard-icp", action="store_true",
+                    help="shard mode: pixel-sharded ICP with the per-iteration sums exchanged through peer memory "
+                         "(default: every rank runs the whole ICP on the composited maps)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch the ranks and set up the process group, report them, run nothing on the GPU")
     return ap.parse_args()
@@ -116,7 +119,9 @@ def config_dict(cfg, args, world: int) -> dict:
                     + (f", {cfg.scene} scene" if cfg.scene != "box_room" else "")
                     + (f", swapping B={cfg.swap_buffer_blocks}" if cfg.use_swapping else ""),
         "frames": f"{args.warmup} warm-up (incl. frame 0) then frames {args.warmup}..{args.warmup + args.steps - 1} timed",
-        "parallelism": (f"volume sharded by block hash over {world} GPUs (NCCL map composite)" if sharded
+        "parallelism": (f"volume sharded by block hash over {world} GPUs (NCCL map composite, "
+                        f"{'pixel-sharded ICP, peer-memory sums' if getattr(args, 'shard_icp', False) else 'replicated ICP'})"
+                        if sharded
                         else f"one sequence per GPU x{world}" if world > 1 else "single GPU"),
         "l2": f"flushed between frames ({args.l2_flush_mib} MiB write, outside the timed intervals)",
         "graphs": True,
@@ -366,7 +371,7 @@ def run_ours(args, dist: Dist):
     if sharded:
         from dataclasses import replace
 
-        settings = replace(settings, shard_count=dist.world, shard_index=dist.rank)
+        settings = replace(settings, shard_count=dist.world, shard_index=dist.rank, shard_icp=args.shard_icp)
 
     def new_pipeline():
         p = make_pipeline(settings, calib, device=device)
@@ -374,6 +379,10 @@ def run_ours(args, dist: Dist):
             from paper_1410_0925_b200.sharding import attach_nccl
 
             attach_nccl(p, dist.rank, dist.world, dist.pg)
+            if args.shard_icp:  # pixel-sharded ICP: per-iteration sums over CUDA IPC peer memory
+                from paper_1410_0925_b200.sharding import attach_icp_peers
+
+                attach_icp_peers(p, dist.rank, dist.world, dist.pg)
         return p
 
     swaps = []

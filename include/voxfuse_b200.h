@@ -103,6 +103,13 @@ typedef struct vf_settings {
    *     blend; parity bar: SDF within 1 LSB of int16 and weight exact on
    *     >= 99.9 % of voxels (SURVEY §8(c) TSDF tolerance). VoxelS only. */
   int integration_mode;
+  /* Pixel-sharded ICP (config 5): 1 = each shard sums the ICP
+   * terms of 1/shard_count of the pixels and the per-iteration 29 sums are
+   * added across shards inside the ICP kernel through peer memory (link the
+   * shards with vf_shard_icp_link / vf_shard_icp_link_local); 0 = every shard
+   * runs the whole ICP on the composited maps (replicated, no exchange). */
+  int shard_icp;
+  int icp_max_ctas; /* 0: one ICP CTA per SM (x occupancy); > 0 caps it (shards sharing a device) */
 } vf_settings;
 
 enum vf_integration_mode { VF_INTEGRATION_EXACT = 0, VF_INTEGRATION_FAST = 1 };
@@ -301,6 +308,17 @@ int vf_swap_load_store(vf_ctx* ctx, const char* path);
 
 /* --- spatial sharding ---
  * Owner shard of a block position (the device rule, for hosts and tests). */
+/* Pixel-sharded ICP links.  One process per GPU: every rank publishes
+ * vf_shard_icp_handle (a 64-byte CUDA IPC handle of its exchange area), the
+ * handles are gathered in rank order, and each rank calls vf_shard_icp_link
+ * with all of them.  Shards sharing one device in one process:
+ * vf_shard_icp_link_local with the contexts in shard order.  Either replaces
+ * the frame graphs; afterwards the shards' frames must run concurrently
+ * (each ICP iteration waits for every shard's sums; ~0.5 s without them
+ * fails the frame's tracking instead of hanging). */
+int vf_shard_icp_handle(vf_ctx* ctx, void* handle_out /* 64 bytes */);
+int vf_shard_icp_link(vf_ctx* ctx, const void* handles /* count x 64 bytes */, int count);
+int vf_shard_icp_link_local(vf_ctx** ctxs, int count);
 int vf_shard_owner(int bx, int by, int bz, int shard_shift, int shard_count);
 /* One process per GPU: rank 0 creates an NCCL unique id (128 bytes), every
  * rank attaches with it; each frame then ends with the nearest-depth map

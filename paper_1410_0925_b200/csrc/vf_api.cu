@@ -165,6 +165,12 @@ struct vf_ctx {
   cudaEvent_t ev_frame0 = nullptr, ev_frame1 = nullptr;
   bool profiling = false;
   bool stage_timing = false;
+  // pixel-sharded ICP (vf_settings.shard_icp): the exchange area and every
+  // shard's mapping of its own (vf_shard_icp_link / _link_local)
+  double* icp_xchg = nullptr;
+  double* icp_peers[kMaxShards] = {};
+  int icp_linked = 0;
+  std::vector<void*> ipc_opened;
   long l2_persist_bytes = 0;  // hash-table bytes under the persisting access-policy window  // per-frame FrameStats::ms_* (event nodes in the frame graph)
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long profiled_frames = 0;
@@ -208,8 +214,17 @@ bool frame_trace() {
 // always for stage calls, in frames only with VF_ICP_TRACE set (the extra
 // stores sit on the critical path of CTA 0 between grid barriers).
 int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool update_state = true,
-               int first_level = 0, bool trace = true) {
+               int first_level = 0, bool trace = true, bool exchange = false) {
   IcpArgs a{};
+  a.xrank = 0;
+  a.xranks = 1;
+  a.ctr = &c->dstate->ctr;
+  if (exchange && c->icp_linked > 1) {  // pixel-sharded ICP, sums exchanged through peer memory
+    a.xrank = c->shard.index;
+    a.xranks = c->icp_linked;
+    for (int r = 0; r < c->icp_linked; ++r) a.xpeer[r] = c->icp_peers[r];
+    a.xstate = reinterpret_cast<unsigned long long*>(c->icp_xchg + kXchgLocal);
+  }
   const int L = c->s.hierarchy_levels - first_level;
   size_t off = 0;
   for (int g = 0; g < c->s.hierarchy_levels; ++g) {
@@ -435,7 +450,7 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
     }
     return enqueue_ren(c, st, true, explicit_init, update_state, launches);
   }
-  if (int rc = launch_icp(c, st, false, update_state, 0, frame_trace())) return rc;
+  if (int rc = launch_icp(c, st, false, update_state, 0, frame_trace(), /*exchange=*/true)) return rc;
   VF_LAUNCHED(c, "k_icp");
   ++*launches;
   return VF_OK;
@@ -873,6 +888,9 @@ void free_all(vf_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hstate) cudaFreeHost(c->hstate);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  if (c->icp_xchg) cudaFree(c->icp_xchg);
   for (uint32_t* h : c->host_chunk_ptrs) cudaFreeHost(h);
   c->host_chunk_ptrs.clear();
   if (c->hpose) cudaFreeHost(c->hpose);
@@ -1179,6 +1197,9 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_icp, kIcpThreads, 0);
   if (occ < 1) occ = 1;
   c->icp_grid = std::min(c->num_sms * std::min(occ, 2), kMaxIcpGrid);
+  // several sharded ICP loops on one device must be co-resident (each waits
+  // for the others' sums): vf_settings.icp_max_ctas caps the grid
+  if (s->icp_max_ctas > 0) c->icp_grid = std::min(c->icp_grid, s->icp_max_ctas);
   {
     // stage up to the whole level-0 share of each thread in shared memory,
     // within what the SM leaves each of its resident ICP CTAs
@@ -1304,6 +1325,13 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaEventCreate(&c->ev_frame0);
   cudaEventCreate(&c->ev_frame1);
+  if (s->shard_icp && s->shard_count > 1 &&
+      (cudaMalloc(reinterpret_cast<void**>(&c->icp_xchg), kXchgBytes) != cudaSuccess ||
+       cudaMemset(c->icp_xchg, 0, kXchgBytes) != cudaSuccess)) {
+    free_all(c);
+    delete c;
+    return VF_ERR_CUDA;
+  }
   persist_hash_table(c);
   if ((rc = reset_volume(c))) {
     free_all(c);
@@ -2030,6 +2058,74 @@ long vf_selftest_division(int device, int mode, float p0, float p1, float p2, lo
   cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
   cudaFree(d);
   return e == cudaSuccess ? (long)h : VF_ERR_CUDA;
+}
+
+// ---- pixel-sharded ICP: peer mappings of the exchange areas ----
+namespace {
+void drop_graphs(vf_ctx* c) {
+  for (auto& plane : c->graph)
+    for (auto& row : plane)
+      for (auto& g : row)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
+}
+}  // namespace
+
+int vf_shard_icp_link_local(vf_ctx** ctxs, int count) {
+  if (!ctxs || count < 2 || count > kMaxShards) return VF_ERR_INVALID;
+  for (int r = 0; r < count; ++r) {
+    vf_ctx* c = ctxs[r];
+    if (!c || !c->icp_xchg || c->shard.count != count || c->shard.index != r || c->device != ctxs[0]->device)
+      return VF_ERR_INVALID;
+  }
+  for (int r = 0; r < count; ++r) {
+    vf_ctx* c = ctxs[r];
+    cudaSetDevice(c->device);
+    VF_CUDA(c, cudaStreamSynchronize(c->stream));
+    VF_CUDA(c, cudaMemset(c->icp_xchg, 0, kXchgBytes));
+    for (int k = 0; k < count; ++k) c->icp_peers[k] = ctxs[k]->icp_xchg;
+    c->icp_linked = count;
+    drop_graphs(c);  // the frame graph now carries the exchange
+  }
+  return VF_OK;
+}
+
+int vf_shard_icp_handle(vf_ctx* c, void* handle_out) {
+  if (!c || !handle_out) return VF_ERR_INVALID;
+  if (!c->icp_xchg) {
+    c->err = "vf_shard_icp_handle: create the context with shard_icp = 1 and shard_count > 1";
+    return VF_ERR_STATE;
+  }
+  cudaSetDevice(c->device);
+  cudaIpcMemHandle_t h;
+  VF_CUDA(c, cudaIpcGetMemHandle(&h, c->icp_xchg));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return VF_OK;
+}
+
+int vf_shard_icp_link(vf_ctx* c, const void* handles, int count) {
+  if (!c || !handles || count != c->shard.count || count < 2 || count > kMaxShards) return VF_ERR_INVALID;
+  if (!c->icp_xchg) return VF_ERR_STATE;
+  cudaSetDevice(c->device);
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemset(c->icp_xchg, 0, kXchgBytes));
+  for (int r = 0; r < count; ++r) {
+    if (r == c->shard.index) {
+      c->icp_peers[r] = c->icp_xchg;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    VF_CUDA(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    c->icp_peers[r] = static_cast<double*>(p);
+  }
+  c->icp_linked = count;
+  drop_graphs(c);
+  return VF_OK;
 }
 
 int vf_shard_owner(int bx, int by, int bz, int shard_shift, int shard_count) {

@@ -163,6 +163,73 @@ __device__ __forceinline__ double warp_sum(double v) {
 // grid is cooperative and partials go through global memory behind a grid
 // barrier (fine levels).  The controller state enters / leaves through
 // a.ctl_io when the loop is split between the two kernels.
+// Sharded ICP: the iteration's 29 sums, summed across the
+// shards inside the persistent kernel over peer memory (NVLink P2P / CUDA IPC
+// mappings) -- the allreduce fused into the ICP loop, no kernel boundary and
+// no host round trip.  CTA 0 of each shard writes its total into every
+// shard's exchange area and raises its flag there (release, system scope),
+// waits for all shards' flags in its own area (acquire), sums the totals in
+// shard order -- identical on every shard, so every controller takes the
+// same decision -- and hands the sum to its own CTAs through a local flag.
+// Exchanges alternate between two parities: a shard can only write parity p
+// again after every shard published the exchange in between, i.e. after every
+// shard finished reading p.  If a peer does not answer within ~0.5 s the sum
+// is replaced by zeros (count 0: every level is left, tracking fails) and an
+// error flag is raised, so a missing shard cannot hang the frame.
+__device__ __forceinline__ void shard_exchange(const IcpArgs& a, unsigned long long seq, double* s_tot, int tid) {
+  __shared__ int s_bad;
+  const int par = (int)(seq & 1ull);
+  unsigned long long* local = a.xstate;  // [0] counter, [1] local flag, [2 + 32 * par + i] summed totals
+  if (blockIdx.x == 0) {
+    if (tid < kAcc)
+      for (int r = 0; r < a.xranks; ++r) a.xpeer[r][kXchgTotals + (par * 16 + a.xrank) * 32 + tid] = s_tot[tid];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      for (int r = 0; r < a.xranks; ++r) {
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(a.xpeer[r] + kXchgFlags) + par * 16 + a.xrank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(seq) : "memory");
+      }
+      const unsigned long long* own = reinterpret_cast<const unsigned long long*>(a.xpeer[a.xrank] + kXchgFlags);
+      int bad = 0;
+      for (int r = 0; r < a.xranks && !bad; ++r) {
+        unsigned long long v = 0;
+        for (long spin = 0;; ++spin) {
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(own + par * 16 + r) : "memory");
+          if (v >= seq) break;
+          if (spin > (1l << 22)) {
+            bad = 1;
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      s_bad = bad;
+      if (bad) atomicOr(&a.ctr->error_flags, kErrShardXchg);
+    }
+    __syncthreads();
+    if (tid < kAcc) {
+      double t = 0;
+      const double* tot = a.xpeer[a.xrank] + kXchgTotals;
+      for (int r = 0; r < a.xranks; ++r) t += *reinterpret_cast<const volatile double*>(tot + (par * 16 + r) * 32 + tid);
+      reinterpret_cast<double*>(local + 2)[32 * par + tid] = s_bad ? 0.0 : t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(local + 1), "l"(seq) : "memory");
+    }
+  } else if (tid == 0) {
+    unsigned long long v = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(local + 1) : "memory");
+    } while (v < seq);
+  }
+  __syncthreads();
+  if (tid < kAcc) s_tot[tid] = *reinterpret_cast<const volatile double*>(reinterpret_cast<double*>(local + 2) + 32 * par + tid);
+  __syncthreads();
+}
+
 template <bool kCluster>
 __device__ __forceinline__ void icp_body(const IcpArgs& a) {
   __shared__ Ctl ctl;
@@ -181,6 +248,12 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
       (reinterpret_cast<uintptr_t>(s_xy + a.max_slots * blockDim.x) + 15) & ~static_cast<uintptr_t>(15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const bool timer = blockIdx.x == 0 && tid == 0 && a.trace;
+  // pixel chunks: this CTA is chunk column vblk of a virtual grid of all
+  // shards' CTAs (one shard: the grid itself)
+  const int vblk = blockIdx.x + a.xrank * gridDim.x, vgrid = gridDim.x * a.xranks;
+  const bool xchg = a.xranks > 1;
+  const unsigned long long xseq0 = xchg ? *reinterpret_cast<volatile unsigned long long*>(a.xstate) : 0ull;
+  unsigned long long nx = 0;  // exchanges done by this launch
   if (tid == 0) {
     if (a.ctl_in) {
       ctl = *reinterpret_cast<const Ctl*>(a.ctl_io);
@@ -212,12 +285,12 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
     // Depth and unprojection are iteration-invariant: stage this CTA's pixel
     // slots (depth + packed x, y) and the level's (x - cx) / fx, (y - cy) / fy
     // tables in shared memory once per level.
-    const int gstride = gridDim.x * blockDim.x;
-    const int nslots = min((npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride, a.max_slots);
+    const int gstride = vgrid * blockDim.x;
+    const int nslots = min((npix - (int)(vblk * blockDim.x) + gstride - 1) / gstride, a.max_slots);
     for (int i = tid; i < lv.w; i += blockDim.x) s_ux[i] = __ldg(lv.ux + i);
     for (int i = tid; i < lv.h; i += blockDim.x) s_uy[i] = __ldg(lv.uy + i);
     for (int k = 0; k < nslots; ++k) {
-      const int pix = blockIdx.x * blockDim.x + tid + k * gstride;
+      const int pix = vblk * blockDim.x + tid + k * gstride;
       float d = 0.0f;
       int xy = 0;
       if (pix < npix) {
@@ -250,7 +323,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
       // into shared memory with cp.async before the back half of step n
       // (bilinear blends, point-to-plane term, sums) consumes its own taps, so
       // the tap round trip and the next transforms overlap the current terms.
-      const int total_slots = (npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride;
+      const int total_slots = (npix - (int)(vblk * blockDim.x) + gstride - 1) / gstride;
       IcpStage st0, st1;
       auto front = [&](int k0, int stage, IcpStage& S) {
         float d[kInflight];
@@ -258,7 +331,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
 #pragma unroll
         for (int k = 0; k < kInflight; ++k) {
           const int slot = k0 + k;
-          const int pix = blockIdx.x * blockDim.x + tid + slot * gstride;
+          const int pix = vblk * blockDim.x + tid + slot * gstride;
           if (slot < nslots) {
             d[k] = s_depth[slot * blockDim.x + tid];
             const int xy = s_xy[slot * blockDim.x + tid];
@@ -364,14 +437,14 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
       // kInflight pixels per step, each pipeline stage issued for all before it is
       // consumed, so their memory round trips (depth + tables, then the
       // eight map taps) overlap.
-      const int total_slots = (npix - (int)(blockIdx.x * blockDim.x) + gstride - 1) / gstride;
+      const int total_slots = (npix - (int)(vblk * blockDim.x) + gstride - 1) / gstride;
       for (int k0 = 0; k0 < total_slots; k0 += kInflight) {
         float d[kInflight];
         double ux[kInflight], uy[kInflight];
 #pragma unroll
         for (int k = 0; k < kInflight; ++k) {
           const int slot = k0 + k;
-          const int pix = blockIdx.x * blockDim.x + tid + slot * gstride;
+          const int pix = vblk * blockDim.x + tid + slot * gstride;
           if (slot < nslots) {  // staged in shared memory
             d[k] = s_depth[slot * blockDim.x + tid];
             const int xy = s_xy[slot * blockDim.x + tid];
@@ -525,6 +598,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
         buf ^= 1;
       }
       __syncthreads();
+      if (xchg) shard_exchange(a, ++nx + xseq0, s_tot, tid);
       long long t3 = timer ? clock64() : 0;
       if (tid == 0) {
         const double* tot = s_tot;
@@ -623,6 +697,7 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
   }
   if (kCluster) cg::this_cluster().sync();  // no CTA leaves while others read its shared memory
   if (blockIdx.x == 0 && tid == 0) {
+    if (xchg) *reinterpret_cast<volatile unsigned long long*>(a.xstate) = xseq0 + nx;
     ctl.trace_rows = trace_rows;
     if (!a.is_last) {
       *reinterpret_cast<Ctl*>(a.ctl_io) = ctl;

@@ -61,7 +61,22 @@ struct IcpArgs {
   void* ctl_io;            // controller state handed from the cluster to the grid kernel
   int ctl_in;              // 1: start from *ctl_io instead of the pose
   int is_last;             // 1: write the IcpResult (and the tracked pose)
+  // Pixel-sharded ICP (vf_settings.shard_icp): this shard sums the terms of
+  // every xranks-th CTA-sized pixel chunk (offset xrank) and the 29 per-shard
+  // totals of each iteration are summed across the shards through peer
+  // memory (IcpXchg).  xranks == 1: no exchange.
+  int xrank, xranks;
+  double* xpeer[16];               // every shard's IcpXchg (own included; P2P / IPC mapped)
+  unsigned long long* xstate;      // own IcpXchg::local (local totals, flags, exchange counter)
+  Counters* ctr;                   // error flag on an exchange timeout
 };
+
+// Per-shard exchange area of the sharded ICP, one cudaMalloc (IPC-shareable):
+//   [0, 2*16*32)        doubles: totals written by shard r for exchange parity p at [(p*16 + r)*32]
+//   [1024, 1024 + 32)   u64: flags, shard r's latest exchange number at [1024 + p*16 + r]
+//   local (xstate): [0] exchange counter, [1] local flag, [2..] 2 x 32 doubles of the summed totals
+constexpr int kXchgTotals = 0, kXchgFlags = 1024, kXchgLocal = 1024 + 32;
+constexpr size_t kXchgBytes = sizeof(double) * (kXchgLocal + 2 + 64);
 
 __global__ void k_prep(const PoseD* pose, IntrD depth_in, IntrD rgb_in, PoseD depth_to_rgb, FrameParams* fp);
 struct ShardSpec {

@@ -109,6 +109,8 @@ class EngineSettings:
     ren_sigma: float = 10.0
     skip_points: bool = False
     integration_mode: int = 0  # 0 exact (bit-exact), 1 fast (<= 1 LSB tolerance; VoxelS)
+    shard_icp: bool = False  # pixel-sharded ICP, per-iteration sums exchanged through peer memory
+    icp_max_ctas: int = 0    # cap of the ICP grid (shards sharing one device)
 
     def to_c(self) -> VfSettings:
         s = VfSettings()

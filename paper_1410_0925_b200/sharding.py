@@ -71,21 +71,36 @@ def composite(points: np.ndarray, normals: np.ndarray, w2c: np.ndarray, rank: in
 
 
 class LocalShardGroup:
-    """G shards of one volume in this process on one device."""
+    """G shards of one volume in this process on one device.
 
-    def __init__(self, settings, calib, count: int, shift: int = 3, device: int = 0, halo: bool = True):
+    shard_icp=True: pixel-sharded ICP, the shards' per-iteration sums
+    exchanged inside the ICP kernels (vf_shard_icp_link_local); the shards'
+    frames are then submitted together so their ICP loops run concurrently,
+    each capped to 128 / G CTAs so they are co-resident on the device."""
+
+    def __init__(self, settings, calib, count: int, shift: int = 3, device: int = 0, halo: bool = True,
+                 shard_icp: bool = False):
         from dataclasses import replace
 
-        self.shards = [make_pipeline(replace(settings, shard_count=count, shard_index=i, shard_shift=shift, shard_halo=halo), calib,
-                                     device) for i in range(count)]
+        extra = {"shard_icp": True, "icp_max_ctas": max(8, 128 // count)} if shard_icp else {}
+        self.shards = [make_pipeline(replace(settings, shard_count=count, shard_index=i, shard_shift=shift,
+                                             shard_halo=halo, **extra), calib, device) for i in range(count)]
         self._handles = (C.c_void_p * count)(*[s.handle.value for s in self.shards])
+        self.shard_icp = shard_icp
+        if shard_icp:
+            _abi.check("vf_shard_icp_link_local", _abi.load().vf_shard_icp_link_local(self._handles, count))
 
     def set_pose(self, pose):
         for s in self.shards:
             s.set_pose(pose)
 
     def process_frame(self, rgb, depth_m):
-        stats = [s.process_frame(rgb, depth_m) for s in self.shards]
+        if self.shard_icp:  # all shards in flight at once: their ICP loops wait for each other
+            for s in self.shards:
+                s.submit_frame(rgb, depth_m)
+            stats = [s.collect_frame() for s in self.shards]
+        else:
+            stats = [s.process_frame(rgb, depth_m) for s in self.shards]
         _abi.check("vf_shard_composite_local",
                    _abi.load().vf_shard_composite_local(self._handles, len(self.shards)))
         return stats
@@ -111,3 +126,15 @@ def attach_nccl(pipe: Pipeline, rank: int, world: int, dist) -> None:
     """One process per GPU: share rank 0's NCCL id over `dist` and attach."""
     idb = (C.c_uint8 * 128).from_buffer_copy(share_nccl_id(rank, dist))
     _abi.check("vf_shard_attach_nccl", _abi.load().vf_shard_attach_nccl(pipe.handle, idb, world, rank))
+
+
+def attach_icp_peers(pipe: Pipeline, rank: int, world: int, dist) -> None:
+    """One process per GPU, pixel-sharded ICP: gather every rank's CUDA IPC
+    handle of its exchange area in rank order and link (vf_shard_icp_link)."""
+    L = _abi.load()
+    own = (C.c_uint8 * 64)()
+    _abi.check("vf_shard_icp_handle", L.vf_shard_icp_handle(pipe.handle, own))
+    allh = [None] * world
+    dist.all_gather_object(allh, bytes(own))
+    buf = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(allh))
+    _abi.check("vf_shard_icp_link", L.vf_shard_icp_link(pipe.handle, buf, world))

@@ -76,6 +76,35 @@ def test_sharded_tracking_replicated_icp(olib):
     ref.close()
 
 
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_tracking_exchanged_icp(olib, G):
+    """Pixel-sharded ICP: each shard sums the ICP terms of 1/G
+    of the pixels and the 29 sums of every iteration are added across the
+    shards inside the ICP kernels through peer memory.  Every shard ends each
+    frame with the bit-identical pose; the poses agree with the replicated-ICP
+    group (only the order of the FP64 sums differs) and the unsharded run
+    within the tracking tolerance."""
+    cfg = CONFIGS["C1"]
+    s, c = settings_from_config(cfg)
+    ref = make_pipeline(s, c)
+    rep = LocalShardGroup(s, c, G, shift=3)
+    grp = LocalShardGroup(s, c, G, shift=3, shard_icp=True)
+    for pose, d, _ in frames(olib, cfg, 8):
+        ref.process_frame(None, d)
+        sr = rep.process_frame(None, d)
+        st = grp.process_frame(None, d)
+        assert all(x.tracking_ok for x in st) and all(x.error_flags == 0 for x in st)
+        assert [x.tracking_iterations for x in st] == [st[0].tracking_iterations] * G
+        ps = [g.pose() for g in grp.shards]
+        assert all(np.array_equal(ps[0], p) for p in ps[1:]), "shards disagree on the pose"
+        pr = rep.shards[0].pose()
+        assert rot_angle(pr, ps[0]) < 1e-4 and centre_dist(pr, ps[0]) < 1e-4
+        assert rot_angle(ref.pose(), ps[0]) < 1e-3 and centre_dist(ref.pose(), ps[0]) < 1e-3
+    grp.close()
+    rep.close()
+    ref.close()
+
+
 def test_owner_rule_matches_device():
     L = _abi.load()
     rng = np.random.default_rng(7)
