@@ -110,6 +110,8 @@ typedef struct vf_settings {
    * runs the whole ICP on the composited maps (replicated, no exchange). */
   int shard_icp;
   int icp_max_ctas; /* 0: one ICP CTA per SM (x occupancy); > 0 caps it (shards sharing a device) */
+  int tracker_exact_solve; /* colour tracker: 1 = every damped LM step through the reference's pivoted
+                              LDLT (color_tracker.hpp:126-128); 0 = register LDLT, pivoted fallback */
 } vf_settings;
 
 enum vf_integration_mode { VF_INTEGRATION_EXACT = 0, VF_INTEGRATION_FAST = 1 };

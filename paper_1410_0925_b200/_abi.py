@@ -89,6 +89,7 @@ class VfSettings(C.Structure):
         ("integration_mode", C.c_int),
         ("shard_icp", C.c_int),
         ("icp_max_ctas", C.c_int),
+        ("tracker_exact_solve", C.c_int),
     ]
 
 

@@ -398,6 +398,7 @@ int enqueue_color(vf_ctx* c, cudaStream_t st, const PoseD* explicit_init, bool u
   a.result = &c->dstate->icp;
   a.update_state = update_state ? 1 : 0;
   a.partials = c->partials;
+  a.exact_solve = s.tracker_exact_solve;
   // one CTA per kColorThreads surface points (up to one per SM), over a
   // cooperative grid: an evaluation is then one point per thread deep
   int g = std::max(1, std::min({c->num_sms, c->icp_grid, (c->surf_cap + kColorThreads - 1) / kColorThreads}));

@@ -182,6 +182,7 @@ struct ColorTrackArgs {
   IcpResult* result;
   int update_state;
   double* partials;  // grid launch: 2 x gridDim x 32 per-CTA sums (double-buffered)
+  int exact_solve;   // 1: every damped step through the reference's pivoted LDLT (vf_settings.tracker_exact_solve)
 };
 __global__ void k_cpyr_base(const uint8_t* rgb, int n, float4* out);
 __global__ void k_cpyr_down(const float4* src, int sw, int sh, float4* dst);

@@ -428,8 +428,10 @@ __global__ void __launch_bounds__(kColorThreads) k_color_track(ColorTrackArgs a)
     if ((long long)s_eval[28] < a.min_valid_points) continue;
     any_level_ok = true;
     for (int iter = 0; iter < a.max_iterations; ++iter) {
-#ifndef VF_COLOR_EXACT_LDLT
-      if (threadIdx.x == 0) {
+      // default: the unrolled register LDLT, the pivoted path only when the
+      // damped system is not numerically SPD; exact_solve: always pivoted
+      // (the reference's LDLT, so accept / convergence ties resolve alike)
+      if (!a.exact_solve && threadIdx.x == 0) {
         double tw[6];
         if (spd_solve_damped6(s_eval, lambda, tw)) {
           s_flag = 0;
@@ -442,9 +444,7 @@ __global__ void __launch_bounds__(kColorThreads) k_color_track(ColorTrackArgs a)
         }
       }
       __syncthreads();
-      if (s_flag == 2)
-#endif
-      if (threadIdx.x == 0) {
+      if ((a.exact_solve || s_flag == 2) && threadIdx.x == 0) {
         s_flag = 0;
         double h[36];
         for (int p = 0, k = 0; p < 6; ++p)

@@ -111,6 +111,7 @@ class EngineSettings:
     integration_mode: int = 0  # 0 exact (bit-exact), 1 fast (<= 1 LSB tolerance; VoxelS)
     shard_icp: bool = False  # pixel-sharded ICP, per-iteration sums exchanged through peer memory
     icp_max_ctas: int = 0    # cap of the ICP grid (shards sharing one device)
+    tracker_exact_solve: bool = False  # colour tracker: the reference's pivoted LDLT on every step
 
     def to_c(self) -> VfSettings:
         s = VfSettings()

@@ -113,3 +113,26 @@ def test_colour_tracker_with_swapping(olib, rlib):
         outs += st.swapped_out
     assert outs > 0
     p.close()
+
+
+def test_colour_sequence_exact_solve_iterations(olib, rlib):
+    """tracker_exact_solve = 1: every damped Levenberg-Marquardt step of the
+    colour tracker goes through the reference's pivoted LDLT
+    (color_tracker.hpp:126-128), so the accept / reject and convergence ties
+    resolve as in the reference: same ok and the same iteration count on every
+    frame of a tracked sequence, poses within 1e-5."""
+    from dataclasses import replace
+    cfg = CONFIGS["C2"].with_(tracking=True, tracker="color")
+    fr = frames(olib, cfg, 6, rgb=True)
+    s, c = settings_from_config(cfg)
+    p = make_pipeline(replace(s, tracker_exact_solve=True), c)
+    r = vf_py.Volume(rlib, cfg, tracking=True)
+    for i, (pose, depth, col) in enumerate(fr):
+        st = p.process_frame(col, depth)
+        sr = r.process(depth, col)
+        assert bool(st.tracking_ok) == bool(sr.tracking_ok), f"frame {i}: ok"
+        assert st.tracking_iterations == sr.tracking_iterations, \
+            f"frame {i}: iterations {st.tracking_iterations} vs {sr.tracking_iterations}"
+        gp, rp = p.pose(), r.pose()
+        assert rot_angle(gp, rp) <= 1e-5 and centre_dist(gp, rp) <= 1e-5, f"frame {i}"
+    p.close()
