@@ -555,7 +555,7 @@ def run_ours(args, dist: Dist):
         stage_kernels = {"raycast": ("k_raycast",), "tracking": ("k_pyramid", "k_icp_cluster", "k_icp")}
         rows = {}
         for stage, kernels in stage_kernels.items():
-            b = sum((ncu_kernel_bytes("r1i_ncu.json", "c1_full", k) or 0.0) for k in kernels)
+            b = sum((ncu_kernel_bytes("r2_ncu.json", "c1_full", k) or 0.0) for k in kernels)
             ms = stages.get(stage, 0.0)
             if b > 0 and ms > 0:
                 gbs = b / (ms * 1e-3) / 1e9
@@ -674,7 +674,10 @@ def roofline_large(args, device: int, hbm_peak: float, peak_src: str) -> dict:
         # B = N_vis (512 sizeof(V) + 4 + 16) + N_mod sizeof(V) + W H 4 (VoxelS)
         b = float(np.mean(nvis)) * (512 * 4 + 20) + float(np.mean(nmod)) * 4 + w * h * 4
         gbs = b / (ms * 1e-3) / 1e9
-        out[name] = {"kernel": "k_integrate_s" if mode == 0 else "k_integrate_fast", "achieved": gbs,
+        kname = "k_integrate_s" if mode == 0 else "k_integrate_fast"
+        tb = ncu_kernel_bytes("r2_ncu.json", "c3_integrate_exact" if mode == 0 else "c3_integrate_fast", kname)
+        out[name] = {"kernel": kname, "achieved": gbs, "traffic": tb,
+                     "traffic_source": "profiles/r2_ncu.json (ncu --set full, same kernel at C3): dram read + write",
                      "frac": gbs / hbm_peak, "ms_per_launch": ms, "algorithmic_bytes_per_launch": b,
                      "visible_blocks": float(np.mean(nvis)), "voxel_visits_per_s": float(np.mean(nvis)) * 512 / (ms * 1e-3)}
     for f in frames:
@@ -685,8 +688,8 @@ def roofline_large(args, device: int, hbm_peak: float, peak_src: str) -> dict:
 # Committed `ncu --set full` captures of the roofline kernel per config
 # (profiles/): dram__bytes_read.sum + dram__bytes_write.sum of one launch.
 NCU_TRAFFIC = {
-    "C1": ("r1i_ncu.json", "c1_full", "k_integrate_s"),
-    "C3": ("r1i_ncu.json", "c3_integrate", "k_integrate_s"),
+    "C1": ("r2_ncu.json", "c1_full", "k_integrate_s"),
+    "C3": ("r2_ncu.json", "c3_integrate_exact", "k_integrate_s"),
     "C2": ("r1d_ncu_c2c4.json", "c2_rgb", "k_integrate_rgb"),
 }
 
