@@ -67,6 +67,9 @@ def parse():
                     help="N>1: one volume spatially sharded by block hash across the GPUs (default; config 5, "
                          "NCCL nearest-depth map composite in the frame graph) or independent sequences per GPU")
     ap.add_argument("--no-roofline-large", action="store_true", help="skip the C3 integration roofline leg")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="shard mode: the per-frame map composite over peer memory in one kernel (default) or "
+                         "as NCCL collectives in the frame graph")
     ap.add_argument("--shard-icp", action="store_true",
                     help="shard mode: pixel-sharded ICP with the per-iteration sums exchanged through peer memory "
                          "(default: every rank runs the whole ICP on the composited maps)")
@@ -119,7 +122,8 @@ def config_dict(cfg, args, world: int) -> dict:
                     + (f", {cfg.scene} scene" if cfg.scene != "box_room" else "")
                     + (f", swapping B={cfg.swap_buffer_blocks}" if cfg.use_swapping else ""),
         "frames": f"{args.warmup} warm-up (incl. frame 0) then frames {args.warmup}..{args.warmup + args.steps - 1} timed",
-        "parallelism": (f"volume sharded by block hash over {world} GPUs (NCCL map composite, "
+        "parallelism": (f"volume sharded by block hash over {world} GPUs "
+                        f"({'peer-memory' if getattr(args, 'transport', 'p2p') == 'p2p' else 'NCCL'} map composite, "
                         f"{'pixel-sharded ICP, peer-memory sums' if getattr(args, 'shard_icp', False) else 'replicated ICP'})"
                         if sharded
                         else f"one sequence per GPU x{world}" if world > 1 else "single GPU"),
@@ -137,11 +141,22 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.dev = None
         if self.world > 1:
+            import torch
             import torch.distributed as dist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("gloo")
+            # the host-side plumbing (barriers, max over ranks, handle exchange)
+            # over NCCL when every rank has its own GPU, else gloo (CPU tests,
+            # VF_BENCH_ONE_DEVICE plumbing runs: NCCL refuses two ranks on one GPU)
+            backend = "gloo"
+            if (torch.cuda.is_available() and torch.cuda.device_count() >= self.world
+                    and not os.environ.get("VF_BENCH_ONE_DEVICE")):
+                backend = "nccl"
+                torch.cuda.set_device(self.local_rank)
+                self.dev = torch.device("cuda", self.local_rank)
+            dist.init_process_group(backend)
             self.pg = dist
 
     def barrier(self):
@@ -153,7 +168,7 @@ class Dist:
             return v
         import torch
 
-        t = torch.tensor([v], dtype=torch.float64)
+        t = torch.tensor([v], dtype=torch.float64, device=self.dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -162,7 +177,7 @@ class Dist:
             return v
         import torch
 
-        t = torch.tensor([v], dtype=torch.float64)
+        t = torch.tensor([v], dtype=torch.float64, device=self.dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
         return float(t.item())
 
@@ -378,7 +393,12 @@ def run_ours(args, dist: Dist):
         if sharded:  # NCCL nearest-depth composite inside the frame graph
             from paper_1410_0925_b200.sharding import attach_nccl
 
-            attach_nccl(p, dist.rank, dist.world, dist.pg)
+            if args.transport == "p2p":  # one composite kernel over peer memory (CUDA IPC over NVLink)
+                from paper_1410_0925_b200.sharding import attach_p2p
+
+                attach_p2p(p, dist.rank, dist.world, dist.pg)
+            else:
+                attach_nccl(p, dist.rank, dist.world, dist.pg)
             if args.shard_icp:  # pixel-sharded ICP: per-iteration sums over CUDA IPC peer memory
                 from paper_1410_0925_b200.sharding import attach_icp_peers
 

@@ -318,6 +318,16 @@ int vf_swap_load_store(vf_ctx* ctx, const char* path);
  * the frame graphs; afterwards the shards' frames must run concurrently
  * (each ICP iteration waits for every shard's sums; ~0.5 s without them
  * fails the frame's tracking instead of hanging). */
+/* The per-frame nearest-depth composite over peer memory instead of NCCL
+ * (one kernel reads the other shards' keys and winning map entries over
+ * NVLink; flags instead of collectives).  One process per GPU: gather every
+ * rank's vf_shard_p2p_handles (4 CUDA IPC handles, 256 bytes) in rank order
+ * and call vf_shard_p2p_link with all of them; shards sharing a device in one
+ * process: vf_shard_p2p_link_local.  Mutually exclusive with the NCCL
+ * attach; the shards' frames must then run concurrently. */
+int vf_shard_p2p_handles(vf_ctx* ctx, void* out /* 4 x 64 bytes */);
+int vf_shard_p2p_link(vf_ctx* ctx, const void* handles /* count x 256 bytes */, int count);
+int vf_shard_p2p_link_local(vf_ctx** ctxs, int count);
 int vf_shard_icp_handle(vf_ctx* ctx, void* handle_out /* 64 bytes */);
 int vf_shard_icp_link(vf_ctx* ctx, const void* handles /* count x 64 bytes */, int count);
 int vf_shard_icp_link_local(vf_ctx** ctxs, int count);

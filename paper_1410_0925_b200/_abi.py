@@ -43,7 +43,7 @@ EXPORTS = [
     "vf_stage_allocate", "vf_stage_integrate", "vf_stage_raycast", "vf_stage_icp", "vf_icp_trace",
     "vf_stage_ren", "vf_stage_color",
     "vf_depth_pyramid", "vf_render_synthetic",
-    "vf_shard_owner", "vf_shard_icp_handle", "vf_shard_icp_link", "vf_shard_icp_link_local", "vf_shard_nccl_unique_id", "vf_shard_attach_nccl", "vf_shard_composite_local",
+    "vf_shard_owner", "vf_shard_p2p_handles", "vf_shard_p2p_link", "vf_shard_p2p_link_local", "vf_shard_icp_handle", "vf_shard_icp_link", "vf_shard_icp_link_local", "vf_shard_nccl_unique_id", "vf_shard_attach_nccl", "vf_shard_composite_local",
     "vf_device_alloc", "vf_device_free", "vf_memcpy_h2d", "vf_memcpy_d2h", "vf_host_alloc_pinned",
     "vf_host_free_pinned", "vf_event_record", "vf_event_elapsed_ms", "vf_set_profiling", "vf_set_stage_timing", "vf_raycast_counters", "vf_stage_times",
     "vf_kernel_launches_per_frame", "vf_readback_bytes", "vf_flush_l2", "vf_flush_time", "vf_last_modified_voxels",
@@ -206,6 +206,9 @@ def load() -> C.CDLL:
         "vf_depth_pyramid": (C.c_int, [vp, vp, vp]),
         "vf_render_synthetic": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, vp, dp, C.POINTER(VfIntrinsics),
                                           C.c_double, C.c_double, vp, vp]),
+        "vf_shard_p2p_handles": (C.c_int, [vp, vp]),
+        "vf_shard_p2p_link": (C.c_int, [vp, vp, C.c_int]),
+        "vf_shard_p2p_link_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
         "vf_shard_icp_handle": (C.c_int, [vp, vp]),
         "vf_shard_icp_link": (C.c_int, [vp, vp, C.c_int]),
         "vf_shard_icp_link_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),

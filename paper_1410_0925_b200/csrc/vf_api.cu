@@ -171,6 +171,10 @@ struct vf_ctx {
   double* icp_peers[kMaxShards] = {};
   int icp_linked = 0;
   std::vector<void*> ipc_opened;
+  // nearest-depth composite over peer memory (vf_shard_p2p_link / _link_local)
+  unsigned long long* p2p_flags = nullptr;
+  P2PArgs p2p{};
+  int p2p_linked = 0;
   long l2_persist_bytes = 0;  // hash-table bytes under the persisting access-policy window  // per-frame FrameStats::ms_* (event nodes in the frame graph)
   double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long profiled_frames = 0;
@@ -619,10 +623,23 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
                                              s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
   }
   VF_LAUNCHED(c, "k_ranges");
+  if (c->p2p_linked > 1) {  // the previous frame's maps and keys are no longer read by any shard
+    k_p2p_wait_done<<<1, 32, 0, st>>>(c->p2p);
+    ++launches;
+  }
   if (int rc = launch_raycast(c, st)) return rc;
   VF_LAUNCHED(c, "k_raycast");
   launches += 2;
-  if (c->nccl_comm) {  // nearest-depth composite across the GPUs (vf_shard.cu)
+  if (c->p2p_linked > 1) {  // nearest-depth composite over peer memory (vf_shard.cu)
+    const int blocks = (c->npix + 255) / 256;
+    k_shard_keys<<<blocks, 256, 0, st>>>(c->points, &c->dstate->fp, c->npix, c->shard.index, c->shard_keys);
+    k_p2p_signal_ready<<<1, 32, 0, st>>>(c->p2p);
+    k_p2p_wait_ready<<<1, 32, 0, st>>>(c->p2p);
+    k_p2p_composite<<<c->num_sms * 4, 256, 0, st>>>(c->p2p, c->points, c->normals, c->npix);
+    k_p2p_signal_done<<<1, 32, 0, st>>>(c->p2p);
+    VF_LAUNCHED(c, "k_p2p_composite");
+    launches += 5;
+  } else if (c->nccl_comm) {  // nearest-depth composite across the GPUs (vf_shard.cu)
     if (nccl_composite(c->nccl_comm, st, &c->dstate->fp, c->points, c->normals, c->shard_keys, c->npix,
                        c->shard.index) != 0) {
       c->err = "NCCL composite failed";
@@ -892,6 +909,7 @@ void free_all(vf_ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->ipc_opened.clear();
   if (c->icp_xchg) cudaFree(c->icp_xchg);
+  if (c->p2p_flags) cudaFree(c->p2p_flags);
   for (uint32_t* h : c->host_chunk_ptrs) cudaFreeHost(h);
   c->host_chunk_ptrs.clear();
   if (c->hpose) cudaFreeHost(c->hpose);
@@ -1326,6 +1344,13 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaEventCreate(&c->ev_frame0);
   cudaEventCreate(&c->ev_frame1);
+  if (s->shard_count > 1 && (cudaMalloc(reinterpret_cast<void**>(&c->p2p_flags),
+                                        sizeof(unsigned long long) * kP2PFlagWords) != cudaSuccess ||
+                             cudaMemset(c->p2p_flags, 0, sizeof(unsigned long long) * kP2PFlagWords) != cudaSuccess)) {
+    free_all(c);
+    delete c;
+    return VF_ERR_CUDA;
+  }
   if (s->shard_icp && s->shard_count > 1 &&
       (cudaMalloc(reinterpret_cast<void**>(&c->icp_xchg), kXchgBytes) != cudaSuccess ||
        cudaMemset(c->icp_xchg, 0, kXchgBytes) != cudaSuccess)) {
@@ -2074,6 +2099,84 @@ void drop_graphs(vf_ctx* c) {
 }
 }  // namespace
 
+// ---- nearest-depth composite over peer memory ----
+namespace {
+void p2p_fill(vf_ctx* c, int r, const unsigned long long* keys, const float4* pts, const float4* nrm,
+              unsigned long long* flags) {
+  c->p2p.keys[r] = keys;
+  c->p2p.points[r] = pts;
+  c->p2p.normals[r] = nrm;
+  c->p2p.flags[r] = flags;
+}
+}  // namespace
+
+int vf_shard_p2p_link_local(vf_ctx** ctxs, int count) {
+  if (!ctxs || count < 2 || count > kMaxShards) return VF_ERR_INVALID;
+  for (int r = 0; r < count; ++r) {
+    vf_ctx* c = ctxs[r];
+    if (!c || !c->p2p_flags || c->shard.count != count || c->shard.index != r || c->device != ctxs[0]->device ||
+        c->npix != ctxs[0]->npix || c->nccl_comm)
+      return VF_ERR_INVALID;
+  }
+  for (int r = 0; r < count; ++r) {
+    vf_ctx* c = ctxs[r];
+    cudaSetDevice(c->device);
+    VF_CUDA(c, cudaStreamSynchronize(c->stream));
+    VF_CUDA(c, cudaMemset(c->p2p_flags, 0, sizeof(unsigned long long) * kP2PFlagWords));
+    c->p2p.n = count;
+    c->p2p.rank = r;
+    c->p2p.ctr = &c->dstate->ctr;
+    for (int k = 0; k < count; ++k)
+      p2p_fill(c, k, ctxs[k]->shard_keys, ctxs[k]->points, ctxs[k]->normals, ctxs[k]->p2p_flags);
+    c->p2p_linked = count;
+    drop_graphs(c);
+  }
+  return VF_OK;
+}
+
+int vf_shard_p2p_handles(vf_ctx* c, void* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  if (!c->p2p_flags) return VF_ERR_STATE;
+  cudaSetDevice(c->device);
+  void* ptrs[4] = {c->shard_keys, c->points, c->normals, c->p2p_flags};
+  for (int k = 0; k < 4; ++k) {
+    cudaIpcMemHandle_t h;
+    VF_CUDA(c, cudaIpcGetMemHandle(&h, ptrs[k]));
+    std::memcpy(static_cast<uint8_t*>(out) + k * sizeof(h), &h, sizeof(h));
+  }
+  return VF_OK;
+}
+
+int vf_shard_p2p_link(vf_ctx* c, const void* handles, int count) {
+  if (!c || !handles || count != c->shard.count || count < 2 || count > kMaxShards || c->nccl_comm)
+    return VF_ERR_INVALID;
+  if (!c->p2p_flags) return VF_ERR_STATE;
+  cudaSetDevice(c->device);
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  VF_CUDA(c, cudaMemset(c->p2p_flags, 0, sizeof(unsigned long long) * kP2PFlagWords));
+  c->p2p.n = count;
+  c->p2p.rank = c->shard.index;
+  c->p2p.ctr = &c->dstate->ctr;
+  for (int r = 0; r < count; ++r) {
+    if (r == c->shard.index) {
+      p2p_fill(c, r, c->shard_keys, c->points, c->normals, c->p2p_flags);
+      continue;
+    }
+    void* p[4];
+    for (int k = 0; k < 4; ++k) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const uint8_t*>(handles) + ((size_t)r * 4 + k) * sizeof(h), sizeof(h));
+      VF_CUDA(c, cudaIpcOpenMemHandle(&p[k], h, cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(p[k]);
+    }
+    p2p_fill(c, r, static_cast<const unsigned long long*>(p[0]), static_cast<const float4*>(p[1]),
+             static_cast<const float4*>(p[2]), static_cast<unsigned long long*>(p[3]));
+  }
+  c->p2p_linked = count;
+  drop_graphs(c);
+  return VF_OK;
+}
+
 int vf_shard_icp_link_local(vf_ctx** ctxs, int count) {
   if (!ctxs || count < 2 || count > kMaxShards) return VF_ERR_INVALID;
   for (int r = 0; r < count; ++r) {
@@ -2239,7 +2342,7 @@ int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
         track = (L > 1 ? 1 : 0) + icp;
     }
   }
-  return 7 + track + (c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 4 : 0);
+  return 7 + track + (c->p2p_linked > 1 ? 6 : c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 4 : 0);
 }
 
 }  // extern "C"

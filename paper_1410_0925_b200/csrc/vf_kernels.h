@@ -242,6 +242,24 @@ struct ShardGroupArgs {
 __global__ void k_shard_keys(const float4* points, const FrameParams* fp, int npix, int rank, unsigned long long* keys);
 __global__ void k_shard_select(const unsigned long long* keys_min, int npix, int rank, float4* points, float4* normals);
 __global__ void k_shard_group_composite(ShardGroupArgs g, int npix);
+// The nearest-depth composite over peer memory (one process per GPU, CUDA IPC
+// mappings over NVLink; or shards sharing a device).  Flags area per shard:
+// [kP2PReady + r] / [kP2PDone + r] = the latest frame shard r published /
+// finished reading; [kP2PSeq] this shard's frame counter.
+constexpr int kP2PReady = 0, kP2PDone = 16, kP2PSeq = 32, kP2PMask = 33, kP2PFlagWords = 40;
+struct P2PArgs {
+  int n, rank;
+  const unsigned long long* keys[kMaxShards];
+  const float4* points[kMaxShards];
+  const float4* normals[kMaxShards];
+  unsigned long long* flags[kMaxShards];  // every shard's flags area (own included)
+  Counters* ctr;
+};
+__global__ void k_p2p_wait_done(P2PArgs a);
+__global__ void k_p2p_signal_ready(P2PArgs a);
+__global__ void k_p2p_wait_ready(P2PArgs a);
+__global__ void k_p2p_composite(P2PArgs a, float4* points, float4* normals, int npix);
+__global__ void k_p2p_signal_done(P2PArgs a);
 int nccl_unique_id(void* out);
 int nccl_comm_init(void** comm, const void* id_bytes, int nranks, int rank);
 void nccl_comm_destroy(void* comm);

@@ -74,6 +74,105 @@ __global__ void k_shard_group_composite(ShardGroupArgs g, int npix) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Peer-memory composite (no NCCL): every shard publishes its per-pixel keys
+// and reads the other shards' keys and winning map entries directly from
+// their memory.  Per frame, on each shard's stream:
+//   k_p2p_wait_done     -- before the raycast overwrites keys / maps: every
+//                          shard finished reading the previous frame's;
+//   raycast, k_shard_keys
+//   k_p2p_signal_ready  -- frame number f into every shard's ready[rank]
+//                          (release, system scope, after a system fence);
+//   k_p2p_wait_ready    -- one thread waits for ready[r] >= f for all r (acquire);
+//   k_p2p_composite     -- per pixel: min key over the shards, the winner's point
+//                          and normal into this shard's maps (its own pixels
+//                          untouched, so readers never race with writers);
+//   k_p2p_signal_done   -- f into every shard's done[rank].
+// Every shard ends with the identical maps the NCCL path produces.  A shard
+// that does not answer within ~0.5 s counts as "no hit" and raises
+// kErrShardXchg instead of hanging the frame.
+namespace {
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// wait until flags[base + r] >= seq for every shard r; returns the mask of shards that answered
+__device__ unsigned wait_all(const P2PArgs& a, int base, unsigned long long seq) {
+  const unsigned long long* own = a.flags[a.rank];
+  unsigned ok = 0;
+  for (int r = 0; r < a.n; ++r) {
+    for (long spin = 0;; ++spin) {
+      if (ld_acquire_sys(own + base + r) >= seq) {
+        ok |= 1u << r;
+        break;
+      }
+      if (spin > (1l << 22)) {
+        atomicOr(&a.ctr->error_flags, kErrShardXchg);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  return ok;
+}
+}  // namespace
+
+__global__ void k_p2p_wait_done(P2PArgs a) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long seq = a.flags[a.rank][kP2PSeq];  // the previous frame (0: none)
+  if (seq > 0) wait_all(a, kP2PDone, seq);
+}
+
+__global__ void k_p2p_signal_ready(P2PArgs a) {
+  if (threadIdx.x != 0) return;
+  unsigned long long* own = a.flags[a.rank];
+  const unsigned long long seq = own[kP2PSeq] + 1;
+  own[kP2PSeq] = seq;
+  __threadfence_system();  // this shard's keys and maps before the flag
+  for (int r = 0; r < a.n; ++r) st_release_sys(a.flags[r] + kP2PReady + a.rank, seq);
+}
+
+// One thread waits (a full grid of spinning CTAs would starve the other
+// shards' kernels when shards share a device); the answer mask goes to the
+// composite through the flags area.
+__global__ void k_p2p_wait_ready(P2PArgs a) {
+  if (threadIdx.x != 0) return;
+  unsigned long long* own = a.flags[a.rank];
+  own[kP2PMask] = wait_all(a, kP2PReady, own[kP2PSeq]);
+}
+
+__global__ void k_p2p_composite(P2PArgs a, float4* __restrict__ points, float4* __restrict__ normals, int npix) {
+  const unsigned ok = (unsigned)a.flags[a.rank][kP2PMask];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += gridDim.x * blockDim.x) {
+    unsigned long long best = ~0ull;
+    for (int r = 0; r < a.n; ++r) {
+      if (!((ok >> r) & 1u)) continue;
+      const unsigned long long k = __ldcv(a.keys[r] + i);
+      best = k < best ? k : best;
+    }
+    const int w = best == ~0ull ? -1 : (int)(best & 0xffffffffu);
+    if (w == a.rank) continue;  // this shard's own hit stays (and may be read by the others)
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p;
+    if (w >= 0) {
+      p = __ldcv(a.points[w] + i);
+      q = __ldcv(a.normals[w] + i);
+    }
+    points[i] = p;
+    normals[i] = q;
+  }
+}
+
+__global__ void k_p2p_signal_done(P2PArgs a) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long seq = a.flags[a.rank][kP2PSeq];
+  __threadfence_system();
+  for (int r = 0; r < a.n; ++r) st_release_sys(a.flags[r] + kP2PDone + a.rank, seq);
+}
+
 }  // namespace vf
 
 // ---------------------------------------------------------------------------

@@ -79,30 +79,39 @@ class LocalShardGroup:
     each capped to 128 / G CTAs so they are co-resident on the device."""
 
     def __init__(self, settings, calib, count: int, shift: int = 3, device: int = 0, halo: bool = True,
-                 shard_icp: bool = False):
+                 shard_icp: bool = False, transport: str = "local"):
         from dataclasses import replace
 
+        if transport not in ("local", "p2p"):
+            raise ValueError("transport: 'local' (one composite kernel over all shards) or 'p2p' (per-shard "
+                             "composite over peer memory, inside each shard's frame)")
         extra = {"shard_icp": True, "icp_max_ctas": max(8, 128 // count)} if shard_icp else {}
         self.shards = [make_pipeline(replace(settings, shard_count=count, shard_index=i, shard_shift=shift,
                                              shard_halo=halo, **extra), calib, device) for i in range(count)]
         self._handles = (C.c_void_p * count)(*[s.handle.value for s in self.shards])
         self.shard_icp = shard_icp
+        self.transport = transport
+        L = _abi.load()
         if shard_icp:
-            _abi.check("vf_shard_icp_link_local", _abi.load().vf_shard_icp_link_local(self._handles, count))
+            _abi.check("vf_shard_icp_link_local", L.vf_shard_icp_link_local(self._handles, count))
+        if transport == "p2p":
+            _abi.check("vf_shard_p2p_link_local", L.vf_shard_p2p_link_local(self._handles, count))
 
     def set_pose(self, pose):
         for s in self.shards:
             s.set_pose(pose)
 
     def process_frame(self, rgb, depth_m):
-        if self.shard_icp:  # all shards in flight at once: their ICP loops wait for each other
+        if self.shard_icp or self.transport == "p2p":
+            # all shards in flight at once: their exchanges wait for each other
             for s in self.shards:
                 s.submit_frame(rgb, depth_m)
             stats = [s.collect_frame() for s in self.shards]
         else:
             stats = [s.process_frame(rgb, depth_m) for s in self.shards]
-        _abi.check("vf_shard_composite_local",
-                   _abi.load().vf_shard_composite_local(self._handles, len(self.shards)))
+        if self.transport == "local":
+            _abi.check("vf_shard_composite_local",
+                       _abi.load().vf_shard_composite_local(self._handles, len(self.shards)))
         return stats
 
     def close(self):
@@ -138,3 +147,16 @@ def attach_icp_peers(pipe: Pipeline, rank: int, world: int, dist) -> None:
     dist.all_gather_object(allh, bytes(own))
     buf = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(allh))
     _abi.check("vf_shard_icp_link", L.vf_shard_icp_link(pipe.handle, buf, world))
+
+
+def attach_p2p(pipe: Pipeline, rank: int, world: int, dist) -> None:
+    """One process per GPU, the composite over peer memory: gather every
+    rank's four CUDA IPC handles (keys, points, normals, flags) in rank order
+    and link (vf_shard_p2p_link)."""
+    L = _abi.load()
+    own = (C.c_uint8 * 256)()
+    _abi.check("vf_shard_p2p_handles", L.vf_shard_p2p_handles(pipe.handle, own))
+    allh = [None] * world
+    dist.all_gather_object(allh, bytes(own))
+    buf = (C.c_uint8 * (256 * world)).from_buffer_copy(b"".join(allh))
+    _abi.check("vf_shard_p2p_link", L.vf_shard_p2p_link(pipe.handle, buf, world))

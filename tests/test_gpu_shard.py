@@ -173,3 +173,104 @@ def test_sharded_corridor_with_swapping(olib):
             assert hit >= 0.99 and pts >= 0.99 and nrm >= 0.97, (hit, pts, nrm)
             ref.close()
         grp.close()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_p2p_composite_matches_group_composite(olib, G):
+    """The composite over peer memory (each shard reads the others' keys and
+    winning map entries inside its own frame) gives the maps of the
+    single-kernel group composite bit for bit, on every shard."""
+    cfg = CONFIGS["T320"].with_(tracking=False)
+    s, c = settings_from_config(cfg)
+    loc = LocalShardGroup(s, c, G, shift=2)
+    p2p = LocalShardGroup(s, c, G, shift=2, transport="p2p")
+    for pose, d, _ in frames(olib, cfg, 4):
+        loc.set_pose(pose)
+        p2p.set_pose(pose)
+        loc.process_frame(None, d)
+        st = p2p.process_frame(None, d)
+        assert all(x.error_flags == 0 for x in st)
+        a = loc.shards[0].tracking_state()
+        for sh in p2p.shards:
+            b = sh.tracking_state()
+            assert np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+            assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+    loc.close()
+    p2p.close()
+
+
+def _mp_shard_worker(rank, world, port, frames_np, q):
+    """One shard per process, both on device 0: IPC handles over gloo,
+    composite and ICP sums over peer memory (the multi-GPU code path; on one
+    device the two contexts time-slice, so only correctness is meaningful)."""
+    import os
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import hashlib
+    from dataclasses import replace
+
+    import torch.distributed as dist
+
+    from paper_1410_0925_b200 import make_pipeline, settings_from_config
+    from paper_1410_0925_b200.scene import CONFIGS
+    from paper_1410_0925_b200.sharding import attach_icp_peers, attach_p2p
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    s, c = settings_from_config(CONFIGS["T320"])
+    s = replace(s, shard_count=world, shard_index=rank, shard_shift=2, shard_icp=True, icp_max_ctas=64)
+    p = make_pipeline(s, c, device=0)
+    attach_p2p(p, rank, world, dist)
+    attach_icp_peers(p, rank, world, dist)
+    out = []
+    for d in frames_np:
+        st = p.process_frame(None, d)
+        pts, nrm = p.tracking_state()
+        out.append((bool(st.tracking_ok), int(st.error_flags), p.pose().tolist(),
+                    hashlib.sha256(pts.tobytes() + nrm.tobytes()).hexdigest()))
+    p.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+def test_two_processes_p2p_shards_match_in_process_group(olib):
+    """The multi-process sharded pipeline -- one process per shard, CUDA IPC
+    mappings exchanged over a real process group, the map composite and the
+    per-iteration ICP sums over peer memory -- reproduces the in-process
+    group bit for bit (poses and maps), on both ranks."""
+    import hashlib
+    import socket
+    from dataclasses import replace
+
+    import torch.multiprocessing as mp
+    cfg = CONFIGS["T320"]
+    fr = [d for _, d, _ in frames(olib, cfg, 4)]
+    s, c = settings_from_config(cfg)
+    grp = LocalShardGroup(s, c, 2, shift=2, shard_icp=True, transport="p2p")
+    want = []
+    for d in fr:
+        st = grp.process_frame(None, d)
+        pts, nrm = grp.shards[0].tracking_state()
+        want.append((bool(st[0].tracking_ok), grp.shards[0].pose().tolist(),
+                     hashlib.sha256(pts.tobytes() + nrm.tobytes()).hexdigest()))
+    grp.close()
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_shard_worker, args=(r, 2, port, fr, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        for i, ((ok, err, pose, digest), (wok, wpose, wdigest)) in enumerate(zip(res[r], want)):
+            assert err == 0, f"rank {r} frame {i}: exchange error flags {err}"
+            assert ok == wok and pose == wpose, f"rank {r} frame {i}: pose differs from the in-process group"
+            assert digest == wdigest, f"rank {r} frame {i}: maps differ"
