@@ -650,12 +650,13 @@ def raycast_rates(cnt, ray_ms: float) -> dict:
 
 
 def roofline_large(args, device: int, hbm_peak: float, peak_src: str) -> dict:
-    """the >= 60 % HBM target is judged at C3 (or a C2 bench
-    with >= 100k visible blocks); C1's ~19k-block launch is latency-bound.
-    Same process, same GPU: the C3 frames (1280x960, 2 mm, 2^20 blocks) at
-    their known poses, per-stage CUDA events around the integration kernel,
-    L2 flushed between frames; both integration modes (exact: bit-exact vs
-    the reference; fast: <= 1 LSB, tests/test_gpu_integration_fast.py)."""
+    """the >= 60 % HBM target is judged at C3 or at a C2
+    kernel bench with >= 100k visible blocks; C1's ~19k-block launch is
+    latency-bound.  Same process, same GPU: the C3 frames (1280x960, 2 mm,
+    2^20 blocks, VoxelS) and the C2L frames (the same at VoxelSRgb, with RGB)
+    at their known poses, per-stage CUDA events around the integration
+    kernel, L2 flushed between frames; both integration modes (exact:
+    bit-exact vs the reference; fast: <= 1 LSB, tests/test_gpu_integration_fast.py)."""
     from dataclasses import replace
 
     from paper_1410_0925_b200 import DeviceBuffer, Intrinsics, make_pipeline, render_synthetic, settings_from_config
@@ -663,45 +664,55 @@ def roofline_large(args, device: int, hbm_peak: float, peak_src: str) -> dict:
     from paper_1410_0925_b200.scene import CONFIGS, scene_for, trajectory_for
 
     L = _abi.load()
-    cfg = CONFIGS["C3"].with_(tracking=False)
-    fx, fy, cx, cy, w, h = cfg.intrinsics
     warm, timed = 3, 10
-    poses = trajectory_for(cfg, warm + timed)
-    spheres, planes, far = scene_for(cfg)
-    frames = [DeviceBuffer(w * h * 4) for _ in poses]
-    for i, pose in enumerate(poses):
-        render_synthetic(pose, Intrinsics(fx, fy, cx, cy, w, h), spheres, planes, frames[i].ptr, None, far=far,
-                         device=device)
-    settings, calib = settings_from_config(cfg)
-    out = {"config": f"C3 frames {warm}..{warm + timed - 1} at known poses (integration kernel only timed), "
-                     f"L2 flushed ({args.l2_flush_mib} MiB) before every frame",
+    out = {"config": f"C3 (VoxelS) and C2L (VoxelSRgb + RGB) frames {warm}..{warm + timed - 1} at known poses "
+                     f"(integration kernel only timed), L2 flushed ({args.l2_flush_mib} MiB) before every frame",
            "bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "peak_source": peak_src}
-    for mode, name in ((0, "exact"), (1, "fast")):
-        p = make_pipeline(replace(settings, integration_mode=mode), calib, device=device)
-        nvis, nmod = [], []
+    for cname in ("C3", "C2L"):
+        cfg = CONFIGS[cname].with_(tracking=False)
+        rgb = cfg.voxel_type == 2
+        vsize = 8 if rgb else 4
+        fx, fy, cx, cy, w, h = cfg.intrinsics
+        poses = trajectory_for(cfg, warm + timed)
+        spheres, planes, far = scene_for(cfg)
+        frames = [DeviceBuffer(w * h * 4) for _ in poses]
+        colours = [DeviceBuffer(w * h * 3) for _ in poses] if rgb else None
         for i, pose in enumerate(poses):
-            if i == warm:
-                p.set_profiling(True)
-            p.set_pose(pose)
-            _abi.check("vf_flush_l2", L.vf_flush_l2(p.handle, args.l2_flush_mib << 20))
-            st = p.process_frame_device(frames[i].ptr, None, read_stats=True)
-            if i >= warm:
-                nvis.append(st.visible_blocks)
-                nmod.append(L.vf_last_modified_voxels(p.handle))
-        stage, nprof = p.stage_times()
-        p.close()
-        ms = stage[2] / max(nprof, 1)
-        # B = N_vis (512 sizeof(V) + 4 + 16) + N_mod sizeof(V) + W H 4 (VoxelS)
-        b = float(np.mean(nvis)) * (512 * 4 + 20) + float(np.mean(nmod)) * 4 + w * h * 4
-        gbs = b / (ms * 1e-3) / 1e9
-        kname = "k_integrate_s" if mode == 0 else "k_integrate_fast"
-        tb = ncu_kernel_bytes("r2_ncu.json", "c3_integrate_exact" if mode == 0 else "c3_integrate_fast", kname)
-        out[name] = {"kernel": kname, "achieved": gbs, "traffic": tb,
-                     "traffic_source": "profiles/r2_ncu.json (ncu --set full, same kernel at C3): dram read + write",
-                     "frac": gbs / hbm_peak, "ms_per_launch": ms, "algorithmic_bytes_per_launch": b,
-                     "visible_blocks": float(np.mean(nvis)), "voxel_visits_per_s": float(np.mean(nvis)) * 512 / (ms * 1e-3)}
-    for f in frames:
-        f.free()
+            render_synthetic(pose, Intrinsics(fx, fy, cx, cy, w, h), spheres, planes, frames[i].ptr,
+                             colours[i].ptr if rgb else None, far=far, device=device)
+        settings, calib = settings_from_config(cfg)
+        for mode, name in ((0, "exact"), (1, "fast")):
+            p = make_pipeline(replace(settings, integration_mode=mode), calib, device=device)
+            nvis, nmod = [], []
+            for i, pose in enumerate(poses):
+                if i == warm:
+                    p.set_profiling(True)
+                p.set_pose(pose)
+                _abi.check("vf_flush_l2", L.vf_flush_l2(p.handle, args.l2_flush_mib << 20))
+                st = p.process_frame_device(frames[i].ptr, colours[i].ptr if rgb else None, read_stats=True)
+                if i >= warm:
+                    nvis.append(st.visible_blocks)
+                    nmod.append(L.vf_last_modified_voxels(p.handle))
+            stage, nprof = p.stage_times()
+            p.close()
+            ms = stage[2] / max(nprof, 1)
+            # B = N_vis (512 sizeof(V) + 4 + 16) + N_mod sizeof(V) + W H 4 (+ W H 3)
+            b = (float(np.mean(nvis)) * (512 * vsize + 20) + float(np.mean(nmod)) * vsize + w * h * 4
+                 + (w * h * 3 if rgb else 0))
+            gbs = b / (ms * 1e-3) / 1e9
+            kname = ("k_integrate_rgb" if rgb else "k_integrate_s") if mode == 0 else \
+                ("k_integrate_fast_rgb" if rgb else "k_integrate_fast")
+            key = name if cname == "C3" else f"{name}_rgb"
+            entry = {"config": cname, "kernel": kname, "achieved": gbs, "frac": gbs / hbm_peak, "ms_per_launch": ms,
+                     "algorithmic_bytes_per_launch": b, "visible_blocks": float(np.mean(nvis)),
+                     "voxel_visits_per_s": float(np.mean(nvis)) * 512 / (ms * 1e-3)}
+            if cname == "C3":
+                tb = ncu_kernel_bytes("r2_ncu.json", "c3_integrate_exact" if mode == 0 else "c3_integrate_fast", kname)
+                entry.update({"traffic": tb, "traffic_source": "profiles/r2_ncu.json (ncu --set full, same kernel "
+                                                               "at C3): dram read + write"})
+            out[key] = entry
+        for f in frames + (colours or []):
+            f.free()
     return out
 
 

@@ -101,7 +101,8 @@ typedef struct vf_settings {
    *   VF_INTEGRATION_FAST (1): the same voxels, pixels and update rule with
    *     FMA-contracted camera transform, approximate reciprocals and an FMA
    *     blend; parity bar: SDF within 1 LSB of int16 and weight exact on
-   *     >= 99.9 % of voxels (SURVEY §8(c) TSDF tolerance). VoxelS only. */
+   *     >= 99.9 % of voxels (SURVEY §8(c) TSDF tolerance); VoxelSRgb: colours
+   *     within one count, colour weights exact. */
   int integration_mode;
   /* Pixel-sharded ICP (config 5): 1 = each shard sums the ICP
    * terms of 1/shard_count of the pixels and the per-iteration 29 sums are

@@ -1139,7 +1139,6 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
   }
   c->vsize = s->voxel_type == VF_VOXEL_S_RGB ? 8 : 4;
   if (s->integration_mode < VF_INTEGRATION_EXACT || s->integration_mode > VF_INTEGRATION_FAST ||
-      (s->integration_mode == VF_INTEGRATION_FAST && c->vsize != 4) ||
       s->tracker_type < VF_TRACKER_ICP || s->tracker_type > VF_TRACKER_ICP_REN ||
       (s->tracker_type == VF_TRACKER_COLOR && c->vsize != 8)) {
     // "colour tracker requires a voxel type with colour information" (pipeline_impl.hpp:55-57)

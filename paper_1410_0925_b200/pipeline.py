@@ -108,7 +108,7 @@ class EngineSettings:
     tracker_type: int = 0  # TrackerType: 0 icp, 1 color, 2 icp_ren (tracking_state.hpp:10)
     ren_sigma: float = 10.0
     skip_points: bool = False
-    integration_mode: int = 0  # 0 exact (bit-exact), 1 fast (<= 1 LSB tolerance; VoxelS)
+    integration_mode: int = 0  # 0 exact (bit-exact), 1 fast (<= 1 LSB / 1 colour count tolerance)
     shard_icp: bool = False  # pixel-sharded ICP, per-iteration sums exchanged through peer memory
     icp_max_ctas: int = 0    # cap of the ICP grid (shards sharing one device)
     tracker_exact_solve: bool = False  # colour tracker: the reference's pivoted LDLT on every step

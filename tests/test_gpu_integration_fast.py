@@ -1,5 +1,5 @@
-"""Fast integration mode (vf_settings.integration_mode = 1) against the
-oracle: the reference's voxels / pixels / update rule with FMA-contracted,
+"""Fast integration mode (vf_settings.integration_mode = 1, VoxelS and
+VoxelSRgb) against the oracle: the reference's voxels / pixels / update rule with FMA-contracted,
 approximate-reciprocal arithmetic (vf_integrate.cu, k_integrate_fast).
 
 Bar (SURVEY.md §8(c) TSDF tolerance: <= 1 LSB of int16, <= 1 count of
@@ -92,8 +92,43 @@ def test_fast_mode_tracked_sequence_close_to_exact(olib):
     pf.close()
 
 
-def test_fast_mode_rejected_for_colour_voxels():
-    from paper_1410_0925_b200._abi import VoxfuseError
-    s, c = settings_from_config(CONFIGS["C2"])
-    with pytest.raises(VoxfuseError):
-        make_pipeline(replace(s, integration_mode=1), c)
+def test_fast_integration_colour_voxels(olib):
+    """VoxelSRgb (config 2 frames, known poses) from the oracle's own volume:
+    SDF within 1 LSB and weights exact as for VoxelS; colour channels within
+    one count and colour weights exact on >= 99.9 % of the voxels either side
+    changes (the colour blend's quotient is an approximate product, and the RGB
+    camera's pixel may flip within a few ulp of a pixel edge)."""
+    cfg = CONFIGS["C2"]
+    fr = frames(olib, cfg, 7, rgb=True)
+    o = vf_py.Volume(olib, cfg, tracking=False)
+    s, c = settings_from_config(cfg)
+    p = make_pipeline(replace(s, integration_mode=1), c)
+    for i, (pose, depth, col) in enumerate(fr):
+        if i not in (0, 6):
+            o.process(depth, col, pose)
+            continue
+        p.import_state(o.entries(), o.voxels(), *_free_stacks(olib, o, cfg))
+        before = voxel_payload(o.voxels(), 8).reshape(-1, 7).astype(np.int64)
+        p.allocate(depth, pose)
+        st = vf_py.AllocStats()
+        olib.lib.vfo_stage_allocate(o.h, depth.ctypes.data_as(vf_py.C.c_void_p),
+                                    pose.ctypes.data_as(vf_py.C.c_void_p), vf_py.C.byref(st))
+        assert entries_equal(p.entries(), o.entries())
+        olib.lib.vfo_stage_integrate(o.h, depth.ctypes.data_as(vf_py.C.c_void_p),
+                                     col.ctypes.data_as(vf_py.C.c_void_p), pose.ctypes.data_as(vf_py.C.c_void_p))
+        p.integrate(depth, col, pose)
+        vo = voxel_payload(o.voxels(), 8).reshape(-1, 7).astype(np.int64)
+        vg = voxel_payload(p.voxels(), 8).reshape(-1, 7).astype(np.int64)
+        changed = (vo != before).any(1) | (vg != before).any(1)
+        sdf = lambda v: (v[:, 0] | (v[:, 1] << 8)).astype(np.uint16).view(np.int16).astype(np.int64)
+        d_sdf = np.abs(sdf(vg[changed]) - sdf(vo[changed]))
+        d_w = vg[changed, 2] != vo[changed, 2]
+        d_clr = np.abs(vg[changed, 3:6] - vo[changed, 3:6]).max(1)
+        d_wc = vg[changed, 6] != vo[changed, 6]
+        print(f"C2 frame {i}: {int(changed.sum())} voxels updated, sdf <=1 LSB {np.mean(d_sdf <= 1):.6f}, "
+              f"weight exact {1 - np.mean(d_w):.6f}, colour <=1 {np.mean(d_clr <= 1):.6f} (exact "
+              f"{np.mean(d_clr == 0):.5f}), colour weight exact {1 - np.mean(d_wc):.6f}")
+        assert np.mean(d_sdf <= 1) >= 0.999 and np.mean(d_w) <= 0.001
+        assert np.mean(d_clr <= 1) >= 0.999 and np.mean(d_wc) <= 0.001
+        olib.lib.vfo_stage_raycast(o.h, pose.ctypes.data_as(vf_py.C.c_void_p))
+    p.close()
