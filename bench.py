@@ -410,7 +410,7 @@ def run_ours(args, dist: Dist):
     def run_device(collect_stages=False):
         p = new_pipeline()
         hctx = p.handle
-        ms_frames, vis_blocks, modified = [], [], []
+        ms_frames, vis_blocks, modified, iters = [], [], [], []
         swaps.clear()
         stage = np.zeros(8)
         for i in range(n_frames):
@@ -434,6 +434,7 @@ def run_ours(args, dist: Dist):
                 st = _abi.VfFrameStats()
                 _abi.check("vf_read_stats", L.vf_read_stats(hctx, C.byref(st)))
                 vis_blocks.append(st.visible_blocks)
+                iters.append(st.tracking_iterations)
                 swaps.append((st.swapped_in, st.swapped_out, st.swap_bytes_in + st.swap_bytes_out,
                               st.allocation_dropped))
                 modified.append(L.vf_last_modified_voxels(hctx))
@@ -442,11 +443,14 @@ def run_ours(args, dist: Dist):
             stage, nprof = p.stage_times()
             stage = stage / max(nprof, 1)
             counters = p.raycast_counters()  # last frame's raycast re-run with counters (untimed)
+            if cfg.tracking and cfg.tracker == "icp":
+                run_device.icp = icp_rates(p, cfg, intr, poses, spheres, planes, far, device)
         launches = sum(p.kernel_launches_per_frame(cfg.tracking and i > 0) for i in range(args.warmup, n_frames))
         if not cfg.tracking:
             launches += n_frames - args.warmup  # k_set_pose per known-pose frame
         p.close()
         run_device.counters = counters
+        run_device.iters = float(np.mean(iters)) if iters else 0.0
         return np.array(ms_frames), np.array(vis_blocks), np.array(modified), stage, launches
 
     # --- timed pass (graphs on) ---
@@ -545,6 +549,7 @@ def run_ours(args, dist: Dist):
 
     # --- profiling pass: per-stage events (no graphs) ---
     _, vis_p, mod_p, stage_ms, _ = run_device(collect_stages=True)
+    st_iters = run_device.iters
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
@@ -600,6 +605,7 @@ def run_ours(args, dist: Dist):
         "stage_throughput": {
             "raycast_rays_per_s": npix / (stages["raycast"] * 1e-3) if stages["raycast"] > 0 else None,
             **raycast_rates(run_device.counters, stages["raycast"]),
+            **icp_throughput(getattr(run_device, "icp", None), stages["tracking"], st_iters),
             "integration_voxel_visits_per_s": nvis * 512 / (integ_ms * 1e-3) if integ_ms > 0 else None,
             "allocation_pixels_per_s": npix / (stages["allocation"] * 1e-3) if stages["allocation"] > 0 else None,
         },
@@ -634,6 +640,59 @@ def run_ours(args, dist: Dist):
                                               "reference pipeline (oracle/_ref) via process_frame"}
     if dist.rank == 0:
         print(json.dumps(line))
+
+
+def icp_rates(p, cfg, intr, poses, spheres, planes, far, device) -> dict:
+    """SURVEY.md §8(d) K4 units: one icp_track call (untimed, traced) of the
+    next frame of the trajectory against the last frame's maps --
+    iterations per level, pixel-iterations (pyramid pixels x iterations) and
+    the per-iteration phase timers of the persistent kernels."""
+    from paper_1410_0925_b200 import DeviceBuffer, render_synthetic
+    from paper_1410_0925_b200.scene import trajectory_for
+
+    nxt = trajectory_for(cfg, len(poses) + 1)[-1]
+    buf = DeviceBuffer(intr.width * intr.height * 4)
+    render_synthetic(nxt, intr, spheres, planes, buf.ptr, None, far=far, device=device)
+    d = buf.to_host(np.float32, (intr.height, intr.width))
+    buf.free()
+    r = p.icp_track(d)
+    tr = p.icp_trace()
+    if not len(tr):
+        return {}
+    levels = {}
+    w, h = intr.width, intr.height
+    sizes = []
+    for _ in range(cfg.levels):
+        sizes.append(w * h)
+        w, h = (w + 1) // 2, (h + 1) // 2
+    pix_it = 0
+    for row in tr:
+        lv = int(row[0])
+        levels[lv] = levels.get(lv, 0) + 1
+        pix_it += sizes[lv]
+    cyc = tr[:, 44:48].sum(0)
+    return {"icp_iterations_per_level": {str(k): v for k, v in sorted(levels.items(), reverse=True)},
+            "icp_pixel_iterations": int(pix_it), "icp_tracking_ok": bool(r["ok"]),
+            "icp_note": "one traced icp_track call: the trajectory's next frame against the last timed frame's maps",
+            "icp_phase_cycles": {"pixel_terms": float(cyc[0]), "barrier": float(cyc[1]), "partial_sums": float(cyc[2]),
+                                 "controller": float(cyc[3])}}
+
+
+def icp_throughput(icp, track_ms: float, iters: float) -> dict:
+    """The traced icp_track call's K4 units, plus the timed frames' solved
+    iterations.  The traced call counts every evaluation (accepted steps,
+    halvings, rejected steps); its device time comes from its phase timers
+    (SM cycles at the 1965 MHz the clocks report under load)."""
+    if not icp or track_ms <= 0:
+        return {}
+    out = dict(icp)
+    evals = sum(icp["icp_iterations_per_level"].values())
+    t = sum(icp["icp_phase_cycles"].values()) / 1.965e9
+    out["icp_evaluations"] = evals
+    out["icp_us_per_evaluation"] = 1e6 * t / max(evals, 1)
+    out["icp_pixel_evaluations_per_s"] = icp["icp_pixel_iterations"] / t if t > 0 else None
+    out["icp_solved_iterations_per_frame"] = iters  # FrameStats::tracking_iterations, timed frames
+    return out
 
 
 def raycast_rates(cnt, ray_ms: float) -> dict:
