@@ -443,6 +443,7 @@ def run_ours(args, dist: Dist):
             stage, nprof = p.stage_times()
             stage = stage / max(nprof, 1)
             counters = p.raycast_counters()  # last frame's raycast re-run with counters (untimed)
+            run_device.alloc = p.alloc_counters()  # and mark_blocks' walk
             if cfg.tracking and cfg.tracker == "icp":
                 run_device.icp = icp_rates(p, cfg, intr, poses, spheres, planes, far, device)
         launches = sum(p.kernel_launches_per_frame(cfg.tracking and i > 0) for i in range(args.warmup, n_frames))
@@ -605,6 +606,7 @@ def run_ours(args, dist: Dist):
         "stage_throughput": {
             "raycast_rays_per_s": npix / (stages["raycast"] * 1e-3) if stages["raycast"] > 0 else None,
             **raycast_rates(run_device.counters, stages["raycast"]),
+            **alloc_rates(getattr(run_device, "alloc", None), stages["allocation"]),
             **icp_throughput(getattr(run_device, "icp", None), stages["tracking"], st_iters),
             "integration_voxel_visits_per_s": nvis * 512 / (integ_ms * 1e-3) if integ_ms > 0 else None,
             "allocation_pixels_per_s": npix / (stages["allocation"] * 1e-3) if stages["allocation"] > 0 else None,
@@ -693,6 +695,16 @@ def icp_throughput(icp, track_ms: float, iters: float) -> dict:
     out["icp_pixel_evaluations_per_s"] = icp["icp_pixel_iterations"] / t if t > 0 else None
     out["icp_solved_iterations_per_frame"] = iters  # FrameStats::tracking_iterations, timed frames
     return out
+
+
+def alloc_rates(cnt, alloc_ms: float) -> dict:
+    """SURVEY.md §8(d) K1 units: mark_blocks' DDA cells (one hash-bucket probe
+    each) of the last frame, over the allocation stage's time."""
+    if not cnt or alloc_ms <= 0:
+        return {}
+    return {"allocation_cells_probed_per_frame": cnt["cells_probed"],
+            "allocation_probes_per_s": cnt["cells_probed"] / (alloc_ms * 1e-3),
+            "allocation_cells_per_depth_pixel": cnt["cells_probed"] / max(cnt["pixels"], 1)}
 
 
 def raycast_rates(cnt, ray_ms: float) -> dict:

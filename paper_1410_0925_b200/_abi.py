@@ -45,7 +45,7 @@ EXPORTS = [
     "vf_depth_pyramid", "vf_render_synthetic",
     "vf_shard_owner", "vf_shard_p2p_handles", "vf_shard_p2p_link", "vf_shard_p2p_link_local", "vf_shard_icp_handle", "vf_shard_icp_link", "vf_shard_icp_link_local", "vf_shard_nccl_unique_id", "vf_shard_attach_nccl", "vf_shard_composite_local",
     "vf_device_alloc", "vf_device_free", "vf_memcpy_h2d", "vf_memcpy_d2h", "vf_host_alloc_pinned",
-    "vf_host_free_pinned", "vf_event_record", "vf_event_elapsed_ms", "vf_set_profiling", "vf_set_stage_timing", "vf_raycast_counters", "vf_stage_times",
+    "vf_host_free_pinned", "vf_event_record", "vf_event_elapsed_ms", "vf_set_profiling", "vf_set_stage_timing", "vf_raycast_counters", "vf_alloc_counters", "vf_stage_times",
     "vf_kernel_launches_per_frame", "vf_readback_bytes", "vf_flush_l2", "vf_flush_time", "vf_last_modified_voxels",
     "vf_selftest_division",
 ]
@@ -227,6 +227,7 @@ def load() -> C.CDLL:
         "vf_set_profiling": (C.c_int, [vp, C.c_int]),
         "vf_set_stage_timing": (C.c_int, [vp, C.c_int]),
         "vf_raycast_counters": (C.c_int, [vp, C.POINTER(C.c_ulonglong)]),
+        "vf_alloc_counters": (C.c_int, [vp, C.POINTER(C.c_ulonglong)]),
         "vf_stage_times": (C.c_int, [vp, dp, C.POINTER(C.c_long)]),
         "vf_kernel_launches_per_frame": (C.c_int, [vp, C.c_int]),
         "vf_readback_bytes": (C.c_long, [vp]),

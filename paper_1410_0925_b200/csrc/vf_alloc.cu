@@ -114,16 +114,20 @@ __global__ void k_prep(const PoseD* __restrict__ pose, IntrD depth_in, IntrD rgb
 // K1a: mark_blocks (allocation.hpp:137-168).  One thread per pixel.  Every
 // CTA derives cam_to_world from the device pose itself; CTA 0 also publishes
 // the frame's camera parameters (k_prep's job) for the later kernels.
-__global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, IntrD in, const PoseD* __restrict__ pose,
-                                              IntrD rgb_in, PoseD depth_to_rgb, FrameParams* __restrict__ fp,
-                                              HashView hv, float voxel_size, float mu, ShardSpec shard,
-                                              unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
-                                              Counters* __restrict__ ctr) {
+// kCount: the measurement twin (vf_alloc_counters, never on the frame path):
+// no requests and no frame parameters written; counts {pixels with depth,
+// DDA cells probed (one bucket sector each), cells missing from the table}.
+template <bool kCount>
+__device__ __forceinline__ void mark_body(const float* __restrict__ depth, IntrD in, const PoseD* __restrict__ pose,
+                                          IntrD rgb_in, PoseD depth_to_rgb, FrameParams* __restrict__ fp,
+                                          HashView hv, float voxel_size, float mu, ShardSpec shard,
+                                          unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
+                                          Counters* __restrict__ ctr, unsigned long long* __restrict__ counts) {
   __shared__ PoseD s_c2w;
   if (threadIdx.x == 0) {
     const PoseD w2c = *pose;
     s_c2w = pose_inverse(w2c);
-    if (blockIdx.x == 0) {
+    if (!kCount && blockIdx.x == 0) {
       fp->w2c = w2c;
       fp->c2w = s_c2w;
       fp->depth_cam = make_camf(w2c, in);
@@ -137,10 +141,10 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const int x = (int)(blockIdx.x % tiles_x) * 32 + ((wq & 3) << 3) + (lane & 7);
   const int y = (int)(blockIdx.x / tiles_x) * 8 + ((wq >> 2) << 2) + (lane >> 3);
-  if (x >= in.width || y >= in.height) return;
+  unsigned n_cells = 0, n_missing = 0;
   const int pixel = y * in.width + x;
-  const float d = __ldg(depth + pixel);
-  if (d <= 0.0f) return;
+  const float d = (x < in.width && y < in.height) ? __ldg(depth + pixel) : 0.0f;
+  if (!(d <= 0.0f)) {  // (kCount: every lane reaches the reduction below)
   D3 p0, p1;
   pixel_segment(x, y, d, in, s_c2w, voxel_size, mu, p0, p1);
   if (shard.count > 1) {
@@ -158,7 +162,10 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
     bool mine = shard_owner(sbx, sby, sbz, shard) == shard.index;
     for (int k = 0; k < 27 && !mine && shard.halo; ++k)
       mine = shard_owner(sbx + k % 3 - 1, sby + (k / 3) % 3 - 1, sbz + k / 9 - 1, shard) == shard.index;
-    if (!mine) return;
+    if (!mine) {
+      if (!kCount) return;
+      n_cells = 0xFFFFFFFFu;  // not this shard's pixel: counted as such below
+    }
   }
   const unsigned long long key_base = (unsigned long long)(pixel + 1) << kStepBits;
   // a missing block: bid for its bucket (the winning key reproduces the
@@ -172,10 +179,44 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
     const unsigned long long old = atomicMax(req_key + bucket, key_base | (unsigned long long)step);
     if (old == 0ull) atomicOr(req_bits + (bucket >> 5), 1u << (bucket & 31u));
   };
-  dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
-    if (find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0) request(cx, cy, cz, step);
-    return true;
-  });
+  if (n_cells != 0xFFFFFFFFu)
+    dda_cells(p0, p1, [&](int cx, int cy, int cz, int step) {
+      const bool missing = find_entry(hv, cx, cy, cz, kEntrySwappedOut) < 0;
+      if (kCount) {
+        ++n_cells;
+        n_missing += missing ? 1u : 0u;
+      } else if (missing) {
+        request(cx, cy, cz, step);
+      }
+      return true;
+    });
+  }
+  if constexpr (kCount) {
+    const unsigned px = (!(d <= 0.0f) && n_cells != 0xFFFFFFFFu) ? 1u : 0u;
+    if (n_cells == 0xFFFFFFFFu) n_cells = 0;
+    unsigned long long v[3] = {px, n_cells, n_missing};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+      if ((threadIdx.x & 31) == 0 && v[k]) atomicAdd(counts + k, v[k]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, IntrD in, const PoseD* __restrict__ pose,
+                                              IntrD rgb_in, PoseD depth_to_rgb, FrameParams* __restrict__ fp,
+                                              HashView hv, float voxel_size, float mu, ShardSpec shard,
+                                              unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
+                                              Counters* __restrict__ ctr) {
+  mark_body<false>(depth, in, pose, rgb_in, depth_to_rgb, fp, hv, voxel_size, mu, shard, req_key, req_bits, ctr,
+                   nullptr);
+}
+
+__global__ void __launch_bounds__(256) k_mark_count(const float* __restrict__ depth, IntrD in,
+                                                    const PoseD* __restrict__ pose, HashView hv, float voxel_size,
+                                                    float mu, ShardSpec shard, unsigned long long* __restrict__ counts) {
+  mark_body<true>(depth, in, pose, in, PoseD{}, nullptr, hv, voxel_size, mu, shard, nullptr, nullptr, nullptr, counts);
 }
 
 // Recover the block position a request key points at by re-walking that

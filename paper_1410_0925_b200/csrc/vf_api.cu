@@ -2039,6 +2039,23 @@ int vf_set_profiling(vf_ctx* c, int enabled) {
   c->profiled_frames = 0;
   return VF_OK;
 }
+int vf_alloc_counters(vf_ctx* c, unsigned long long* out) {
+  if (!c || !out) return VF_ERR_INVALID;
+  if (!c->maps_valid) {
+    c->err = "vf_alloc_counters: no frame processed yet";
+    return VF_ERR_STATE;
+  }
+  unsigned long long* d = nullptr;
+  VF_CUDA(c, cudaMallocAsync(reinterpret_cast<void**>(&d), 3 * sizeof(unsigned long long), c->stream));
+  VF_CUDA(c, cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), c->stream));
+  k_mark_count<<<mark_grid(c), 256, 0, c->stream>>>(c->depth, c->din, &c->dstate->pose, hash_view(c),
+                                                    c->s.voxel_size, c->s.mu, c->shard, d);
+  VF_CUDA(c, cudaGetLastError());
+  VF_CUDA(c, cudaMemcpyAsync(out, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  VF_CUDA(c, cudaFreeAsync(d, c->stream));
+  VF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return VF_OK;
+}
 int vf_raycast_counters(vf_ctx* c, unsigned long long* out) {
   if (!c || !out) return VF_ERR_INVALID;
   if (!c->maps_valid) {

@@ -91,6 +91,8 @@ __host__ __device__ inline int shard_owner(int bx, int by, int bz, const ShardSp
   return (int)(h % (uint32_t)sp.count);
 }
 
+__global__ void k_mark_count(const float* depth, IntrD in, const PoseD* pose, HashView hv, float voxel_size, float mu,
+                             ShardSpec shard, unsigned long long* counts);
 __global__ void k_mark(const float* depth, IntrD in, const PoseD* pose, IntrD rgb_in, PoseD depth_to_rgb,
                        FrameParams* fp, HashView hv, float voxel_size, float mu, ShardSpec shard,
                        unsigned long long* req_key, uint32_t* req_bits, Counters* ctr);

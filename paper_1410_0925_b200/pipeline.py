@@ -540,6 +540,12 @@ class Pipeline:
         self._chk("vf_raycast_counters", self._L.vf_raycast_counters(self._h, out))
         return {"table_probes": out[0], "voxel_reads": out[1], "rays": out[2], "hits": out[3]}
 
+    def alloc_counters(self) -> dict:
+        """mark_blocks' DDA walk over the last frame without requests (measurement only)."""
+        out = (C.c_ulonglong * 3)()
+        self._chk("vf_alloc_counters", self._L.vf_alloc_counters(self._h, out))
+        return {"pixels": out[0], "cells_probed": out[1], "cells_missing": out[2]}
+
     def set_stage_timing(self, enabled: bool) -> None:
         """Fill FrameStats.ms_tracking .. ms_raycast on every blocking frame
         (pipeline.hpp:56-57) from event records inside the frame graph."""

@@ -224,3 +224,25 @@ def test_raycast_counters_rerun_is_identical():
     assert 0 < cnt["rays"] <= p.width * p.height
     assert 0 < cnt["table_probes"] < cnt["voxel_reads"]
     p.close()
+
+
+def test_alloc_counters_do_not_touch_the_volume():
+    """vf_alloc_counters walks mark_blocks' DDA without requests: the table
+    is unchanged, every pixel with depth is counted, and after the frame no
+    cell is missing (nothing was dropped)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import vf_py
+    from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, trajectory
+    s, c = settings_from_config(CONFIGS["C1"])
+    p = make_pipeline(s, c)
+    olib = vf_py.oracle_lib()
+    d = vf_py.render_depth(olib, CONFIGS["C1"], trajectory(1)[0], BOX_ROOM_SPHERES, BOX_ROOM_PLANES)
+    st = p.process_frame(None, d)
+    e0 = p.entries()
+    cnt = p.alloc_counters()
+    assert np.array_equal(p.entries(), e0)
+    assert cnt["pixels"] == int((d > 0).sum())
+    assert cnt["cells_probed"] >= cnt["pixels"] and cnt["cells_missing"] == st.allocation_dropped == 0
+    p.close()
