@@ -376,7 +376,8 @@ int vf_raycast_counters(vf_ctx* ctx, unsigned long long* out /* 4 */);
 /* Measurement only: mark_blocks' walk (allocation.hpp:137-168) over the last
  * frame's depth and pose, without requests: {pixels with depth, DDA cells
  * probed (one hash-bucket read each), cells still missing from the table
- * (after the frame: the dropped requests)}. */
+ * (after the frame: blocks whose bucket already took this frame's one
+ * request, allocation.hpp:155-159, and dropped requests)}. */
 int vf_alloc_counters(vf_ctx* ctx, unsigned long long* out /* 3 */);
 int vf_kernel_launches_per_frame(vf_ctx* ctx, int tracking_frame);
 /* Bytes of the per-frame stats readback (the D2H of vf_process_frame). */

@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "vf_device.cuh"
 #include "vf_kernels.h"
@@ -194,7 +195,9 @@ struct NcclApi {
 NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
+    // one already in the process (PyTorch's) first, then VF_NCCL_LIB, then the system's
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h && std::getenv("VF_NCCL_LIB")) h = dlopen(std::getenv("VF_NCCL_LIB"), RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("/usr/lib/x86_64-linux-gnu/libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return a;

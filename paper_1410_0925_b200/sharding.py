@@ -119,9 +119,18 @@ class LocalShardGroup:
             s.close()
 
 
+def _load_torch_nccl() -> None:
+    """The library dlopens libnccl.so.2 on first use and reuses one already
+    loaded.  In a Python process that is PyTorch's (its own, newer build):
+    import torch first, or the system library the C side would otherwise load
+    shadows it and a later `import torch` fails on missing NCCL symbols."""
+    import torch  # noqa: F401  (loads libtorch_cuda and its libnccl.so.2)
+
+
 def share_nccl_id(rank: int, dist) -> bytes:
     """Rank 0 creates the NCCL unique id (vf_shard_nccl_unique_id, no GPU
     needed) and every rank receives it over the host process group."""
+    _load_torch_nccl()
     L = _abi.load()
     buf = (C.c_uint8 * 128)()
     if rank == 0:

@@ -228,8 +228,10 @@ def test_raycast_counters_rerun_is_identical():
 
 def test_alloc_counters_do_not_touch_the_volume():
     """vf_alloc_counters walks mark_blocks' DDA without requests: the table
-    is unchanged, every pixel with depth is counted, and after the frame no
-    cell is missing (nothing was dropped)."""
+    is unchanged and every pixel with depth is counted.  Cells can still be
+    missing after the frame: a bucket takes one request per frame
+    (allocation.hpp:155-159), so colliding blocks wait for a later frame --
+    and the same walk after a second identical frame finds fewer."""
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
@@ -244,5 +246,8 @@ def test_alloc_counters_do_not_touch_the_volume():
     cnt = p.alloc_counters()
     assert np.array_equal(p.entries(), e0)
     assert cnt["pixels"] == int((d > 0).sum())
-    assert cnt["cells_probed"] >= cnt["pixels"] and cnt["cells_missing"] == st.allocation_dropped == 0
+    assert cnt["cells_probed"] >= cnt["pixels"] and 0 < cnt["cells_missing"] < cnt["cells_probed"]
+    assert st.allocation_dropped == 0
+    p.process_frame(None, d)
+    assert p.alloc_counters()["cells_missing"] < cnt["cells_missing"]
     p.close()

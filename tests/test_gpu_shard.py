@@ -117,6 +117,8 @@ def test_owner_rule_matches_device():
 def test_nccl_composite_plumbing_single_rank(olib):
     """NCCL path with one rank: unique id, communicator, collectives captured
     in the frame graph; with one rank the composite must be the identity."""
+    from paper_1410_0925_b200.sharding import _load_torch_nccl
+    _load_torch_nccl()  # the NCCL the library finds loaded is then PyTorch's own
     L = _abi.load()
     cfg = CONFIGS["T320"].with_(tracking=False)
     s, c = settings_from_config(cfg)
