@@ -88,6 +88,9 @@ namespace {
 #endif
 constexpr int kRayThreads = 128;
 constexpr int kCacheWays = 8;
+#ifndef VF_RAY_SPLIT
+#define VF_RAY_SPLIT 0
+#endif
 
 __device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { return find_slot(hv, x, y, z); }
 
@@ -308,10 +311,17 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
     smp.init();
     F3 hw;
     if (march(smp, start, dir, total, mu / vs, vs, hw)) {
-      F3 n;
-      if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
-        out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
-        out_n = make_float4(n.x, n.y, n.z, 1.0f);
+#if VF_RAY_SPLIT
+      if (!kCount) {
+        out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);  // the normal follows in k_ray_normals
+      } else
+#endif
+      {
+        F3 n;
+        if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
+          out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
+          out_n = make_float4(n.x, n.y, n.z, 1.0f);
+        }
       }
     }
     if constexpr (kCount) {
@@ -335,6 +345,42 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
   else
     raycast_body<2>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
 }
+
+#if VF_RAY_SPLIT
+// Split raycast: the normals of all hits in a second pass, with full warps
+// (in the fused kernel each ray's normal runs when its own march ends, under
+// divergence).  Same pixel tiling as k_raycast; a failed normal clears the
+// hit, as render_maps does (raycast.hpp:427-431).
+__global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
+    k_ray_normals(HashView hv, const uint32_t* __restrict__ vox, int vstride, IntrD in, float vs,
+                  float4* __restrict__ points, float4* __restrict__ normals) {
+  __shared__ int4 s_cache[kCacheWays * kRayThreads];
+  const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int x = fxi * kFragmentSize + (lane & 7) + ((wq & 1) << 3);
+  const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (lane >> 3) + ((wq >> 1) << 2);
+  if (x >= in.width || y >= in.height) return;
+  const size_t pix = (size_t)y * in.width + x;
+  const float4 p = points[pix];
+  if (p.w == 0.0f) return;
+  F3 n;
+  bool ok;
+  if (vstride == 1) {
+    Sampler<1> smp{hv, vox, s_cache + threadIdx.x};
+    smp.init();
+    ok = smp.normal(F3{p.x / vs, p.y / vs, p.z / vs}, n);
+  } else {
+    Sampler<2> smp{hv, vox, s_cache + threadIdx.x};
+    smp.init();
+    ok = smp.normal(F3{p.x / vs, p.y / vs, p.z / vs}, n);
+  }
+  if (ok) {
+    normals[pix] = make_float4(n.x, n.y, n.z, 1.0f);
+  } else {
+    points[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+#endif
 
 // Measurement twin of k_raycast (vf_raycast_counters, never on the frame
 // path): same maps, plus counters {table probes, voxel reads, rays, hits}.
