@@ -578,7 +578,7 @@ def run_ours(args, dist: Dist):
     # capture's DRAM bytes per launch over this run's event-timed stage: shows
     # how far from memory-bound they are (C1 only; the capture is C1's).
     if args.config == "C1":
-        stage_kernels = {"raycast": ("k_raycast",), "tracking": ("k_pyramid", "k_icp_cluster", "k_icp")}
+        stage_kernels = {"raycast": ("k_raycast", "k_ray_normals"), "tracking": ("k_pyramid", "k_icp_cluster", "k_icp")}
         rows = {}
         for stage, kernels in stage_kernels.items():
             b = sum((ncu_kernel_bytes("r2_ncu.json", "c1_full", k) or 0.0) for k in kernels)

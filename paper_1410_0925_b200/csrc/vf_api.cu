@@ -467,10 +467,8 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
   const uint32_t* vox = reinterpret_cast<const uint32_t*>(c->voxels);
   k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->ranges, &c->dstate->fp,
                                                              c->din, s.voxel_size, s.mu, c->points, c->normals);
-#if VF_RAY_SPLIT
   k_ray_normals<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->din, s.voxel_size,
                                                                  c->points, c->normals);
-#endif
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
 }
@@ -633,7 +631,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   }
   if (int rc = launch_raycast(c, st)) return rc;
   VF_LAUNCHED(c, "k_raycast");
-  launches += 2;
+  launches += 3;  // k_ranges, k_raycast, k_ray_normals
   if (c->p2p_linked > 1) {  // nearest-depth composite over peer memory (vf_shard.cu)
     const int blocks = (c->npix + 255) / 256;
     k_shard_keys<<<blocks, 256, 0, st>>>(c->points, &c->dstate->fp, c->npix, c->shard.index, c->shard_keys);
@@ -2362,7 +2360,7 @@ int vf_kernel_launches_per_frame(vf_ctx* c, int tracking_frame) {
         track = (L > 1 ? 1 : 0) + icp;
     }
   }
-  return 7 + track + (c->p2p_linked > 1 ? 6 : c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 4 : 0);
+  return 8 + track + (c->p2p_linked > 1 ? 6 : c->nccl_comm ? 2 : 0) + (c->vsize == 8 ? 1 : 0) + (c->swapping ? 4 : 0);
 }
 
 }  // extern "C"

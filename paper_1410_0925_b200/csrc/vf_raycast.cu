@@ -88,9 +88,7 @@ namespace {
 #endif
 constexpr int kRayThreads = 128;
 constexpr int kCacheWays = 8;
-#ifndef VF_RAY_SPLIT
-#define VF_RAY_SPLIT 0
-#endif
+
 
 __device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { return find_slot(hv, x, y, z); }
 
@@ -311,12 +309,9 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
     smp.init();
     F3 hw;
     if (march(smp, start, dir, total, mu / vs, vs, hw)) {
-#if VF_RAY_SPLIT
       if (!kCount) {
         out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);  // the normal follows in k_ray_normals
-      } else
-#endif
-      {
+      } else {
         F3 n;
         if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
           out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);
@@ -346,11 +341,12 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     raycast_body<2>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
 }
 
-#if VF_RAY_SPLIT
-// Split raycast: the normals of all hits in a second pass, with full warps
-// (in the fused kernel each ray's normal runs when its own march ends, under
-// divergence).  Same pixel tiling as k_raycast; a failed normal clears the
-// hit, as render_maps does (raycast.hpp:427-431).
+// K3b second pass: the normals of all hits (sdf_surface_normal, the 48-read
+// stencil) with full warps -- in one fused kernel each ray's normal ran when
+// its own march ended, with the warp's other lanes idle or still marching
+// (C1 raycast 0.204 -> 0.178 ms, C3 0.584 -> 0.524 ms).  Same pixel tiling
+// as k_raycast; the hit is re-read in metres and divided by vs as before, and
+// a failed normal clears the hit, as render_maps does (raycast.hpp:427-431).
 __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     k_ray_normals(HashView hv, const uint32_t* __restrict__ vox, int vstride, IntrD in, float vs,
                   float4* __restrict__ points, float4* __restrict__ normals) {
@@ -380,7 +376,6 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     points[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
-#endif
 
 // Measurement twin of k_raycast (vf_raycast_counters, never on the frame
 // path): same maps, plus counters {table probes, voxel reads, rays, hits}.
