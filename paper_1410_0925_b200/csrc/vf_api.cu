@@ -467,8 +467,9 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
   const uint32_t* vox = reinterpret_cast<const uint32_t*>(c->voxels);
   k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->ranges, &c->dstate->fp,
                                                              c->din, s.voxel_size, s.mu, c->points, c->normals);
-  k_ray_normals<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->din, s.voxel_size,
-                                                                 c->points, c->normals);
+  k_ray_normals<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->ranges,
+                                                                 &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points,
+                                                                 c->normals);
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
 }

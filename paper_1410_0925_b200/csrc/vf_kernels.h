@@ -121,8 +121,8 @@ __global__ void k_ranges(const HashEntry* entries, const int* visible_list, cons
                          int frag_w);
 __global__ void k_raycast(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
                           IntrD in, float vs, float mu, float4* points, float4* normals);
-__global__ void k_ray_normals(HashView hv, const uint32_t* vox, int vstride, IntrD in, float vs, float4* points,
-                              float4* normals);
+__global__ void k_ray_normals(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
+                              IntrD in, float vs, float mu, float4* points, float4* normals);
 __global__ void k_raycast_count(HashView hv, const uint32_t* vox, int vstride, const float2* ranges,
                                 const FrameParams* fp, IntrD in, float vs, float mu, float4* points, float4* normals,
                                 unsigned long long* counters);

@@ -88,6 +88,12 @@ namespace {
 #endif
 constexpr int kRayThreads = 128;
 constexpr int kCacheWays = 8;
+// 1: the march ends at the zero-crossing bracket and the two refinement
+// steps run in k_ray_normals too, with full warps (C1 raycast 0.180 ->
+// 0.176 ms, C3 0.528 -> 0.515); 0: refinement inside the march.
+#ifndef VF_RAY_REFINE_SPLIT
+#define VF_RAY_REFINE_SPLIT 1
+#endif
 
 
 __device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { return find_slot(hv, x, y, z); }
@@ -196,7 +202,32 @@ struct Sampler : SamplerCounts<kCount> {
 
 // cast_ray (raycast.hpp:171-263) from the ray's start point and unit
 // direction in voxel units.  Returns the hit in metres.
+// The zero-crossing refinement (two trilinear secant / Newton steps) and the
+// hit, from the bracket the march ends on: in the normals pass
+// (VF_RAY_REFINE_SPLIT = 1, default) or in the march kernel.
 template <typename TSampler>
+__device__ __forceinline__ F3 refine_hit(TSampler& smp, F3 start, F3 dir, float t, float sdf, float mu_vox, float vs) {
+  float t_back = t, sdf_back = sdf;
+#pragma unroll 1
+  for (int i = 0; i < 2; ++i) {
+    const float tri = smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t});
+    if (tri != tri) break;
+    const float denom = sdf_back - tri;
+    if (fabsf(denom) > 1e-12f && fabsf(t_back - t) > 1e-6f) {
+      const float slope = denom / (t_back - t);
+      t_back = t;
+      sdf_back = tri;
+      t -= tri / (fabsf(slope) > 1e-6f ? slope : 1.0f / mu_vox);
+    } else {
+      t += tri * mu_vox;
+    }
+  }
+  const F3 h{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
+  return F3{h.x * vs, h.y * vs, h.z * vs};
+}
+
+// kDefer: stop at the bracket and return it as hw = (t, sdf, 0).
+template <bool kDefer = false, typename TSampler>
 __device__ __forceinline__ bool march(TSampler& smp, F3 start, F3 dir, float total, float mu_vox, float vs, F3& hw) {
   const float fine_step = (8.0f < mu_vox) ? 8.0f : mu_vox;
   int state = 0;  // 0 coarse, 1 fine, 2 surface
@@ -235,23 +266,11 @@ __device__ __forceinline__ bool march(TSampler& smp, F3 start, F3 dir, float tot
       } else {
         t += sdf * mu_vox;
       }
-      float t_back = t, sdf_back = sdf;
-#pragma unroll 1
-      for (int i = 0; i < 2; ++i) {
-        const float tri = smp.trilinear(F3{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t});
-        if (tri != tri) break;
-        const float denom = sdf_back - tri;
-        if (fabsf(denom) > 1e-12f && fabsf(t_back - t) > 1e-6f) {
-          const float slope = denom / (t_back - t);
-          t_back = t;
-          sdf_back = tri;
-          t -= tri / (fabsf(slope) > 1e-6f ? slope : 1.0f / mu_vox);
-        } else {
-          t += tri * mu_vox;
-        }
+      if (kDefer) {
+        hw = F3{t, sdf, 0.0f};
+      } else {
+        hw = refine_hit(smp, start, dir, t, sdf, mu_vox, vs);
       }
-      const F3 h{start.x + dir.x * t, start.y + dir.y * t, start.z + dir.z * t};
-      hw = F3{h.x * vs, h.y * vs, h.z * vs};
       return true;
     }
     t_front = t;
@@ -264,6 +283,24 @@ __device__ __forceinline__ bool march(TSampler& smp, F3 start, F3 dir, float tot
 }
 
 }  // namespace
+
+// cast_ray's ray (raycast.hpp:176-198): start and end of the fragment's range
+// in voxel units (FP64 -> float), the direction not yet normalised.
+__device__ __forceinline__ void ray_setup(int x, int y, float2 range, const FrameParams* __restrict__ fp,
+                                          const IntrD& in, float vs, F3& start, F3& dir, float& total) {
+  if (range.x <= range.y) {  // RangeImage::valid
+    const PoseD& c2w = fp->c2w;
+    const double inv_vox = 1.0 / (double)vs;
+    const double dx = (x - in.cx) / in.fx, dy = (y - in.cy) / in.fy;
+    const double r0 = range.x, r1 = range.y;
+    const D3 s0 = apply(c2w, mk(dx * r0, dy * r0, 1.0 * r0));
+    const D3 e0 = apply(c2w, mk(dx * r1, dy * r1, 1.0 * r1));
+    start = F3{(float)(s0.x * inv_vox), (float)(s0.y * inv_vox), (float)(s0.z * inv_vox)};
+    const F3 end{(float)(e0.x * inv_vox), (float)(e0.y * inv_vox), (float)(e0.z * inv_vox)};
+    dir = F3{end.x - start.x, end.y - start.y, end.z - start.z};
+    total = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
+  }
+}
 
 // K3b: render_maps (raycast.hpp:415-435).  128-thread CTAs cover half a
 // 16x16 fragment (16 x 8 pixels), so every CTA reads one range.
@@ -290,27 +327,21 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
   const float2 range = __ldg(ranges + fyi * gridDim.x + fxi);
   F3 start, dir;
   float total = 0.0f;
-  if (range.x <= range.y) {  // RangeImage::valid
-    const PoseD& c2w = fp->c2w;
-    const double inv_vox = 1.0 / (double)vs;
-    const double dx = (x - in.cx) / in.fx, dy = (y - in.cy) / in.fy;
-    const double r0 = range.x, r1 = range.y;
-    const D3 s0 = apply(c2w, mk(dx * r0, dy * r0, 1.0 * r0));
-    const D3 e0 = apply(c2w, mk(dx * r1, dy * r1, 1.0 * r1));
-    start = F3{(float)(s0.x * inv_vox), (float)(s0.y * inv_vox), (float)(s0.z * inv_vox)};
-    const F3 end{(float)(e0.x * inv_vox), (float)(e0.y * inv_vox), (float)(e0.z * inv_vox)};
-    dir = F3{end.x - start.x, end.y - start.y, end.z - start.z};
-    total = sqrtf(dir.x * dir.x + dir.y * dir.y + dir.z * dir.z);
-  }
+  ray_setup(x, y, range, fp, in, vs, start, dir, total);
   float4 out_p = make_float4(0.f, 0.f, 0.f, 0.f), out_n = make_float4(0.f, 0.f, 0.f, 0.f);
   if (total > 0) {
     dir = F3{dir.x / total, dir.y / total, dir.z / total};
     Sampler<kStride, kCount> smp{hv, vox, s_cache + threadIdx.x};
     smp.init();
     F3 hw;
-    if (march(smp, start, dir, total, mu / vs, vs, hw)) {
+    if (march<VF_RAY_REFINE_SPLIT && !kCount>(smp, start, dir, total, mu / vs, vs, hw)) {
       if (!kCount) {
-        out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);  // the normal follows in k_ray_normals
+        if (VF_RAY_REFINE_SPLIT) {  // the bracket (t, sdf): refinement, hit and normal in k_ray_normals
+          out_p = make_float4(0.f, 0.f, 0.f, 2.0f);
+          out_n = make_float4(hw.x, hw.y, 0.f, 0.f);
+        } else {
+          out_p = make_float4(hw.x, hw.y, hw.z, 1.0f);  // the normal follows in k_ray_normals
+        }
       } else {
         F3 n;
         if (smp.normal(F3{hw.x / vs, hw.y / vs, hw.z / vs}, n)) {
@@ -341,15 +372,48 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     raycast_body<2>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
 }
 
-// K3b second pass: the normals of all hits (sdf_surface_normal, the 48-read
-// stencil) with full warps -- in one fused kernel each ray's normal ran when
-// its own march ended, with the warp's other lanes idle or still marching
-// (C1 raycast 0.204 -> 0.178 ms, C3 0.584 -> 0.524 ms).  Same pixel tiling
-// as k_raycast; the hit is re-read in metres and divided by vs as before, and
-// a failed normal clears the hit, as render_maps does (raycast.hpp:427-431).
+// K3b second pass: the zero-crossing refinement and the normal of every hit
+// (sdf_surface_normal, the 48-read stencil) with full warps -- in one fused
+// kernel each ray's refinement and normal ran when its own march ended, with
+// the warp's other lanes idle or still marching (C1 raycast 0.204 -> 0.176
+// ms, C3 0.584 -> 0.515 ms).  Same pixel tiling as k_raycast; the march
+// leaves the bracket (t, sdf) in the normal map and a marker in the point map;
+// the ray is set up again exactly as cast_ray does, the hit is formed in
+// metres and divided by vs for the normal as before, and a failed normal
+// clears the hit, as render_maps does (raycast.hpp:427-431).
+template <int kStride>
+__device__ __forceinline__ void ray_normal_body(const HashView& hv, const uint32_t* __restrict__ vox,
+                                                float2 range, const FrameParams* __restrict__ fp,
+                                                const IntrD& in, float vs, float mu, int x, int y, size_t pix,
+                                                float4* __restrict__ points, float4* __restrict__ normals,
+                                                int4* s_cache) {
+  float4 p = points[pix];
+  if (p.w == 0.0f) return;
+  Sampler<kStride> smp{hv, vox, s_cache + threadIdx.x};
+  smp.init();
+  if (p.w == 2.0f) {  // deferred: refine the bracket (t, sdf) the march ended on
+    const float4 b = normals[pix];
+    F3 start{0, 0, 0}, dir{0, 0, 0};
+    float total = 0.0f;
+    ray_setup(x, y, range, fp, in, vs, start, dir, total);
+    dir = F3{dir.x / total, dir.y / total, dir.z / total};
+    const F3 hw = refine_hit(smp, start, dir, b.x, b.y, mu / vs, vs);
+    p = make_float4(hw.x, hw.y, hw.z, 1.0f);
+  }
+  F3 n;
+  if (smp.normal(F3{p.x / vs, p.y / vs, p.z / vs}, n)) {
+    points[pix] = p;
+    normals[pix] = make_float4(n.x, n.y, n.z, 1.0f);
+  } else {
+    points[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
+    normals[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
-    k_ray_normals(HashView hv, const uint32_t* __restrict__ vox, int vstride, IntrD in, float vs,
-                  float4* __restrict__ points, float4* __restrict__ normals) {
+    k_ray_normals(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
+                  const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
+                  float4* __restrict__ normals) {
   __shared__ int4 s_cache[kCacheWays * kRayThreads];
   const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
@@ -357,24 +421,11 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
   const int y = fyi * kFragmentSize + ((blockIdx.y & 1) << 3) + (lane >> 3) + ((wq >> 1) << 2);
   if (x >= in.width || y >= in.height) return;
   const size_t pix = (size_t)y * in.width + x;
-  const float4 p = points[pix];
-  if (p.w == 0.0f) return;
-  F3 n;
-  bool ok;
-  if (vstride == 1) {
-    Sampler<1> smp{hv, vox, s_cache + threadIdx.x};
-    smp.init();
-    ok = smp.normal(F3{p.x / vs, p.y / vs, p.z / vs}, n);
-  } else {
-    Sampler<2> smp{hv, vox, s_cache + threadIdx.x};
-    smp.init();
-    ok = smp.normal(F3{p.x / vs, p.y / vs, p.z / vs}, n);
-  }
-  if (ok) {
-    normals[pix] = make_float4(n.x, n.y, n.z, 1.0f);
-  } else {
-    points[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  const float2 range = VF_RAY_REFINE_SPLIT ? __ldg(ranges + fyi * gridDim.x + fxi) : make_float2(0.f, 0.f);
+  if (vstride == 1)
+    ray_normal_body<1>(hv, vox, range, fp, in, vs, mu, x, y, pix, points, normals, s_cache);
+  else
+    ray_normal_body<2>(hv, vox, range, fp, in, vs, mu, x, y, pix, points, normals, s_cache);
 }
 
 // Measurement twin of k_raycast (vf_raycast_counters, never on the frame
