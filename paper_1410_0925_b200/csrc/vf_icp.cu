@@ -557,8 +557,15 @@ __device__ __forceinline__ void icp_body(const IcpArgs& a) {
         cluster.sync();
         t2 = timer ? clock64() : 0;
         if (tid < kAcc) {  // every CTA sums the cluster's partials in rank order
+          // all remote loads issued before the first add (<= 16 CTAs per cluster)
+          const unsigned nb = cluster.num_blocks();
+          double v[16];
+#pragma unroll
+          for (unsigned r = 0; r < 16; ++r) v[r] = r < nb ? cluster.map_shared_rank(&s_part[buf][0], r)[tid] : 0.0;
           double t = 0;
-          for (unsigned r = 0; r < cluster.num_blocks(); ++r) t += cluster.map_shared_rank(&s_part[buf][0], r)[tid];
+#pragma unroll
+          for (unsigned r = 0; r < 16; ++r)
+            if (r < nb) t += v[r];
           s_tot[tid] = t;
         }
         buf ^= 1;

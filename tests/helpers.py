@@ -19,6 +19,14 @@ def frames(olib, cfg, n, rgb=False, amplitude=1.0):
     return out
 
 
+def far_pose(pose, offset=(150.3, -80.7, 230.1)):
+    """The same view with the world shifted: camera centre c -> c + offset,
+    so t -> t - R offset (world-to-camera, scene.trajectory)."""
+    q = np.array(pose, dtype=np.float64).copy()
+    q[9:] = q[9:] - q[:9].reshape(3, 3) @ np.asarray(offset)
+    return q
+
+
 def entries_equal(a, b):
     return all(np.array_equal(a[f], b[f]) for f in ENTRY_FIELDS)
 

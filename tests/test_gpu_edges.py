@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import vf_py
-from helpers import centre_dist, entries_equal, frames, rot_angle, voxel_payload
+from helpers import centre_dist, entries_equal, far_pose, frames, rot_angle, voxel_payload
 from paper_1410_0925_b200 import make_pipeline, settings_from_config
 from paper_1410_0925_b200.scene import BOX_ROOM_PLANES, BOX_ROOM_SPHERES, CONFIGS, HashConfig, trajectory
 
@@ -143,4 +143,23 @@ def test_scene_and_hash_parameters(olib, variant):
         so = o.process(d, col, pose)
         assert (st.blocks_allocated, st.visible_blocks) == (so.blocks_allocated, so.visible_blocks)
         _same_state(p, o, vsize)
+    p.close()
+
+
+def test_far_from_origin_bit_exact(olib):
+    """Integration skips the per-voxel border compares on blocks whose worst
+    corner clears every image bound by a margin that grows with the
+    coordinates (block_interior, vf_integrate.cu).  ~300 m from the origin the
+    float camera coordinates carry ~1e-5 m of rounding; the known-pose
+    sequence must still be bit-exact against the oracle."""
+    cfg = CONFIGS["T320"].with_(tracking=False)
+    p, o = _pair(olib, cfg, False)
+    for pose, depth, _ in frames(olib, cfg, 3):
+        q = far_pose(pose)
+        p.set_pose(q)
+        st = p.process_frame(None, depth)
+        so = o.process(depth, None, q)
+        assert (st.blocks_allocated, st.visible_blocks) == (so.blocks_allocated, so.visible_blocks)
+        assert st.visible_blocks > 100
+        _same_state(p, o)
     p.close()

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import vf_py
-from helpers import entries_equal, frames, voxel_payload
+from helpers import entries_equal, far_pose, frames, voxel_payload
 from paper_1410_0925_b200 import make_pipeline, settings_from_config
 from paper_1410_0925_b200.scene import CONFIGS
 
@@ -35,10 +35,15 @@ def _sdf_w(v):
     return v[:, :2].copy().view(np.int16)[:, 0].astype(np.int64), v[:, 2].astype(np.int64)
 
 
-@pytest.mark.parametrize("name,checked", [("T320", (0, 2, 4)), ("C1", (0, 6, 12))])
-def test_fast_integration_within_one_lsb(olib, name, checked):
+@pytest.mark.parametrize("name,checked,far", [("T320", (0, 2, 4), False), ("C1", (0, 6, 12), False),
+                                              ("T320", (0, 2), True)])
+def test_fast_integration_within_one_lsb(olib, name, checked, far):
+    """far: the same frames ~300 m from the origin (helpers.far_pose),
+    where block_interior's rounding allowance is largest."""
     cfg = CONFIGS[name].with_(tracking=False)
     fr = frames(olib, cfg, max(checked) + 1)
+    if far:
+        fr = [(far_pose(pose), d, c) for pose, d, c in fr]
     o = vf_py.Volume(olib, cfg, tracking=False)
     s, c = settings_from_config(cfg)
     p = make_pipeline(replace(s, integration_mode=1), c)
