@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(256) k_mark(const float* __restrict__ depth, I
                                               HashView hv, float voxel_size, float mu, ShardSpec shard,
                                               unsigned long long* __restrict__ req_key, uint32_t* __restrict__ req_bits,
                                               Counters* __restrict__ ctr) {
+  pdl_enter();
   mark_body<false>(depth, in, pose, rgb_in, depth_to_rgb, fp, hv, voxel_size, mu, shard, req_key, req_bits, ctr,
                    nullptr);
 }
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_alloc_compact(uint32_t* __r
                                                                    unsigned long long* scan, AllocMeta* __restrict__ meta,
                                                                    Counters* __restrict__ ctr,
                                                                    float2* __restrict__ ranges, int n_frag) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ int s_warp[kCompactThreads / 32];
   __shared__ unsigned s_base_req, s_base_ex;
@@ -388,6 +390,7 @@ __global__ void __launch_bounds__(256) k_alloc_apply(const float* __restrict__ d
                                                      const AllocMeta* __restrict__ meta, int* __restrict__ vba_slots,
                                                      int* __restrict__ excess_slots, int* __restrict__ alloc_list,
                                                      int alloc_cap, Counters* __restrict__ ctr) {
+  pdl_enter();
   const AllocMeta m = *meta;
   const PoseD c2w = fp->c2w;
   if (!m.slow) {
@@ -530,6 +533,7 @@ __global__ void __launch_bounds__(256) k_visible(const HashEntry* __restrict__ e
                                                  const FrameParams* __restrict__ fp, IntrD in, float vs, float near_clip,
                                                  float far_clip, int margin, int* __restrict__ visible_list,
                                                  Counters* __restrict__ ctr) {
+  pdl_enter();
   __shared__ PoseD s_w2c;
   if (threadIdx.x < sizeof(PoseD) / sizeof(double))
     reinterpret_cast<double*>(&s_w2c)[threadIdx.x] = reinterpret_cast<const double*>(&fp->w2c)[threadIdx.x];

@@ -203,6 +203,17 @@ struct vf_ctx {
     }                                                                                       \
   } while (0)
 
+// Programmatic dependent launch between the frame's consecutive main-stream
+// kernels (launch_pdl, vf_kernels.h): each kernel's launch and prologue
+// overlap its predecessor's tail.  VF_PDL=0 turns it off (A/B runs).
+bool vf::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VF_PDL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 namespace {
 
 HashView hash_view(vf_ctx* c) { return HashView{c->entries, c->mask, c->s.bucket_size, c->ordered}; }
@@ -279,13 +290,15 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
     cfg.blockDim = dim3(kIcpThreads);
     cfg.dynamicSmemBytes = c->icp_smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = c->icp_cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     VF_CUDA(c, cudaLaunchKernelEx(&cfg, k_icp_cluster, ac));
     if (ac.is_last) return VF_OK;
   }
@@ -298,11 +311,13 @@ int launch_icp(vf_ctx* c, cudaStream_t st, bool with_initial = false, bool updat
   cfg.blockDim = dim3(kIcpThreads);
   cfg.dynamicSmemBytes = c->icp_smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   VF_CUDA(c, cudaLaunchKernelEx(&cfg, k_icp, a));
   return VF_OK;
 }
@@ -440,8 +455,8 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
     return enqueue_color(c, st, explicit_init, update_state, launches);
   }
   if (s.hierarchy_levels > 1) {
-    k_pyramid<<<dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), 256, 0, st>>>(
-        c->depth, c->din.width, c->din.height, s.hierarchy_levels, c->pyr);
+    VF_CUDA(c, launch_pdl(k_pyramid, dim3((c->din.width + 31) / 32, (c->din.height + 31) / 32), dim3(256), 0, st,
+                          c->depth, c->din.width, c->din.height, s.hierarchy_levels, c->pyr));
     VF_LAUNCHED(c, "k_pyramid");
     ++*launches;
   }
@@ -465,11 +480,10 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
 int launch_raycast(vf_ctx* c, cudaStream_t st) {
   const vf_settings& s = c->s;
   const uint32_t* vox = reinterpret_cast<const uint32_t*>(c->voxels);
-  k_raycast<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->ranges, &c->dstate->fp,
-                                                             c->din, s.voxel_size, s.mu, c->points, c->normals);
-  k_ray_normals<<<dim3(c->frag_w, c->frag_h * 2), 128, 0, st>>>(hash_view(c), vox, c->vsize / 4, c->ranges,
-                                                                 &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points,
-                                                                 c->normals);
+  VF_CUDA(c, launch_pdl(k_raycast, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox, c->vsize / 4,
+                        c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals));
+  VF_CUDA(c, launch_pdl(k_ray_normals, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox,
+                        c->vsize / 4, c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals));
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
 }
@@ -521,9 +535,9 @@ int launch_alloc_scan(vf_ctx* c, cudaStream_t st) {
   const int n_words = c->s.bucket_count / 32;
   const int tiles = (n_words + kCompactThreads - 1) / kCompactThreads;
   VF_CUDA(c, cudaMemsetAsync(c->compact_scan, 0, sizeof(unsigned long long) * (1 + (size_t)tiles), st));
-  k_alloc_compact<<<tiles, kCompactThreads, 0, st>>>(c->req_bits, n_words, hash_view(c), c->req_list,
-                                                     c->req_excess_rank, c->compact_scan, &c->dstate->meta,
-                                                     &c->dstate->ctr, c->ranges, c->frag_w * c->frag_h);
+  VF_CUDA(c, launch_pdl(k_alloc_compact, dim3(tiles), dim3(kCompactThreads), 0, st, c->req_bits, n_words,
+                        hash_view(c), c->req_list, c->req_excess_rank, c->compact_scan, &c->dstate->meta,
+                        &c->dstate->ctr, c->ranges, c->frag_w * c->frag_h));
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
 }
@@ -548,20 +562,20 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
     if (int rc = enqueue_tracker(c, st, with_rgb, nullptr, true, &launches)) return rc;
   }
   stage_mark(c, 1);
-  k_mark<<<mark_grid(c), 256, 0, st>>>(c->depth, c->din, &c->dstate->pose, c->rgbin, c->depth_to_rgb,
-                                                &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
-                                                c->req_bits, &c->dstate->ctr);
+  VF_CUDA(c, launch_pdl(k_mark, dim3(mark_grid(c)), dim3(256), 0, st, c->depth, c->din, &c->dstate->pose, c->rgbin,
+                        c->depth_to_rgb, &c->dstate->fp, hash_view(c), s.voxel_size, s.mu, c->shard, c->req_key,
+                        c->req_bits, &c->dstate->ctr));
   VF_LAUNCHED(c, "k_mark");
   if (int rc = launch_alloc_scan(c, st)) return rc;
   VF_LAUNCHED(c, "k_alloc_compact");
-  k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
-                                                c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
-                                                c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots,
-                                                c->alloc_list, c->alloc_cap, &c->dstate->ctr);
+  VF_CUDA(c, launch_pdl(k_alloc_apply, dim3(c->num_sms * 2), dim3(256), 0, st, c->depth, c->din, &c->dstate->fp,
+                        s.voxel_size, s.mu, c->entries, c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
+                        c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots, c->alloc_list,
+                        c->alloc_cap, &c->dstate->ctr));
   VF_LAUNCHED(c, "k_alloc_apply");
-  k_visible<<<c->num_sms * 4, 256, 0, st>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
-                                            s.near_clip, s.far_clip, s.visibility_margin_px, c->visible_list,
-                                            &c->dstate->ctr);
+  VF_CUDA(c, launch_pdl(k_visible, dim3(c->num_sms * 4), dim3(256), 0, st, c->entries, c->alloc_list, &c->dstate->fp,
+                        c->din, s.voxel_size, s.near_clip, s.far_clip, s.visibility_margin_px, c->visible_list,
+                        &c->dstate->ctr));
   VF_LAUNCHED(c, "k_visible");
   launches += 5;
   stage_mark(c, 2);

@@ -43,6 +43,7 @@ namespace vf {
 // shared memory (32 = 2^5 keeps tiles aligned for up to 6 levels).
 __global__ void __launch_bounds__(256) k_pyramid(const float* __restrict__ depth0, int w0, int h0, int levels,
                                                  float* __restrict__ out /* levels 1.. back to back */) {
+  pdl_enter();
   __shared__ float tile[2][32 * 32];
   const int tx0 = blockIdx.x * 32, ty0 = blockIdx.y * 32;
   for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
@@ -232,6 +233,7 @@ __device__ __forceinline__ void shard_exchange(const IcpArgs& a, unsigned long l
 
 template <bool kCluster>
 __device__ __forceinline__ void icp_body(const IcpArgs& a) {
+  pdl_wait();  // no early trigger: the successor's CTAs would wait beside a grid / cluster barrier
   __shared__ Ctl ctl;
   __shared__ double s_red[kIcpThreads / 32][kAccStride];
   __shared__ double s_tot[kAccStride];

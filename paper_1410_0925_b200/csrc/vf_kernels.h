@@ -270,4 +270,24 @@ void nccl_comm_destroy(void* comm);
 int nccl_composite(void* comm, cudaStream_t st, const FrameParams* fp, float4* points, float4* normals,
                    unsigned long long* keys, int npix, int rank);
 
+// VF_PDL=0 turns programmatic dependent launch off (vf_api.cu).
+bool pdl_enabled();
+// A kernel launch on a frame stream with the programmatic-serialization
+// attribute (the kernel starts with pdl_enter / pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace vf

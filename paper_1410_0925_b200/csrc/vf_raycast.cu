@@ -100,6 +100,14 @@ constexpr int kCacheWays = 8;
 #ifndef VF_NORM_SHARED
 #define VF_NORM_SHARED 128
 #endif
+// 1: the normal's six trilinears read their 32 distinct voxels at once
+// (Sampler::normal32); 0: six dependent trilinears of 8 reads each.
+#ifndef VF_NORM_STENCIL32
+#define VF_NORM_STENCIL32 0
+#endif
+#ifndef VF_NORM_MIN_BLOCKS
+#define VF_NORM_MIN_BLOCKS 8
+#endif
 
 
 __device__ __noinline__ int probe(const HashView hv, int x, int y, int z) { return find_slot(hv, x, y, z); }
@@ -214,6 +222,92 @@ struct Sampler : SamplerCounts<kCount> {
       const F3 q{a == 0 ? p.x + sgn : p.x, a == 1 ? p.y + sgn : p.y, a == 2 ? p.z + sgn : p.z};
       v[k] = trilinear(q);
       if (v[k] != v[k]) return false;
+    }
+    const float gx = v[1] - v[0], gy = v[3] - v[2], gz = v[5] - v[4];
+    const float len = sqrtf(gx * gx + gy * gy + gz * gz);
+    if (len < 1e-12f) return false;
+    n = F3{gx / len, gy / len, gz / len};
+    return true;
+  }
+
+  // The same six trilinears from their 32 distinct voxels, all read at once
+  // (one memory round trip instead of six dependent ones).  Centre corner
+  // b = floor(p - 0.5) per axis; the -1 / +1 stencils along an axis use
+  // b - 1, b and b + 1, b + 2 there and b, b + 1 on the other two axes, so
+  // their union is the 2x2x2 cube at b plus two 2x2 layers per axis.  Every
+  // stencil's corner and fractions are computed with the generic path's own
+  // float operations; when p -/+ 1 rounds so that a stencil's corner is not
+  // b -/+ 1 the generic path runs instead.  A missing block reads as
+  // weight 0 (both make the trilinear, hence the normal, fail).
+  __device__ __noinline__ bool normal32(F3 p, F3& n) {
+    const float cx = p.x - 0.5f, cy = p.y - 0.5f, cz = p.z - 0.5f;
+    const int bx = __float2int_rz(floorf(cx)), by = __float2int_rz(floorf(cy)), bz = __float2int_rz(floorf(cz));
+    const float lx = (p.x + -1.0f) - 0.5f, hx = (p.x + 1.0f) - 0.5f;
+    const float ly = (p.y + -1.0f) - 0.5f, hy = (p.y + 1.0f) - 0.5f;
+    const float lz = (p.z + -1.0f) - 0.5f, hz = (p.z + 1.0f) - 0.5f;
+    const int ilx = __float2int_rz(floorf(lx)), ihx = __float2int_rz(floorf(hx));
+    const int ily = __float2int_rz(floorf(ly)), ihy = __float2int_rz(floorf(hy));
+    const int ilz = __float2int_rz(floorf(lz)), ihz = __float2int_rz(floorf(hz));
+    if (ilx != bx - 1 || ihx != bx + 1 || ily != by - 1 || ihy != by + 1 || ilz != bz - 1 || ihz != bz + 1)
+      return normal(p, n);
+    auto rd = [&](int ox, int oy, int oz) -> uint32_t {
+      const int x = bx + ox, y = by + oy, z = bz + oz;
+      const int s = lookup(x >> 3, y >> 3, z >> 3);
+      return s < 0 ? 0u : raw(s, x & 7, y & 7, z & 7);
+    };
+    // X[ox + 1][oy][oz] (ox -1..2, oy, oz 0..1); Y[oy == 2][ox][oz] (oy -1, 2); Z[oz == 2][ox][oy] (oz -1, 2)
+    uint32_t X[4][2][2], Y[2][2][2], Z[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) X[i][j][k] = rd(i - 1, j, k);
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          Y[s][i][j] = rd(i, s ? 2 : -1, j);
+          Z[s][i][j] = rd(i, j, s ? 2 : -1);
+        }
+    const float fxc = cx - (float)bx, fyc = cy - (float)by, fzc = cz - (float)bz;
+    // trilinear_sdf's blend (corner order, weight products as the generic path)
+    auto blend = [&](const uint32_t (&r)[8], float fx, float fy, float fz, float& value) -> bool {
+      value = 0.0f;
+#pragma unroll
+      for (int corner = 0; corner < 8; ++corner) {
+        const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+        if (((r[corner] >> 16) & 0xFFu) == 0) return false;
+        const float v = sdf_bits_to_float(r[corner]);
+        const float w = (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz);
+        value += w * v;
+      }
+      return true;
+    };
+    float v[6];
+    uint32_t r[8];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int a = k >> 1, hi = k & 1;
+#pragma unroll
+      for (int corner = 0; corner < 8; ++corner) {
+        const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+        if (a == 0) {
+          r[corner] = X[2 * hi + dx][dy][dz];
+        } else if (a == 1) {
+          const int oy = 2 * hi - 1 + dy;  // -1..2
+          r[corner] = (oy == -1 || oy == 2) ? Y[oy == 2][dx][dz] : X[1 + dx][oy][dz];
+        } else {
+          const int oz = 2 * hi - 1 + dz;
+          r[corner] = (oz == -1 || oz == 2) ? Z[oz == 2][dx][dy] : X[1 + dx][dy][oz];
+        }
+      }
+      const float fx = a == 0 ? (hi ? hx - (float)ihx : lx - (float)ilx) : fxc;
+      const float fy = a == 1 ? (hi ? hy - (float)ihy : ly - (float)ily) : fyc;
+      const float fz = a == 2 ? (hi ? hz - (float)ihz : lz - (float)ilz) : fzc;
+      if (!blend(r, fx, fy, fz, v[k])) return false;
     }
     const float gx = v[1] - v[0], gy = v[3] - v[2], gz = v[5] - v[4];
     const float len = sqrtf(gx * gx + gy * gy + gz * gz);
@@ -388,6 +482,7 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
               const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
               float4* __restrict__ normals) {
+  pdl_enter();
   __shared__ int4 s_cache[kCacheWays * kRayThreads];
   if (vstride == 1)
     raycast_body<1>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
@@ -424,7 +519,8 @@ __device__ __forceinline__ void ray_normal_body(const HashView& hv, const uint32
     p = make_float4(hw.x, hw.y, hw.z, 1.0f);
   }
   F3 n;
-  if (smp.normal(F3{p.x / vs, p.y / vs, p.z / vs}, n)) {
+  const F3 pv{p.x / vs, p.y / vs, p.z / vs};
+  if (VF_NORM_STENCIL32 ? smp.normal32(pv, n) : smp.normal(pv, n)) {
     points[pix] = p;
     normals[pix] = make_float4(n.x, n.y, n.z, 1.0f);
   } else {
@@ -433,10 +529,11 @@ __device__ __forceinline__ void ray_normal_body(const HashView& hv, const uint32
   }
 }
 
-__global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
+__global__ void __launch_bounds__(kRayThreads, VF_NORM_MIN_BLOCKS)
     k_ray_normals(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
                   const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
                   float4* __restrict__ normals) {
+  pdl_enter();
   __shared__ int4 s_cache[kCacheWays * kRayThreads];
   __shared__ int4 s_blocks[VF_NORM_SHARED > 0 ? VF_NORM_SHARED : 1];
   if (VF_NORM_SHARED > 0) {
