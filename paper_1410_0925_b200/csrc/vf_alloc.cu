@@ -389,8 +389,14 @@ __global__ void __launch_bounds__(256) k_alloc_apply(const float* __restrict__ d
                                                      const int* __restrict__ req_excess_rank,
                                                      const AllocMeta* __restrict__ meta, int* __restrict__ vba_slots,
                                                      int* __restrict__ excess_slots, int* __restrict__ alloc_list,
-                                                     int alloc_cap, Counters* __restrict__ ctr) {
+                                                     int alloc_cap, Counters* __restrict__ ctr,
+                                                     unsigned long long* __restrict__ scan_reset, int n_reset) {
   pdl_enter();
+  // k_alloc_compact has finished with its ticket and look-back words: clear
+  // them for the next frame here (no memset node between k_mark and the
+  // compaction, so that edge stays a programmatic one)
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < n_reset; i += blockDim.x) scan_reset[i] = 0ull;
   const AllocMeta m = *meta;
   const PoseD c2w = fp->c2w;
   if (!m.slow) {

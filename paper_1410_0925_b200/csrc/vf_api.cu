@@ -530,11 +530,14 @@ void persist_hash_table(vf_ctx* c) {
 // k_mark's grid: one thread per pixel, 32 x 8 pixel tiles.
 int mark_grid(const vf_ctx* c) { return ((c->din.width + 31) / 32) * ((c->din.height + 7) / 8); }
 
+// k_alloc_compact's ticket + per-tile look-back words.
+int scan_words(const vf_ctx* c) { return 1 + (c->s.bucket_count / 32 + kCompactThreads - 1) / kCompactThreads; }
+
 // perform_allocations' ordered compaction of the request bitmap (k_alloc_compact).
 int launch_alloc_scan(vf_ctx* c, cudaStream_t st) {
   const int n_words = c->s.bucket_count / 32;
   const int tiles = (n_words + kCompactThreads - 1) / kCompactThreads;
-  VF_CUDA(c, cudaMemsetAsync(c->compact_scan, 0, sizeof(unsigned long long) * (1 + (size_t)tiles), st));
+  // compact_scan is zero here: cleared at creation and by every k_alloc_apply after its compaction
   VF_CUDA(c, launch_pdl(k_alloc_compact, dim3(tiles), dim3(kCompactThreads), 0, st, c->req_bits, n_words,
                         hash_view(c), c->req_list, c->req_excess_rank, c->compact_scan, &c->dstate->meta,
                         &c->dstate->ctr, c->ranges, c->frag_w * c->frag_h));
@@ -571,7 +574,7 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   VF_CUDA(c, launch_pdl(k_alloc_apply, dim3(c->num_sms * 2), dim3(256), 0, st, c->depth, c->din, &c->dstate->fp,
                         s.voxel_size, s.mu, c->entries, c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
                         c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots, c->alloc_list,
-                        c->alloc_cap, &c->dstate->ctr));
+                        c->alloc_cap, &c->dstate->ctr, c->compact_scan, scan_words(c)));
   VF_LAUNCHED(c, "k_alloc_apply");
   VF_CUDA(c, launch_pdl(k_visible, dim3(c->num_sms * 4), dim3(256), 0, st, c->entries, c->alloc_list, &c->dstate->fp,
                         c->din, s.voxel_size, s.near_clip, s.far_clip, s.visibility_margin_px, c->visible_list,
@@ -904,6 +907,10 @@ int collect_frame(vf_ctx* c, vf_frame_stats* stats) {
 template <typename T>
 int dalloc(vf_ctx* c, T** p, size_t bytes) {
   VF_CUDA(c, cudaMalloc(reinterpret_cast<void**>(p), bytes));
+  return VF_OK;
+}
+int dzero(vf_ctx* c, void* p, size_t bytes) {
+  VF_CUDA(c, cudaMemset(p, 0, bytes));
   return VF_OK;
 }
 
@@ -1297,6 +1304,8 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->req_excess_rank, sizeof(int) * (size_t)s->bucket_count)) ||
       (rc = dalloc(c, &c->compact_scan,
                    sizeof(unsigned long long) * (2 + (size_t)s->bucket_count / 32 / kCompactThreads))) ||
+      (rc = dzero(c, c->compact_scan,
+                  sizeof(unsigned long long) * (2 + (size_t)s->bucket_count / 32 / kCompactThreads))) ||
       (rc = dalloc(c, &c->alloc_list, sizeof(int) * (size_t)c->alloc_cap)) ||
       (rc = dalloc(c, &c->visible_list, sizeof(int) * (size_t)c->alloc_cap)) ||
       (rc = dalloc(c, &c->dstate, sizeof(DevState))) ||
@@ -1831,7 +1840,8 @@ int vf_stage_allocate(vf_ctx* c, const float* depth_m, const double pose[12], vf
   k_alloc_apply<<<c->num_sms * 2, 256, 0, st>>>(c->depth, c->din, &c->dstate->fp, s.voxel_size, s.mu, c->entries,
                                                 c->mask, s.bucket_size, c->ordered, c->req_key, c->req_list,
                                                 c->req_excess_rank, &c->dstate->meta, c->vba_slots, c->excess_slots,
-                                                c->alloc_list, c->alloc_cap, &c->dstate->ctr);
+                                                c->alloc_list, c->alloc_cap, &c->dstate->ctr, c->compact_scan,
+                                                scan_words(c));
   k_visible<<<c->num_sms * 4, 256, 0, st>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
                                             s.near_clip, s.far_clip, s.visibility_margin_px, c->visible_list,
                                             &c->dstate->ctr);

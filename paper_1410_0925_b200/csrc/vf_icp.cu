@@ -233,7 +233,12 @@ __device__ __forceinline__ void shard_exchange(const IcpArgs& a, unsigned long l
 
 template <bool kCluster>
 __device__ __forceinline__ void icp_body(const IcpArgs& a) {
-  pdl_wait();  // no early trigger: the successor's CTAs would wait beside a grid / cluster barrier
+  // the successor (k_icp after the cluster kernel, k_mark after k_icp) may be
+  // scheduled now; its CTAs wait in their own pdl_wait until this grid is done.
+  // Not with the shard exchange: shards' ICP loops sharing a device must all
+  // become resident, and waiting successor CTAs could hold the SMs they need.
+  pdl_wait();
+  if (a.xranks <= 1) pdl_trigger();
   __shared__ Ctl ctl;
   __shared__ double s_red[kIcpThreads / 32][kAccStride];
   __shared__ double s_tot[kAccStride];

@@ -103,7 +103,7 @@ __global__ void k_alloc_apply(const float* depth, IntrD in, const FrameParams* f
                               HashEntry* entries, uint32_t mask, int bucket_size, int ordered,
                               unsigned long long* req_key, const int* req_list, const int* req_excess_rank,
                               const AllocMeta* meta, int* vba_slots, int* excess_slots, int* alloc_list,
-                              int alloc_cap, Counters* ctr);
+                              int alloc_cap, Counters* ctr, unsigned long long* scan_reset, int n_reset);
 __global__ void k_visible(const HashEntry* entries, const int* alloc_list, const FrameParams* fp, IntrD in, float vs,
                           float near_clip, float far_clip, int margin, int* visible_list, Counters* ctr);
 __global__ void k_integrate_s(const HashEntry* entries, const int* visible_list, const Counters* ctr, void* voxels,
