@@ -370,16 +370,17 @@ int launch_forward_project(vf_ctx* c) {
 int enqueue_ren(vf_ctx* c, cudaStream_t st, bool combine_icp, const PoseD* explicit_init, bool update_state,
                 int* launches) {
   const vf_settings& s = c->s;
-  k_ren_init<<<1, 32, 0, st>>>(&c->dstate->icp, &c->dstate->pose, combine_icp ? 1 : 0, explicit_init, &c->dstate->ren);
+  VF_CUDA(c, launch_pdl(k_ren_init, dim3(1), dim3(32), 0, st, &c->dstate->icp, &c->dstate->pose, combine_icp ? 1 : 0,
+                        explicit_init, &c->dstate->ren));
   for (int it = 0; it < s.max_iterations; ++it) {
-    k_ren_terms<<<c->ren_grid, 256, 0, st>>>(c->depth, c->din, hash_view(c), reinterpret_cast<const uint32_t*>(c->voxels),
-                                             c->vsize / 4, s.voxel_size, (double)s.ren_sigma, &c->dstate->ren,
-                                             c->ren_partials);
-    k_ren_ctl<<<1, 32, 0, st>>>(c->ren_partials, c->ren_grid, &c->dstate->ren, s.min_valid_points, s.max_condition,
-                                s.convergence_eps);
+    VF_CUDA(c, launch_pdl(k_ren_terms, dim3(c->ren_grid), dim3(256), 0, st, c->depth, c->din, hash_view(c),
+                          reinterpret_cast<const uint32_t*>(c->voxels), c->vsize / 4, s.voxel_size,
+                          (double)s.ren_sigma, &c->dstate->ren, c->ren_partials));
+    VF_CUDA(c, launch_pdl(k_ren_ctl, dim3(1), dim3(32), 0, st, c->ren_partials, c->ren_grid, &c->dstate->ren,
+                          s.min_valid_points, s.max_condition, s.convergence_eps));
   }
-  k_ren_finish<<<1, 32, 0, st>>>(&c->dstate->ren, combine_icp ? 1 : 0, &c->dstate->icp,
-                                 &c->dstate->pose, update_state ? 1 : 0);
+  VF_CUDA(c, launch_pdl(k_ren_finish, dim3(1), dim3(32), 0, st, &c->dstate->ren, combine_icp ? 1 : 0, &c->dstate->icp,
+                        &c->dstate->pose, update_state ? 1 : 0));
   VF_CUDA(c, cudaGetLastError());
   *launches += 2 + 2 * s.max_iterations;
   return VF_OK;

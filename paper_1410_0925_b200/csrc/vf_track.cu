@@ -112,6 +112,7 @@ __device__ void block_reduce32(double (&acc)[32], double* s_red /* [32][32] */, 
 // ---------------------------------------------------------------------------
 __global__ void k_ren_init(const IcpResult* __restrict__ icp, const PoseD* __restrict__ state, int use_icp,
                            const PoseD* __restrict__ explicit_init, RenCtl* __restrict__ ctl) {
+  pdl_enter();
   if (threadIdx.x != 0) return;
   PoseD init = *state;
   if (explicit_init) init = *explicit_init;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(256) k_ren_terms(const float* __restrict__ dep
                                                    const uint32_t* __restrict__ vox, int vstride, float vs,
                                                    double sigma, const RenCtl* __restrict__ ctl,
                                                    double* __restrict__ partials) {
+  pdl_enter();
   __shared__ double s_red[32 * 32];
   __shared__ double s_out[32];
   if (ctl->done) return;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(256) k_ren_terms(const float* __restrict__ dep
 // the reference's per-iteration control (ren_tracker.hpp:82-110)
 __global__ void k_ren_ctl(const double* __restrict__ partials, int nparts, RenCtl* __restrict__ ctl,
                           int min_valid_points, double max_condition, float convergence_eps) {
+  pdl_enter();
   __shared__ double s_tot[32];
   if (ctl->done) return;
   const int lane = threadIdx.x;
@@ -234,6 +237,7 @@ __global__ void k_ren_ctl(const double* __restrict__ partials, int nparts, RenCt
 // frame's TrackingResult and, when ok and update_state, the pose.
 __global__ void k_ren_finish(RenCtl* __restrict__ ctl, int combine_icp, IcpResult* __restrict__ res,
                              PoseD* __restrict__ state, int update_state) {
+  pdl_enter();
   if (threadIdx.x != 0) return;
   const bool ok = ctl->done ? ctl->ok != 0 : true;  // max_iterations reached: ok
   IcpResult out;
