@@ -397,12 +397,15 @@ int enqueue_color(vf_ctx* c, cudaStream_t st, const PoseD* explicit_init, bool u
     const int n = in.width * in.height;
     float4* col = c->cpyr + c->cpyr_off[l];
     if (l == 0) {
-      k_cpyr_base<<<(n + 255) / 256, 256, 0, st>>>(c->rgb, n, col);
+      VF_CUDA(c, launch_pdl(k_cpyr_base, dim3((n + 255) / 256), dim3(256), 0, st, c->rgb, n, col));
     } else {
       const IntrD& up = c->rgb_levels[l - 1];
-      k_cpyr_down<<<(n + 255) / 256, 256, 0, st>>>(c->cpyr + c->cpyr_off[l - 1], up.width, up.height, col);
+      VF_CUDA(c, launch_pdl(k_cpyr_down, dim3((n + 255) / 256), dim3(256), 0, st, c->cpyr + c->cpyr_off[l - 1],
+                            up.width, 
+                            up.height, col));
     }
-    k_cpyr_grad<<<(n + 255) / 256, 256, 0, st>>>(col, in.width, in.height, col + n, col + 2 * (size_t)n);
+    VF_CUDA(c, launch_pdl(k_cpyr_grad, dim3((n + 255) / 256), dim3(256), 0, st, col, in.width, in.height, col + n,
+                          col + 2 * (size_t)n));
     a.lv[l] = ColorLevel{col, col + n, col + 2 * (size_t)n, in.width, in.height, in.fx, in.fy, in.cx, in.cy};
   }
   a.levels = L;
@@ -424,17 +427,19 @@ int enqueue_color(vf_ctx* c, cudaStream_t st, const PoseD* explicit_init, bool u
   int g = std::max(1, std::min({c->num_sms, c->icp_grid, (c->surf_cap + kColorThreads - 1) / kColorThreads}));
   if (const char* e = std::getenv("VF_COLOR_GRID")) g = std::max(1, std::min(g, std::atoi(e)));  // tuning override
   if (g == 1) {
-    k_color_track<<<1, kColorThreads, 0, st>>>(a);
+    VF_CUDA(c, launch_pdl(k_color_track, dim3(1), dim3(kColorThreads), 0, st, a));
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(g);
     cfg.blockDim = dim3(kColorThreads);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     VF_CUDA(c, cudaLaunchKernelEx(&cfg, k_color_track, a));
   }
   VF_CUDA(c, cudaGetLastError());
@@ -595,15 +600,15 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   cudaStream_t branch = fork ? c->side : st;
   auto enqueue_swap = [&](cudaStream_t sst) -> int {
     // request_swap_ins/outs + execute_swap_in/out (pipeline_impl.hpp:104-113)
-    k_swap_request<<<c->num_sms * 4, 256, 0, sst>>>(c->entries, c->alloc_list, &c->dstate->fp, c->din, s.voxel_size,
-                                                    s.near_clip, s.far_clip, s.visibility_margin_px, s.swap_margin_px,
-                                                    c->sw, &c->dstate->ctr);
+    VF_CUDA(c, launch_pdl(k_swap_request, dim3(c->num_sms * 4), dim3(256), 0, sst, c->entries, c->alloc_list,
+                          &c->dstate->fp, c->din, s.voxel_size, s.near_clip, s.far_clip, s.visibility_margin_px,
+                          s.swap_margin_px, c->sw, &c->dstate->ctr));
     VF_LAUNCHED(c, "k_swap_request");
-    k_swap_select<<<1, 1024, 0, sst>>>(c->entries, c->vba_slots, c->sw, s.swap_buffer_blocks,
-                                       (c->vsize == 8 ? 7 : 3) * kBlockVolume, &c->dstate->ctr);
+    VF_CUDA(c, launch_pdl(k_swap_select, dim3(1), dim3(1024), 0, sst, c->entries, c->vba_slots, c->sw,
+                          s.swap_buffer_blocks, (c->vsize == 8 ? 7 : 3) * kBlockVolume, &c->dstate->ctr));
     VF_LAUNCHED(c, "k_swap_select");
-    k_swap_transfer<<<c->num_sms * 2, 256, 0, sst>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
-                                                     s.max_weight, 0);
+    VF_CUDA(c, launch_pdl(k_swap_transfer, dim3(c->num_sms * 2), dim3(256), 0, sst,
+                          reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw, s.max_weight, 0));
     VF_LAUNCHED(c, "k_swap_transfer");
     launches += 3;
     return VF_OK;
@@ -611,9 +616,9 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   if (fork) {
     VF_CUDA(c, cudaEventRecord(c->ev_fork, st));
     VF_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    k_ranges<<<c->num_sms * 2, 256, 0, c->side>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp,
-                                                  c->din, s.voxel_size, s.near_clip, s.far_clip, c->ranges,
-                                                  c->frag_w);
+    VF_CUDA(c, launch_pdl(k_ranges, dim3(c->num_sms * 2), dim3(256), 0, c->side, c->entries, c->visible_list,
+                          &c->dstate->ctr, &c->dstate->fp, c->din, s.voxel_size, s.near_clip, s.far_clip, c->ranges,
+                          c->frag_w));
     if (c->swapping)
       if (int rc = enqueue_swap(c->side)) return rc;
     VF_CUDA(c, cudaEventRecord(c->ev_join, c->side));
@@ -632,16 +637,17 @@ int enqueue_frame(vf_ctx* c, bool track, bool with_rgb) {
   }
   if (c->swapping) {
     // swap-outs: after the selection, beside the raycast
-    k_swap_transfer<<<c->num_sms * 2, 256, 0, branch>>>(reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw,
-                                                        s.max_weight, 1);
+    VF_CUDA(c, launch_pdl(k_swap_transfer, dim3(c->num_sms * 2), dim3(256), 0, branch,
+                          reinterpret_cast<uint32_t*>(c->voxels), c->vsize / 4, c->sw, s.max_weight, 1));
     VF_LAUNCHED(c, "k_swap_transfer");
     if (fork) VF_CUDA(c, cudaEventRecord(c->ev_join2, c->side));
     ++launches;
   }
   stage_mark(c, 4);
   if (!fork) {
-    k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
-                                             s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
+    VF_CUDA(c, launch_pdl(k_ranges, dim3(c->num_sms * 2), dim3(256), 0, st, c->entries, c->visible_list,
+                          &c->dstate->ctr, &c->dstate->fp, c->din, s.voxel_size, s.near_clip, s.far_clip, c->ranges,
+                          c->frag_w));
   }
   VF_LAUNCHED(c, "k_ranges");
   if (c->p2p_linked > 1) {  // the previous frame's maps and keys are no longer read by any shard
@@ -1881,8 +1887,9 @@ int vf_stage_raycast(vf_ctx* c, const double pose[12]) {
   if (int rc = set_pose_dev(c, pose)) return rc;
   k_prep<<<1, 32, 0, st>>>(&c->dstate->pose, c->din, c->rgbin, c->depth_to_rgb, &c->dstate->fp);
   k_init_ranges<<<(c->frag_w * c->frag_h + 255) / 256, 256, 0, st>>>(c->ranges, c->frag_w * c->frag_h);
-  k_ranges<<<c->num_sms * 2, 256, 0, st>>>(c->entries, c->visible_list, &c->dstate->ctr, &c->dstate->fp, c->din,
-                                           s.voxel_size, s.near_clip, s.far_clip, c->ranges, c->frag_w);
+  VF_CUDA(c, launch_pdl(k_ranges, dim3(c->num_sms * 2), dim3(256), 0, st, c->entries, c->visible_list,
+                        &c->dstate->ctr, &c->dstate->fp, c->din, s.voxel_size, s.near_clip, s.far_clip, c->ranges,
+                        c->frag_w));
   if (int rc = launch_raycast(c, st)) return rc;
   VF_CUDA(c, cudaGetLastError());
   VF_CUDA(c, cudaStreamSynchronize(st));

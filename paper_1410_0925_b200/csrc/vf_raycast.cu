@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(256) k_ranges(const HashEntry* __restrict__ en
                                                 const int* __restrict__ visible_list, const Counters* __restrict__ ctr,
                                                 const FrameParams* __restrict__ fp, IntrD in, float vs, float near_clip,
                                                 float far_clip, float2* __restrict__ ranges, int frag_w) {
+  pdl_enter();
   __shared__ PoseD s_w2c;
   if (threadIdx.x < sizeof(PoseD) / sizeof(double))
     reinterpret_cast<double*>(&s_w2c)[threadIdx.x] = reinterpret_cast<const double*>(&fp->w2c)[threadIdx.x];

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(256) k_swap_request(const HashEntry* __restric
                                                       const FrameParams* __restrict__ fp, IntrD in, float vs,
                                                       float near_clip, float far_clip, int margin, int swap_margin,
                                                       SwapDev sw, Counters* __restrict__ ctr) {
+  pdl_enter();
   __shared__ PoseD s_w2c;
   if (threadIdx.x < sizeof(PoseD) / sizeof(double))
     reinterpret_cast<double*>(&s_w2c)[threadIdx.x] = reinterpret_cast<const double*>(&fp->w2c)[threadIdx.x];
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(256) k_swap_request(const HashEntry* __restric
 __global__ void __launch_bounds__(1024) k_swap_select(HashEntry* __restrict__ entries, int* __restrict__ vba_slots,
                                                       SwapDev sw, int buffer_blocks, int payload_bytes,
                                                       Counters* __restrict__ ctr) {
+  pdl_enter();
   __shared__ int s_sort[kSwapSortCap];
   __shared__ int s_hist[4096];
   __shared__ int s_misc[4];
@@ -298,6 +300,7 @@ __device__ __forceinline__ void transfer_block(uint4* dev, uint4* host, bool in,
 
 __global__ void __launch_bounds__(256) k_swap_transfer(uint32_t* __restrict__ voxels, int words_per_voxel,
                                                        SwapDev sw, int max_weight, int which) {
+  pdl_enter();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int k_in = sw.ctr->staged_in, k_out = sw.ctr->staged_out;

@@ -266,6 +266,7 @@ __global__ void k_ren_finish(RenCtl* __restrict__ ctl, int combine_icp, IcpResul
 // Colour pyramid (pyramid.hpp:66-132); colours as float4 (w unused)
 // ---------------------------------------------------------------------------
 __global__ void k_cpyr_base(const uint8_t* __restrict__ rgb, int n, float4* __restrict__ out) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   out[i] = make_float4((float)rgb[3 * i] / 255.0f, (float)rgb[3 * i + 1] / 255.0f, (float)rgb[3 * i + 2] / 255.0f,
@@ -274,6 +275,7 @@ __global__ void k_cpyr_base(const uint8_t* __restrict__ rgb, int n, float4* __re
 
 // downsample_mean: sum of the in-bounds 2x2 samples times 1 / n
 __global__ void k_cpyr_down(const float4* __restrict__ src, int sw, int sh, float4* __restrict__ dst) {
+  pdl_enter();
   const int dw = (sw + 1) / 2, dh = (sh + 1) / 2;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= dw * dh) return;
@@ -297,6 +299,7 @@ __global__ void k_cpyr_down(const float4* __restrict__ src, int sw, int sh, floa
 // image_gradients: central differences, zero on the border
 __global__ void k_cpyr_grad(const float4* __restrict__ src, int w, int h, float4* __restrict__ gx,
                             float4* __restrict__ gy) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= w * h) return;
   const int x = i % w, y = i / w;
@@ -410,6 +413,7 @@ __device__ void evaluate_color_grid(const ColorTrackArgs& a, int n, const ColorL
 // grid (every CTA runs the same damping logic on the same sums).  Writes the
 // frame's TrackingResult; the pose when ok and update_state.
 __global__ void __launch_bounds__(kColorThreads) k_color_track(ColorTrackArgs a) {
+  pdl_wait();
   __shared__ double s_red[32 * 32];
   __shared__ double s_eval[32], s_trial[32];
   __shared__ PoseD s_pose, s_cand;
