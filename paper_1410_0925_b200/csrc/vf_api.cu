@@ -107,6 +107,7 @@ struct vf_ctx {
   uint8_t* rgb = nullptr;
   float* pyr = nullptr;
   float2* ranges = nullptr;
+  unsigned* ray_flags = nullptr;  // k_raycast -> k_ray_normals per-CTA completion flags
   float4* points = nullptr;
   float4* normals = nullptr;
   double* partials = nullptr;
@@ -487,9 +488,10 @@ int launch_raycast(vf_ctx* c, cudaStream_t st) {
   const vf_settings& s = c->s;
   const uint32_t* vox = reinterpret_cast<const uint32_t*>(c->voxels);
   VF_CUDA(c, launch_pdl(k_raycast, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox, c->vsize / 4,
-                        c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals));
+                        c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals, c->ray_flags));
   VF_CUDA(c, launch_pdl(k_ray_normals, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox,
-                        c->vsize / 4, c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals));
+                        c->vsize / 4, c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals,
+                        c->ray_flags, &c->dstate->ctr));
   VF_CUDA(c, cudaGetLastError());
   return VF_OK;
 }
@@ -929,7 +931,8 @@ void free_all(vf_ctx* c) {
         if (g) cudaGraphExecDestroy(g);
   void* ptrs[] = {c->entries, c->voxels, c->vba_slots, c->excess_slots, c->req_key, c->req_bits, c->req_list,
                   c->req_excess_rank, c->alloc_list, c->visible_list, c->dstate, c->depth, c->rgb, c->pyr,
-                  c->ranges, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf, c->shard_keys, c->icp_ctl,
+                  c->ranges, c->ray_flags, c->points, c->normals, c->partials, c->utab, c->trace, c->flush_buf,
+                  c->shard_keys, c->icp_ctl,
                   c->surf_points, c->surf_colors, c->surf_scan, c->image, c->image_dmax,
                   c->sw.state, c->sw.host_slot, c->sw.host_free, c->sw.in_cand, c->sw.out_cand,
                   c->sw.stage_entry, c->sw.stage_slot, c->sw.stage_host, c->disp, c->image_depth_scratch,
@@ -1322,6 +1325,8 @@ int vf_create(const vf_settings* s, const vf_calib* calib, int device, vf_ctx** 
       (rc = dalloc(c, &c->rgb, 3 * (size_t)c->rgbin.width * c->rgbin.height)) ||
       (rc = dalloc(c, &c->pyr, sizeof(float) * std::max<size_t>(c->pyr_floats, 1))) ||
       (rc = dalloc(c, &c->ranges, sizeof(float2) * (size_t)c->frag_w * c->frag_h)) ||
+      (rc = dalloc(c, &c->ray_flags, sizeof(unsigned) * 2 * (size_t)c->frag_w * c->frag_h)) ||
+      (rc = dzero(c, c->ray_flags, sizeof(unsigned) * 2 * (size_t)c->frag_w * c->frag_h)) ||
       (rc = dalloc(c, &c->points, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->normals, sizeof(float4) * (size_t)c->npix)) ||
       (rc = dalloc(c, &c->partials, sizeof(double) * 2 * 32 * (size_t)c->icp_grid)) ||

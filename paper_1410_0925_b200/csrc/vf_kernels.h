@@ -120,9 +120,10 @@ __global__ void k_ranges(const HashEntry* entries, const int* visible_list, cons
                          const FrameParams* fp, IntrD in, float vs, float near_clip, float far_clip, float2* ranges,
                          int frag_w);
 __global__ void k_raycast(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
-                          IntrD in, float vs, float mu, float4* points, float4* normals);
+                          IntrD in, float vs, float mu, float4* points, float4* normals, unsigned* ray_flags);
 __global__ void k_ray_normals(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
-                              IntrD in, float vs, float mu, float4* points, float4* normals);
+                              IntrD in, float vs, float mu, float4* points, float4* normals, unsigned* ray_flags,
+                              Counters* ctr);
 __global__ void k_raycast_count(HashView hv, const uint32_t* vox, int vstride, const float2* ranges,
                                 const FrameParams* fp, IntrD in, float vs, float mu, float4* points, float4* normals,
                                 unsigned long long* counters);

@@ -482,13 +482,21 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
 __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
     k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
               const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
-              float4* __restrict__ normals) {
+              float4* __restrict__ normals, unsigned* __restrict__ ray_flags) {
   pdl_enter();
   __shared__ int4 s_cache[kCacheWays * kRayThreads];
   if (vstride == 1)
     raycast_body<1>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
   else
     raycast_body<2>(hv, vox, ranges, fp, in, vs, mu, points, normals, s_cache);
+  // this CTA's half fragment is in the maps: release it to the k_ray_normals
+  // CTA of the same index (which may already be waiting, see there)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ray_flags + blockIdx.y * gridDim.x + blockIdx.x), "r"(1u)
+                 : "memory");
+  }
 }
 
 // K3b second pass: the zero-crossing refinement and the normal of every hit
@@ -533,14 +541,35 @@ __device__ __forceinline__ void ray_normal_body(const HashView& hv, const uint32
 __global__ void __launch_bounds__(kRayThreads, VF_NORM_MIN_BLOCKS)
     k_ray_normals(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
                   const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
-                  float4* __restrict__ normals) {
-  pdl_enter();
+                  float4* __restrict__ normals, unsigned* __restrict__ ray_flags, Counters* __restrict__ ctr) {
+  // No griddepcontrol.wait on the whole march grid: this CTA waits only for
+  // the k_raycast CTA of the same index (its completion flag), so the normals
+  // of finished half fragments run in the march's tail.  Safe: PDL launches
+  // this grid only after every k_raycast CTA has executed its own
+  // pdl_enter (so everything before the march is complete and every march
+  // CTA is resident and will finish); without PDL the march is complete.
+  // The flag is cleared here for the next launch pair (launch_raycast always
+  // launches both); a flag that never arrives (~0.5 s) raises kErrRayFlags.
+  pdl_trigger();
   __shared__ int4 s_cache[kCacheWays * kRayThreads];
   __shared__ int4 s_blocks[VF_NORM_SHARED > 0 ? VF_NORM_SHARED : 1];
-  if (VF_NORM_SHARED > 0) {
-    for (int i = threadIdx.x; i < VF_NORM_SHARED; i += blockDim.x) s_blocks[i] = make_int4(0x7fffffff, 0, 0, -1);
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* f = ray_flags + blockIdx.y * gridDim.x + blockIdx.x;
+    unsigned v = 0;
+    for (long spin = 0;; ++spin) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v != 0u) break;
+      if (spin > (1l << 22)) {
+        atomicOr(&ctr->error_flags, kErrRayFlags);
+        break;
+      }
+      __nanosleep(64);
+    }
+    *f = 0u;
   }
+  if (VF_NORM_SHARED > 0)
+    for (int i = threadIdx.x; i < VF_NORM_SHARED; i += blockDim.x) s_blocks[i] = make_int4(0x7fffffff, 0, 0, -1);
+  __syncthreads();
   const int fxi = blockIdx.x, fyi = blockIdx.y >> 1;
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const int x = fxi * kFragmentSize + (lane & 7) + ((wq & 1) << 3);
