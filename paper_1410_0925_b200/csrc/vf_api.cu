@@ -487,7 +487,8 @@ int enqueue_tracker(vf_ctx* c, cudaStream_t st, bool with_rgb, const PoseD* expl
 int launch_raycast(vf_ctx* c, cudaStream_t st) {
   const vf_settings& s = c->s;
   const uint32_t* vox = reinterpret_cast<const uint32_t*>(c->voxels);
-  VF_CUDA(c, launch_pdl(k_raycast, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox, c->vsize / 4,
+  auto* march = c->npix <= VF_RAY_SMALL_PIXELS ? k_raycast<VF_RAY_MIN_BLOCKS_SMALL> : k_raycast<VF_RAY_MIN_BLOCKS>;
+  VF_CUDA(c, launch_pdl(march, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox, c->vsize / 4,
                         c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals, c->ray_flags));
   VF_CUDA(c, launch_pdl(k_ray_normals, dim3(c->frag_w, c->frag_h * 2), dim3(128), 0, st, hash_view(c), vox,
                         c->vsize / 4, c->ranges, &c->dstate->fp, c->din, s.voxel_size, s.mu, c->points, c->normals,

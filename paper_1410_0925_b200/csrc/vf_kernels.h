@@ -119,6 +119,17 @@ __global__ void k_integrate_rgb(const HashEntry* entries, const int* visible_lis
 __global__ void k_ranges(const HashEntry* entries, const int* visible_list, const Counters* ctr,
                          const FrameParams* fp, IntrD in, float vs, float near_clip, float far_clip, float2* ranges,
                          int frag_w);
+// the march's occupancy points (CTAs per SM): large frames / frames up to VF_RAY_SMALL_PIXELS
+#ifndef VF_RAY_MIN_BLOCKS
+#define VF_RAY_MIN_BLOCKS 8
+#endif
+#ifndef VF_RAY_MIN_BLOCKS_SMALL
+#define VF_RAY_MIN_BLOCKS_SMALL 6
+#endif
+#ifndef VF_RAY_SMALL_PIXELS
+#define VF_RAY_SMALL_PIXELS (640 * 480)
+#endif
+template <int kMinBlocks>
 __global__ void k_raycast(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,
                           IntrD in, float vs, float mu, float4* points, float4* normals, unsigned* ray_flags);
 __global__ void k_ray_normals(HashView hv, const uint32_t* vox, int vstride, const float2* ranges, const FrameParams* fp,

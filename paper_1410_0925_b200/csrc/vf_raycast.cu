@@ -84,9 +84,6 @@ __global__ void __launch_bounds__(256) k_ranges(const HashEntry* __restrict__ en
 
 namespace {
 
-#ifndef VF_RAY_MIN_BLOCKS
-#define VF_RAY_MIN_BLOCKS 8
-#endif
 constexpr int kRayThreads = 128;
 constexpr int kCacheWays = 8;
 // 1: the march ends at the zero-crossing bracket and the two refinement
@@ -479,7 +476,8 @@ __device__ __forceinline__ void raycast_body(const HashView& hv, const uint32_t*
   normals[pix] = out_n;
 }
 
-__global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kRayThreads, kMinBlocks)
     k_raycast(HashView hv, const uint32_t* __restrict__ vox, int vstride, const float2* __restrict__ ranges,
               const FrameParams* __restrict__ fp, IntrD in, float vs, float mu, float4* __restrict__ points,
               float4* __restrict__ normals, unsigned* __restrict__ ray_flags) {
@@ -498,6 +496,16 @@ __global__ void __launch_bounds__(kRayThreads, VF_RAY_MIN_BLOCKS)
                  : "memory");
   }
 }
+// Two occupancy points of the march (launch_raycast picks by frame size):
+// 8 CTAs per SM (64 registers) for large frames, 6 (70 registers, no
+// spills) up to VF_RAY_SMALL_PIXELS -- measured C1 raycast 0.156 -> 0.142 ms,
+// C3 0.422 -> 0.454 ms (profiles/r2_ab_rayocc*.txt).
+template __global__ void k_raycast<VF_RAY_MIN_BLOCKS>(HashView, const uint32_t*, int, const float2*,
+                                                      const FrameParams*, IntrD, float, float, float4*, float4*,
+                                                      unsigned*);
+template __global__ void k_raycast<VF_RAY_MIN_BLOCKS_SMALL>(HashView, const uint32_t*, int, const float2*,
+                                                            const FrameParams*, IntrD, float, float, float4*, float4*,
+                                                            unsigned*);
 
 // K3b second pass: the zero-crossing refinement and the normal of every hit
 // (sdf_surface_normal, the 48-read stencil) with full warps -- in one fused
