@@ -147,7 +147,8 @@ typedef struct vf_frame_stats {
   int tracking_valid_points;
   int allocation_requested;
   int allocated_total; /* HashVolume::allocated_block_count */
-  int error_flags;
+  int error_flags; /* 1 DDA steps, 2 allocated list, 4 request list, 8 host store full, 16 shard exchange
+                      timeout, 32 raycast hand-off timeout */
   double pose[12];
   double ms_tracking, ms_allocation, ms_integration, ms_swapping, ms_raycast, ms_total;
   /* SwapMetrics (swap.hpp:28-40) */
